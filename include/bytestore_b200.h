@@ -1,0 +1,243 @@
+/*
+ * bytestore_b200.h -- C ABI of the B200-native ByteStore scan/lookup hot path.
+ *
+ * This is the drop-in boundary under the reference's Python layout API
+ * (reference: /root/reference/pkg/src/bytestore/, cited below as file:line).
+ * The reference has no FFI of its own: its boundary is the Python surface
+ * re-exported by __init__.py:10-52 and the string-keyed layout dispatch in
+ * engine.py:172-221.  Each entry point below replaces one reference routine;
+ * the ctypes binding a maintainer would add to the reference is shown in
+ * INTEGRATION.md, and the package paper_2209_00220_b200 is that binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ *    (cudaMalloc / torch allocations) unless the name says host.  `stream`
+ *    is a cudaStream_t passed as void*; NULL means the legacy default stream.
+ *  - Buffers are caller-allocated.  Functions never synchronise the stream
+ *    except where documented ("syncs"): a value must come back to the host.
+ *  - Bitvectors: uint32 words, bit i of row space = bit (i % 32) of word
+ *    i / 32, LSB first (reference bitvector.py:1-6).  Words beyond
+ *    ceil(n_rows/32) are never written; tail bits >= n_rows are written 0.
+ *  - Status codes map to the reference's exceptions: BSB_EINVAL/BSB_ERANGE ->
+ *    ValueError, BSB_ENOTFOUND -> LookupError, BSB_EKEY -> KeyError,
+ *    BSB_ECUDA -> RuntimeError (CUDA error; bsb_last_error() has the text).
+ */
+#ifndef BYTESTORE_B200_H
+#define BYTESTORE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSB_LANES 32          /* rows per block / bits per result word        */
+#define BSB_TILE_BLOCKS 32    /* blocks per tile (one warp, lane = block)      */
+#define BSB_TILE_ROWS 1024    /* rows per tile                                  */
+#define BSB_MAX_LEVELS 8      /* slices per code (reference vbs.py:77-78)       */
+#define BSB_MAX_CONJ 8        /* predicates fused by bsb_conj_scan              */
+#define BSB_STATS_WORDS 24    /* int64 counters written by the *_scan stats path */
+
+enum bsb_status {
+  BSB_OK = 0,
+  BSB_EINVAL = 1,     /* bad argument / shape mismatch        -> ValueError   */
+  BSB_ERANGE = 2,     /* value out of range (width, length)   -> ValueError   */
+  BSB_ENOTFOUND = 3,  /* padded code not in dictionary        -> LookupError  */
+  BSB_ECUDA = 4,      /* CUDA runtime error                   -> RuntimeError */
+  BSB_EKEY = 5        /* value missing from dictionary        -> KeyError     */
+};
+
+/* Operators: reference predicate.py:13-38 (Op). */
+enum bsb_op { BSB_EQ = 0, BSB_NE = 1, BSB_LT = 2, BSB_LE = 3, BSB_GT = 4, BSB_GE = 5,
+              BSB_BETWEEN = 6 };
+
+/* Code-space predicate: reference predicate.py:62-95 (ResolvedPredicate).
+ * trivial: -1 = real comparison, 0 = constant false, 1 = constant true.
+ * length/length2 are BYTES (big-endian literal of that many bytes). */
+typedef struct bsb_pred {
+  int32_t op;
+  int32_t trivial;
+  uint64_t code;
+  uint64_t code2;
+  int32_t length;
+  int32_t length2;
+} bsb_pred;
+
+/* Device-resident ByteSlice column (reference byteslice.py:34-49).
+ * slices: n_slices planes of `stride` bytes each.  Inside every 32-row block
+ * the 32 bytes of a plane are stored swizzled: row r of the block lives at
+ * byte ((r & 7) << 2) | (r >> 3), so one
+ * 256-bit load per lane gives SWAR-ready words.  stride is a multiple of
+ * BSB_TILE_ROWS and >= n_rows; padding rows are zero. */
+typedef struct bsb_byteslice {
+  int64_t n_rows;
+  int64_t stride;
+  int32_t width_bits;
+  int32_t n_slices;
+  const uint8_t* slices;
+} bsb_byteslice;
+
+/* Device-resident PP-VBS column (reference vbs.py:42-65).
+ * bs1:        first byte of every row, `stride` bytes, swizzled like ByteSlice.
+ * deep[j]:    slice j+1 (j = 1..max_len-1): bytes of rows whose code has a
+ *             (j+1)-th byte, packed in row order exactly like the reference
+ *             (vbs.py:98-100); allocation padded by >= 64 bytes.
+ * exist[j]:   uint32 existence word per block of slice j+1 (vbs.py:101-104),
+ *             `stride/32` words.
+ * block_dir[j]: int64[stride/32 + 1]: bytes of slice j+1 before block b
+ *             (vbs.py:105-106).
+ * Index 0 of deep/exist/block_dir is unused (level 1 is bs1). */
+typedef struct bsb_vbs {
+  int64_t n_rows;
+  int64_t stride;
+  int32_t max_len;
+  int32_t reserved;
+  const uint8_t* bs1;
+  const uint8_t* deep[BSB_MAX_LEVELS];
+  const uint32_t* exist[BSB_MAX_LEVELS];
+  const int64_t* block_dir[BSB_MAX_LEVELS];
+  int64_t deep_len[BSB_MAX_LEVELS];
+} bsb_vbs;
+
+/* One column reference for the fused conjunction (engine.py:322-332). */
+enum bsb_layout { BSB_LAYOUT_BYTESLICE = 0, BSB_LAYOUT_PPVBS = 1 };
+typedef struct bsb_column_ref {
+  int32_t layout;
+  int32_t reserved;
+  const bsb_byteslice* byteslice;  /* host pointers to the descriptors */
+  const bsb_vbs* vbs;
+} bsb_column_ref;
+
+/* ----------------------------------------------------------------- misc */
+const char* bsb_version(void);
+const char* bsb_last_error(void);
+/* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */
+int64_t bsb_stride_for(int64_t n_rows);
+
+/* ------------------------------------------------------------ ByteSlice */
+/* build_byteslice (byteslice.py:56-73): codes uint64[n_rows] -> swizzled,
+ * left-aligned planes into slices[n_slices * stride] (caller-allocated,
+ * n_slices = ceil(width_bits/8)).  Validates 1 <= width_bits <= 64 and
+ * codes < 2^width (BSB_ERANGE; syncs to read the device check). */
+int bsb_byteslice_build(const uint64_t* codes, int64_t n_rows, int32_t width_bits,
+                        uint8_t* slices, int64_t stride, void* stream);
+/* Same, from int64 ranks (Dictionary.encode_rows output, dictionary.py:381-397). */
+int bsb_byteslice_build_ranks(const int64_t* ranks, int64_t n_rows, int32_t width_bits,
+                              uint8_t* slices, int64_t stride, void* stream);
+/* Reference (unswizzled) planes, uint8[n_slices][ceil(n/32)*32] -- parity helper. */
+int bsb_byteslice_export(const bsb_byteslice* col, uint8_t* out, void* stream);
+
+/* scan_byteslice (byteslice.py:109-140).  mask may be NULL (no input
+ * bitvector).  out_words: ceil(n/32) words.  count: one uint64, overwritten.
+ * stats/depth may be NULL; when given, BETWEEN runs as two pipelined legs and
+ * stats (BSB_STATS_WORDS int64, see bsb_stats_layout) / depth (int8 per
+ * block) reproduce the reference ScanStats exactly (stats.py:18-84). */
+int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred, const uint32_t* mask,
+                       uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                       void* stream);
+
+/* lookup_byteslice (byteslice.py:143-158) for a row-id list (any order,
+ * duplicates allowed; output in input order).  Writes right-aligned codes to
+ * out_codes (may be NULL) and, when rank_values (int64[dict size]) is given,
+ * decoded values values[code] (dictionary.py:413-414) to out_values (int64,
+ * may be NULL) and/or out_values32 (int32, may be NULL). */
+int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t* rows, int64_t n_ids,
+                              uint64_t* out_codes, const int64_t* rank_values,
+                              int64_t* out_values, int32_t* out_values32, void* stream);
+
+/* ----------------------------------------------------------------- PP-VBS */
+/* build_vbs, pass 1 (vbs.py:68-82): validate lengths 1..8 and code widths,
+ * return max_len and, per level j (1-based), the number of rows whose code
+ * has a j-th byte: level_rows[j-1].  Syncs. */
+int bsb_vbs_plan(const uint64_t* codes, const uint8_t* lens, int64_t n_rows,
+                 int32_t* max_len_host, int64_t* level_rows_host, void* stream);
+/* build_vbs, pass 2 (vbs.py:84-114): fills a descriptor whose arrays the
+ * caller allocated from the plan (deep[j] >= level_rows[j] + 64 bytes). */
+int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const bsb_vbs* col,
+                  void* stream);
+/* Reference (unswizzled) first slice, uint8[ceil(n/32)*32] -- parity helper. */
+int bsb_vbs_export_bs1(const bsb_vbs* col, uint8_t* out, void* stream);
+
+/* scan_vbs (vbs.py:292-324): Alg. 3 with the existence shortcut.  Same
+ * argument contract as bsb_byteslice_scan.  A literal longer than max_len
+ * is BSB_ERANGE (the reference raises IndexError at vbs.py:274). */
+int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
+                 uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                 void* stream);
+
+/* lookup_vbs (vbs.py:331-371) for a row-id list: padded codes
+ * code << 8*(max_len - len) to out_padded (may be NULL); when sorted_padded
+ * (uint64[n_dict], strictly increasing: ordered dictionaries, dictionary.py:
+ * 370-373) and dict_values (int64[n_dict]) are given, also decode_padded
+ * (dictionary.py:403-411) into out_values / out_values32 (either may be
+ * NULL).  A code absent from the dictionary sets BSB_ENOTFOUND (syncs only
+ * when decoding).  level_counts (uint64[BSB_MAX_LEVELS], may be NULL) is
+ * overwritten with the number of looked-up rows owning a byte at each level
+ * (LookupStats accounting, vbs.py:346-370). */
+int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
+                        uint64_t* out_padded, const uint64_t* sorted_padded,
+                        const int64_t* dict_values, int64_t n_dict, int64_t* out_values,
+                        int32_t* out_values32, uint64_t* level_counts, void* stream);
+
+/* ------------------------------------------------------------ bitvectors */
+/* ResultBitVector.to_indices (bitvector.py:71-72): ascending int64 row ids of
+ * the set bits into rows_out (capacity >= popcount); count written to
+ * *n_out_host.  Syncs. */
+int bsb_bits_to_rows(const uint32_t* words, int64_t n_rows, int64_t* rows_out,
+                     int64_t* n_out_host, void* stream);
+/* Same but with a row offset added (sharded global ids) and no sync: the
+ * count is written to the device scalar n_out_dev. */
+int bsb_bits_to_rows_async(const uint32_t* words, int64_t n_rows, int64_t row_offset,
+                           int64_t* rows_out, uint64_t* n_out_dev, void* stream);
+/* & | ~ and popcount (bitvector.py:84-125).  op: 0 = and, 1 = or, 2 = not
+ * (b ignored), 3 = andnot (a & ~b).  Tail bits cleared. */
+int bsb_bits_combine(int32_t op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                     int64_t n_rows, void* stream);
+int bsb_bits_popcount(const uint32_t* words, int64_t n_rows, uint64_t* count, void* stream);
+
+/* --------------------------------------------------- fused conjunction */
+/* engine.execute's pipelined conjunction (engine.py:322-332) in one pass:
+ * predicate i sees the running result of predicates 0..i-1 as its input
+ * mask; blocks already zero skip every later predicate's slices.  Columns
+ * must share n_rows.  k <= BSB_MAX_CONJ. */
+int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
+                  const uint32_t* mask, uint32_t* out_words, uint64_t* count, void* stream);
+
+/* --------------------------------------------------------------- encoders */
+/* build_frequency_table for numeric columns (dictionary.py:101-106) plus
+ * encode_rows (dictionary.py:381-397) in one device sort:
+ * values int64[n] -> distinct sorted values + counts (capacity n) and the
+ * rank of every row.  *n_distinct_host receives the distinct count.  Syncs. */
+int bsb_freq_table(const int64_t* values, int64_t n, int64_t* uniq_out, int64_t* counts_out,
+                   int64_t* ranks_out, int64_t* n_distinct_host, void* stream);
+/* Dictionary.encode_rows against an existing sorted table (binary search);
+ * a value absent from the table -> BSB_EKEY (syncs). */
+int bsb_encode_rows(const int64_t* values, int64_t n, const int64_t* table_values,
+                    int64_t n_dict, int64_t* ranks_out, void* stream);
+/* ppe_numerical (dictionary.py:148-196), HOST arrays: weights int64[n] ->
+ * codes uint64[n], lengths uint8[n].  Stable top-255 tie-break. */
+int bsb_ppe_numerical_host(const int64_t* weights_host, int64_t n, uint64_t* codes_host,
+                           uint8_t* lengths_host);
+/* Dictionary.row_codes (dictionary.py:399-401): gather per-row codes/lengths. */
+int bsb_gather_codes(const int64_t* ranks, int64_t n, const uint64_t* dict_codes,
+                     const uint8_t* dict_lens, uint64_t* codes_out, uint8_t* lens_out,
+                     void* stream);
+/* gen_zipf's inverse-CDF step (datagen.py:50-56): searchsorted(cdf, u,
+ * side="right") for float64 uniforms u[n] over cdf[domain]. */
+int bsb_zipf_from_uniform(const double* u, int64_t n, const double* cdf, int64_t domain,
+                          int64_t* values_out, void* stream);
+
+/* Layout of the stats buffer (int64):
+ *   [0..7]   words_loaded per level     [8..15] bytes_loaded per level
+ *   [16]     blocks_total               [17]    blocks_skipped
+ *   [18]     levels (column K)          [19..23] reserved
+ * mask_bytes is derived on the host: live_blocks * 4 * (min(len+1, K) - 1)
+ * (vbs.py:286-287). */
+void bsb_stats_layout(int32_t* words_off, int32_t* bytes_off, int32_t* total_off,
+                      int32_t* skipped_off, int32_t* levels_off);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BYTESTORE_B200_H */

@@ -1,0 +1,438 @@
+// bsb_scan.cu -- scan kernels (ByteSlice, PP-VBS, fused conjunction) and
+// their C-ABI launchers.  Kernel bodies live in bsb_scan_impl.cuh.
+#include <cstring>
+
+#include "bsb_scan_impl.cuh"
+
+namespace bsb {
+
+constexpr int kScanThreads = 256;
+
+struct ScanArgs {
+  int64_t n_rows;
+  int64_t nb;
+  int64_t ntiles;
+  BsDesc bs;
+  VbsDesc vbs;
+  Leg A, B;
+  const uint32_t* mask;
+  uint32_t* out;
+  unsigned long long* count;
+  int64_t* stats;
+  int8_t* depth;
+  int32_t skipped_slot;
+  int32_t depth_max;  // STATS: 1 = depth[b] = max(depth[b], d) (second BETWEEN leg)
+};
+
+template <bool STATS>
+__device__ __forceinline__ void flush_stats(const ScanArgs& a, StatAcc& st) {
+  if (!STATS) return;
+#pragma unroll
+  for (int j = 0; j < kMaxLevels; ++j) {
+    long long w = st.words[j], by = st.bytes[j];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      w += __shfl_xor_sync(kFull, w, d);
+      by += __shfl_xor_sync(kFull, by, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (w) atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + j), (unsigned long long)w);
+      if (by)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 8 + j),
+                  (unsigned long long)by);
+    }
+  }
+  long long s = st.skipped;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
+  if ((threadIdx.x & 31) == 0 && s)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + a.skipped_slot),
+              (unsigned long long)s);
+}
+
+template <int LAYOUT, bool BETWEEN, bool STATS>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(const __grid_constant__ ScanArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cnt = 0;
+  StatAcc st;
+  if (STATS) {
+#pragma unroll
+    for (int j = 0; j < kMaxLevels; ++j) st.words[j] = st.bytes[j] = 0;
+    st.skipped = 0;
+  }
+  for (int64_t tile = warp; tile < a.ntiles; tile += nwarps) {
+    const int64_t b = tile * 32 + lane;
+    const bool inb = b < a.nb;
+    uint32_t valid = tail_valid(b, a.n_rows);
+    if (a.mask != nullptr && inb) valid &= __ldg(a.mask + b);
+    if (STATS && inb && valid == 0) st.skipped += 1;
+    int depth = 0;
+    uint32_t res;
+    if (LAYOUT == BSB_LAYOUT_BYTESLICE)
+      res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, &st, &depth);
+    else
+      res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, &st, &depth);
+    if (inb) {
+      a.out[b] = res;
+      if (STATS && a.depth != nullptr) {
+        if (a.depth_max) {
+          const int8_t old = a.depth[b];
+          a.depth[b] = (int8_t)(depth > old ? depth : old);
+        } else {
+          a.depth[b] = (int8_t)depth;
+        }
+      }
+    }
+    cnt += __popc(res);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+  flush_stats<STATS>(a, st);
+}
+
+// Trivial predicates (vbs.py:200-208): true -> mask & valid, false -> 0.
+__global__ void trivial_kernel(int64_t n_rows, int64_t nb, const uint32_t* mask, int value,
+                               uint32_t* out, unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    if (value) {
+      v = tail_valid(b, n_rows);
+      if (mask) v &= mask[b];
+    }
+    out[b] = v;
+    c += __popc(v);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// ------------------------------------------------------------ host helpers
+
+static void fill_leg(Leg& L, int op, uint64_t code, int len, int levels) {
+  std::memset(&L, 0, sizeof(L));
+  L.op = op;
+  L.len = len;
+  for (int j = 0; j < kMaxLevels; ++j) {
+    uint32_t byte = 0;
+    if (j < levels) byte = (uint32_t)((code >> (8 * (levels - 1 - j))) & 0xFF);
+    L.byte[j] = byte;
+    L.lv[j] = make_level_lit(byte);
+  }
+}
+
+// ByteSlice literal: left-aligned like the codes, pred.length ignored
+// (byteslice.py:81).
+static void bs_leg(Leg& L, int op, uint64_t code, int width_bits, int K) {
+  const int shift = 8 * K - width_bits;
+  const uint64_t aligned = shift >= 64 ? 0 : (code << shift);
+  fill_leg(L, op, aligned, K, K);
+}
+
+static bool pred_ok(const bsb_pred* p) {
+  if (!p) return false;
+  if (p->trivial >= 0) return true;
+  return p->op >= BSB_EQ && p->op <= BSB_BETWEEN;
+}
+
+template <typename KernelT>
+static int launch_scan(KernelT kern, const ScanArgs& a, cudaStream_t s) {
+  const int grid = persistent_grid(kern, kScanThreads, kScanThreads / 32, a.ntiles);
+  kern<<<grid, kScanThreads, 0, s>>>(a);
+  BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}
+
+static int run_trivial(int64_t n, const bsb_pred* p, const uint32_t* mask, uint32_t* out,
+                       uint64_t* count, int64_t* stats, int8_t* depth, int levels,
+                       cudaStream_t s) {
+  const int64_t nb = (n + 31) / 32;
+  BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
+  int grid = (int)((nb + 255) / 256);
+  if (grid > 4096) grid = 4096;
+  if (grid < 1) grid = 1;
+  trivial_kernel<<<grid, 256, 0, s>>>(n, nb, mask, p->trivial, out,
+                                      reinterpret_cast<unsigned long long*>(count));
+  BSB_LAUNCH_CHECK();
+  if (stats) {
+    int64_t h[BSB_STATS_WORDS] = {0};
+    h[16] = nb;
+    h[17] = nb;  // every block counts as skipped (vbs.py:203-204)
+    h[18] = levels;
+    h[19] = nb;
+    BSB_CUDA(cudaMemcpyAsync(stats, h, sizeof(h), cudaMemcpyHostToDevice, s));
+    BSB_CUDA(cudaStreamSynchronize(s));  // h is a stack buffer
+  }
+  if (depth) BSB_CUDA(cudaMemsetAsync(depth, 0, nb, s));
+  return BSB_OK;
+}
+
+template <int LAYOUT>
+static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_t s) {
+  const bool between = p->op == BSB_BETWEEN;
+  const bool stats = a.stats != nullptr;
+  BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
+  if (!stats) {
+    if (between) return launch_scan(scan_kernel<LAYOUT, true, false>, a, s);
+    return launch_scan(scan_kernel<LAYOUT, false, false>, a, s);
+  }
+  // Stats path: reproduce the reference's two pipelined legs exactly
+  // (vbs.py:299-304, stats.py:47-67).
+  int64_t h[BSB_STATS_WORDS] = {0};
+  h[16] = a.nb;
+  h[18] = levels;
+  BSB_CUDA(cudaMemcpyAsync(a.stats, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  if (!between) {
+    a.skipped_slot = 17;
+    a.depth_max = 0;
+    int rc = launch_scan(scan_kernel<LAYOUT, false, true>, a, s);
+    BSB_CUDA(cudaStreamSynchronize(s));
+    return rc;
+  }
+  uint32_t* tmp = nullptr;
+  BSB_CUDA(cudaMallocAsync(&tmp, (size_t)a.nb * 4 + 4, s));
+  ScanArgs leg1 = a;
+  leg1.B = a.B;
+  leg1.out = tmp;
+  leg1.skipped_slot = 17;
+  leg1.depth_max = 0;
+  // leg 1: GE(lo) over the caller's mask; leg 2: LE(hi) over leg 1's result
+  leg1.A.op = BSB_GE;
+  unsigned long long* dummy = nullptr;
+  BSB_CUDA(cudaMallocAsync(&dummy, 8, s));
+  BSB_CUDA(cudaMemsetAsync(dummy, 0, 8, s));
+  leg1.count = dummy;
+  int rc = launch_scan(scan_kernel<LAYOUT, false, true>, leg1, s);
+  if (rc) return rc;
+  ScanArgs leg2 = a;
+  leg2.A = a.B;
+  leg2.A.op = BSB_LE;
+  leg2.mask = tmp;
+  leg2.skipped_slot = 19;
+  leg2.depth_max = 1;
+  rc = launch_scan(scan_kernel<LAYOUT, false, true>, leg2, s);
+  if (rc) return rc;
+  BSB_CUDA(cudaFreeAsync(tmp, s));
+  BSB_CUDA(cudaFreeAsync(dummy, s));
+  BSB_CUDA(cudaStreamSynchronize(s));
+  return BSB_OK;
+}
+
+}  // namespace bsb
+
+using namespace bsb;
+
+extern "C" int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred,
+                                  const uint32_t* mask, uint32_t* out_words, uint64_t* count,
+                                  int64_t* stats, int8_t* depth, void* stream) {
+  if (!col || !pred_ok(pred) || !out_words || !count || col->n_rows <= 0) return BSB_EINVAL;
+  if (col->n_slices < 1 || col->n_slices > kMaxLevels) return BSB_ERANGE;
+  cudaStream_t s = as_stream(stream);
+  if (pred->trivial >= 0)
+    return run_trivial(col->n_rows, pred, mask, out_words, count, stats, depth, col->n_slices,
+                       s);
+  ScanArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_rows = col->n_rows;
+  a.nb = (col->n_rows + 31) / 32;
+  a.ntiles = (a.nb + 31) / 32;
+  a.bs.slices = col->slices;
+  a.bs.stride = col->stride;
+  a.bs.K = col->n_slices;
+  const int K = col->n_slices;
+  if (pred->op == BSB_BETWEEN) {
+    bs_leg(a.A, BSB_GE, pred->code, col->width_bits, K);
+    bs_leg(a.B, BSB_LE, pred->code2, col->width_bits, K);
+  } else {
+    bs_leg(a.A, pred->op, pred->code, col->width_bits, K);
+    a.B = a.A;
+  }
+  a.mask = mask;
+  a.out = out_words;
+  a.count = reinterpret_cast<unsigned long long*>(count);
+  a.stats = stats;
+  a.depth = depth;
+  return scan_dispatch<BSB_LAYOUT_BYTESLICE>(a, pred, K, s);
+}
+
+static void fill_vbs_desc(VbsDesc& d, const bsb_vbs* col) {
+  std::memset(&d, 0, sizeof(d));
+  d.bs1 = col->bs1;
+  d.K = col->max_len;
+  for (int j = 0; j < kMaxLevels; ++j) {
+    d.deep[j] = col->deep[j];
+    d.exist[j] = col->exist[j];
+    d.dir[j] = col->block_dir[j];
+  }
+}
+
+extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
+                            uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                            void* stream) {
+  if (!col || !pred_ok(pred) || !out_words || !count || col->n_rows <= 0) return BSB_EINVAL;
+  if (col->max_len < 1 || col->max_len > kMaxLevels) return BSB_ERANGE;
+  cudaStream_t s = as_stream(stream);
+  const int K = col->max_len;
+  if (pred->trivial >= 0)
+    return run_trivial(col->n_rows, pred, mask, out_words, count, stats, depth, K, s);
+  ScanArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_rows = col->n_rows;
+  a.nb = (col->n_rows + 31) / 32;
+  a.ntiles = (a.nb + 31) / 32;
+  fill_vbs_desc(a.vbs, col);
+  auto bad_len = [&](int l) { return l < 1 || l > K; };
+  if (pred->op == BSB_BETWEEN) {
+    if (bad_len(pred->length) || bad_len(pred->length2)) return BSB_ERANGE;
+    fill_leg(a.A, BSB_GE, pred->code, pred->length, pred->length);
+    fill_leg(a.B, BSB_LE, pred->code2, pred->length2, pred->length2);
+  } else {
+    if (bad_len(pred->length)) return BSB_ERANGE;
+    fill_leg(a.A, pred->op, pred->code, pred->length, pred->length);
+    a.B = a.A;
+  }
+  a.mask = mask;
+  a.out = out_words;
+  a.count = reinterpret_cast<unsigned long long*>(count);
+  a.stats = stats;
+  a.depth = depth;
+  return scan_dispatch<BSB_LAYOUT_PPVBS>(a, pred, K, s);
+}
+
+// ------------------------------------------------------ fused conjunction
+
+namespace bsb {
+
+struct ConjItem {
+  int32_t layout;
+  int32_t between;
+  BsDesc bs;
+  VbsDesc vbs;
+  Leg A, B;
+};
+struct ConjArgs {
+  int64_t n_rows, nb, ntiles;
+  int32_t k;
+  ConjItem item[BSB_MAX_CONJ];
+  const uint32_t* mask;
+  uint32_t* out;
+  unsigned long long* count;
+};
+
+__global__ void __launch_bounds__(kScanThreads) conj_kernel(const __grid_constant__ ConjArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cnt = 0;
+  for (int64_t tile = warp; tile < a.ntiles; tile += nwarps) {
+    const int64_t b = tile * 32 + lane;
+    const bool inb = b < a.nb;
+    uint32_t z = tail_valid(b, a.n_rows);
+    if (a.mask != nullptr && inb) z &= __ldg(a.mask + b);
+    for (int i = 0; i < a.k; ++i) {
+      if (!__any_sync(kFull, z != 0)) break;  // whole tile already ruled out
+      const ConjItem& it = a.item[i];
+      if (it.layout == BSB_LAYOUT_BYTESLICE) {
+        z = it.between ? scan_tile_bs<true, false>(it.bs, it.A, it.B, b, z, nullptr, nullptr)
+                       : scan_tile_bs<false, false>(it.bs, it.A, it.B, b, z, nullptr, nullptr);
+      } else {
+        z = it.between
+                ? scan_tile_vbs<true, false>(it.vbs, it.A, it.B, tile, b, z, nullptr, nullptr)
+                : scan_tile_vbs<false, false>(it.vbs, it.A, it.B, tile, b, z, nullptr, nullptr);
+      }
+    }
+    if (inb) a.out[b] = z;
+    cnt += __popc(z);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
+}  // namespace bsb
+
+extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
+                             const uint32_t* mask, uint32_t* out_words, uint64_t* count,
+                             void* stream) {
+  if (k < 0 || k > BSB_MAX_CONJ || (k > 0 && (!cols || !preds)) || !out_words || !count)
+    return BSB_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  ConjArgs a;
+  std::memset(&a, 0, sizeof(a));
+  int64_t n = -1;
+  bool all_false = false;
+  int m = 0;
+  for (int i = 0; i < k; ++i) {
+    const bsb_column_ref& c = cols[i];
+    const bsb_pred* p = &preds[i];
+    if (!pred_ok(p)) return BSB_EINVAL;
+    int64_t ni;
+    if (c.layout == BSB_LAYOUT_BYTESLICE) {
+      if (!c.byteslice) return BSB_EINVAL;
+      ni = c.byteslice->n_rows;
+    } else if (c.layout == BSB_LAYOUT_PPVBS) {
+      if (!c.vbs) return BSB_EINVAL;
+      ni = c.vbs->n_rows;
+    } else {
+      return BSB_EINVAL;
+    }
+    if (n >= 0 && ni != n) return BSB_EINVAL;
+    n = ni;
+    if (p->trivial == 0) all_false = true;
+    if (p->trivial >= 0) continue;  // constant true: no-op in a conjunction
+    ConjItem& it = a.item[m++];
+    it.layout = c.layout;
+    it.between = p->op == BSB_BETWEEN;
+    if (c.layout == BSB_LAYOUT_BYTESLICE) {
+      const bsb_byteslice* col = c.byteslice;
+      it.bs.slices = col->slices;
+      it.bs.stride = col->stride;
+      it.bs.K = col->n_slices;
+      if (it.between) {
+        bs_leg(it.A, BSB_GE, p->code, col->width_bits, col->n_slices);
+        bs_leg(it.B, BSB_LE, p->code2, col->width_bits, col->n_slices);
+      } else {
+        bs_leg(it.A, p->op, p->code, col->width_bits, col->n_slices);
+        it.B = it.A;
+      }
+    } else {
+      const bsb_vbs* col = c.vbs;
+      const int K = col->max_len;
+      fill_vbs_desc(it.vbs, col);
+      auto bad = [&](int l) { return l < 1 || l > K; };
+      if (it.between) {
+        if (bad(p->length) || bad(p->length2)) return BSB_ERANGE;
+        fill_leg(it.A, BSB_GE, p->code, p->length, p->length);
+        fill_leg(it.B, BSB_LE, p->code2, p->length2, p->length2);
+      } else {
+        if (bad(p->length)) return BSB_ERANGE;
+        fill_leg(it.A, p->op, p->code, p->length, p->length);
+        it.B = it.A;
+      }
+    }
+  }
+  if (n < 0) return BSB_EINVAL;  // need at least one column to know n_rows
+  a.n_rows = n;
+  a.nb = (n + 31) / 32;
+  a.ntiles = (a.nb + 31) / 32;
+  a.k = all_false ? 0 : m;
+  a.mask = mask;
+  a.out = out_words;
+  a.count = reinterpret_cast<unsigned long long*>(count);
+  BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
+  if (all_false) {
+    bsb_pred f;
+    std::memset(&f, 0, sizeof(f));
+    f.trivial = 0;
+    return run_trivial(n, &f, mask, out_words, count, nullptr, nullptr, 0, s);
+  }
+  const int grid = persistent_grid(conj_kernel, kScanThreads, kScanThreads / 32, a.ntiles);
+  conj_kernel<<<grid, kScanThreads, 0, s>>>(a);
+  BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}

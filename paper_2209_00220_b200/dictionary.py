@@ -1,0 +1,333 @@
+"""Dictionary encoders (mirror of reference dictionary.py, numeric columns).
+
+Device work: the frequency table + row ranks come from one radix sort on the
+GPU (bsb_freq_table); encode_rows is a device binary search; row codes are a
+device gather.  Host work (O(distinct)): ppe_numerical in C++
+(bsb_ppe_numerical_host), literal resolution (scalar searchsorted) and the
+decode tables handed to the lookup kernels.
+
+Scope: numeric (integer) columns, i.e. the ordered kinds the north-star
+configs use.  Categorical / string dictionaries (ppe_categorical, prefix-free
+codes) are out of scope for the device path and raise ValueError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import device, stream, to_dev_i64
+from .predicate import Op, Predicate, ResolvedPredicate
+
+__all__ = ["ColumnKind", "FrequencyTable", "build_frequency_table", "CodeAssignment",
+           "ppe_numerical", "fixed_assignment", "Dictionary", "compare_codes",
+           "freq_table_and_ranks"]
+
+MAX_CODE_BYTES = 8
+MAX_FIXED_BITS = 32
+
+
+class ColumnKind(enum.Enum):
+    NUMERIC = "numeric"
+    CATEGORICAL = "categorical"
+    ORDERED_STRING = "ordered_string"
+
+    @property
+    def ordered(self) -> bool:
+        return self is not ColumnKind.CATEGORICAL
+
+
+def _require_numeric(kind: ColumnKind):
+    if kind is not ColumnKind.NUMERIC:
+        raise ValueError(f"{kind.value} columns are outside the device path "
+                         "(numeric columns only; see DESIGN.md scope)")
+
+
+@dataclass(frozen=True)
+class FrequencyTable:
+    """Distinct values (ascending) and their counts (dictionary.py:57-82)."""
+
+    values: np.ndarray
+    weights: np.ndarray
+    kind: ColumnKind
+
+    def __post_init__(self):
+        if len(self.values) == 0:
+            raise ValueError("empty column")
+        if len(self.values) != len(self.weights):
+            raise ValueError("values and weights differ in length")
+
+    @property
+    def n(self) -> int:
+        return len(self.values)
+
+
+def _values_tensor(values) -> torch.Tensor:
+    if isinstance(values, torch.Tensor):
+        if values.dtype.is_floating_point or values.dtype == torch.bool:
+            raise ValueError("numeric column holds a non-integer")
+        if values.ndim != 1 or values.numel() == 0:
+            raise ValueError("column must be a nonempty 1-d sequence")
+        return to_dev_i64(values)
+    arr = np.asarray(values)
+    if arr.ndim != 1 or arr.size == 0:
+        raise ValueError("column must be a nonempty 1-d sequence")
+    if arr.dtype.kind not in "iu":
+        if arr.dtype == object and all(isinstance(v, (int, np.integer)) and
+                                       not isinstance(v, bool) for v in arr):
+            arr = arr.astype(np.int64)
+        else:
+            raise ValueError("numeric column holds a non-integer")
+    return to_dev_i64(arr.astype(np.int64))
+
+
+def freq_table_and_ranks(values):
+    """Device sort -> (sorted distinct values, counts, per-row ranks) tensors.
+
+    One pass gives build_frequency_table (dictionary.py:101-106) and
+    encode_rows (dictionary.py:381-397) for the same column.
+    """
+    v = _values_tensor(values)
+    n = v.numel()
+    lib = _lib.load()
+    uniq = torch.empty(n, dtype=torch.int64, device=v.device)
+    cnts = torch.empty(n, dtype=torch.int64, device=v.device)
+    ranks = torch.empty(n, dtype=torch.int64, device=v.device)
+    D = ctypes.c_int64(0)
+    _lib.check(lib.bsb_freq_table(v.data_ptr(), n, uniq.data_ptr(), cnts.data_ptr(),
+                                  ranks.data_ptr(), ctypes.byref(D), stream()), "freq_table")
+    D = int(D.value)
+    return uniq[:D], cnts[:D], ranks
+
+
+def build_frequency_table(values, kind: ColumnKind) -> FrequencyTable:
+    """dictionary.py:101-109 for numeric columns (device radix sort)."""
+    _require_numeric(kind)
+    u, c, _ = freq_table_and_ranks(values)
+    return FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), kind)
+
+
+@dataclass(frozen=True)
+class CodeAssignment:
+    """dictionary.py:115-140."""
+
+    codes: np.ndarray
+    lengths: np.ndarray
+    scheme: str
+    width_bits: int = 0
+
+    @property
+    def n(self) -> int:
+        return len(self.codes)
+
+    @property
+    def max_len(self) -> int:
+        return int(self.lengths.max())
+
+    @property
+    def bit_granular(self) -> bool:
+        return self.scheme == "prefix_free"
+
+
+def ppe_numerical(weights) -> CodeAssignment:
+    """Alg. 1 (dictionary.py:148-196), native host implementation."""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.int64))
+    n = len(w)
+    if n == 0:
+        raise ValueError("empty weight table")
+    if (w < 0).any():
+        raise ValueError("negative weight")
+    codes = np.zeros(n, np.uint64)
+    lens = np.zeros(n, np.uint8)
+    _lib.check(_lib.load().bsb_ppe_numerical_host(w.ctypes.data, n, codes.ctypes.data,
+                                                  lens.ctypes.data), "ppe_numerical")
+    return CodeAssignment(codes, lens, "ppe_numerical")
+
+
+def fixed_assignment(n: int) -> CodeAssignment:
+    """Rank codes at w = max(1, ceil(log2 n)) bits (dictionary.py:233-242)."""
+    if n <= 0:
+        raise ValueError("need at least one value")
+    width = max(1, (n - 1).bit_length())
+    if width > MAX_FIXED_BITS:
+        raise ValueError("dictionary width overflow (more than 2**32 values)")
+    return CodeAssignment(np.arange(n, dtype=np.uint64),
+                          np.full(n, (width + 7) // 8, np.uint8), "fixed", width_bits=width)
+
+
+def compare_codes(code1: int, len1: int, code2: int, len2: int):
+    """Lemma 1 comparator (dictionary.py:293-309): (sign, bytes examined)."""
+    m = min(len1, len2)
+    for k in range(1, m + 1):
+        a = (code1 >> (8 * (len1 - k))) & 0xFF
+        b = (code2 >> (8 * (len2 - k))) & 0xFF
+        if a != b:
+            return (1 if a > b else -1), k
+    if len1 == len2:
+        return 0, m
+    return (1 if len1 > len2 else -1), m
+
+
+class Dictionary:
+    """Value table plus one code assignment (dictionary.py:316-485)."""
+
+    def __init__(self, table: FrequencyTable, assignment: CodeAssignment):
+        if assignment.n != table.n:
+            raise ValueError("assignment size does not match table")
+        self.table = table
+        self.assignment = assignment
+
+    @classmethod
+    def build(cls, table: FrequencyTable, scheme: str) -> "Dictionary":
+        _require_numeric(table.kind)
+        if scheme == "fixed":
+            return cls(table, fixed_assignment(table.n))
+        if scheme == "prefix_preserving":
+            a = ppe_numerical(table.weights)
+            if a.max_len > MAX_CODE_BYTES:
+                raise ValueError("code length overflow")
+            return cls(table, a)
+        if scheme == "prefix_free":
+            raise ValueError("prefix_free (PE-VBP) dictionaries are outside the device path")
+        raise ValueError(f"unknown scheme {scheme!r}")
+
+    @property
+    def kind(self) -> ColumnKind:
+        return self.table.kind
+
+    @property
+    def n(self) -> int:
+        return self.table.n
+
+    @property
+    def max_len(self) -> int:
+        return self.assignment.max_len
+
+    @cached_property
+    def padded(self) -> np.ndarray:
+        """code << 8*(K - len) (dictionary.py:360-368)."""
+        a = self.assignment
+        shift = np.uint64(8) * (np.uint64(a.max_len) - a.lengths.astype(np.uint64))
+        return a.codes << shift
+
+    @cached_property
+    def _padded_order(self):
+        order = np.argsort(self.padded, kind="stable")
+        return self.padded[order], order
+
+    # device-side tables ------------------------------------------------
+    @cached_property
+    def dev_values(self) -> torch.Tensor:
+        return to_dev_i64(self.table.values)
+
+    @cached_property
+    def dev_decode(self):
+        """(sorted padded codes, values in that order) for lookup decode."""
+        srt, order = self._padded_order
+        return (torch.from_numpy(srt.view(np.int64)).to(device()),
+                to_dev_i64(self.table.values[order]))
+
+    @cached_property
+    def dev_codes(self):
+        a = self.assignment
+        return (torch.from_numpy(a.codes.view(np.int64)).to(device()),
+                torch.from_numpy(a.lengths).to(device()))
+
+    # row encoding / decoding -------------------------------------------
+    def encode_rows_device(self, values) -> torch.Tensor:
+        v = _values_tensor(values)
+        ranks = torch.empty_like(v)
+        _lib.check(_lib.load().bsb_encode_rows(v.data_ptr(), v.numel(),
+                                               self.dev_values.data_ptr(), self.n,
+                                               ranks.data_ptr(), stream()), "encode_rows")
+        return ranks
+
+    def encode_rows(self, values) -> np.ndarray:
+        """dictionary.py:381-397: ranks of raw values (KeyError if absent)."""
+        try:
+            return self.encode_rows_device(values).cpu().numpy()
+        except KeyError:
+            raise KeyError("value missing from dictionary") from None
+
+    def row_codes_device(self, ranks):
+        r = to_dev_i64(ranks)
+        codes = torch.empty_like(r)
+        lens = torch.empty(r.numel(), dtype=torch.uint8, device=r.device)
+        dc, dl = self.dev_codes
+        _lib.check(_lib.load().bsb_gather_codes(r.data_ptr(), r.numel(), dc.data_ptr(),
+                                                dl.data_ptr(), codes.data_ptr(),
+                                                lens.data_ptr(), stream()), "row_codes")
+        return codes, lens
+
+    def row_codes(self, ranks):
+        """dictionary.py:399-401."""
+        r = np.asarray(ranks, dtype=np.int64)
+        return self.assignment.codes[r], self.assignment.lengths[r]
+
+    def decode_padded(self, padded_codes) -> np.ndarray:
+        """dictionary.py:403-411 (host); the device decode is fused into lookups."""
+        q = np.asarray(padded_codes, dtype=np.uint64)
+        srt, order = self._padded_order
+        pos = np.searchsorted(srt, q)
+        hit = (pos < self.n) & (srt[np.minimum(pos, self.n - 1)] == q)
+        if not hit.all():
+            raise LookupError("padded code not in dictionary")
+        return self.table.values[order[pos]]
+
+    def decode_ranks(self, ranks) -> np.ndarray:
+        return self.table.values[np.asarray(ranks, dtype=np.int64)]
+
+    # literal resolution (dictionary.py:418-485) -------------------------
+    def _literal_value(self, value) -> int:
+        if isinstance(value, bool) or not isinstance(value, (int, np.integer)):
+            raise TypeError("numeric column needs an integer literal")
+        return int(value)
+
+    def _code_at(self, rank: int):
+        return int(self.assignment.codes[rank]), int(self.assignment.lengths[rank])
+
+    def _resolve_one(self, op: Op, value) -> ResolvedPredicate:
+        v = self._literal_value(value)
+        vals = self.table.values
+        n = self.n
+        if op in (Op.EQ, Op.NE):
+            i = int(np.searchsorted(vals, v))
+            if i < n and int(vals[i]) == v:
+                return ResolvedPredicate.compare(op, *self._code_at(i))
+            return ResolvedPredicate.constant(op is Op.NE)
+        if op in (Op.LT, Op.LE):
+            cut = int(np.searchsorted(vals, v, side="left" if op is Op.LT else "right"))
+            if cut == 0:
+                return ResolvedPredicate.constant(False)
+            if cut == n:
+                return ResolvedPredicate.constant(True)
+            return ResolvedPredicate.compare(Op.LE, *self._code_at(cut - 1))
+        if op in (Op.GT, Op.GE):
+            cut = int(np.searchsorted(vals, v, side="right" if op is Op.GT else "left"))
+            if cut == n:
+                return ResolvedPredicate.constant(False)
+            if cut == 0:
+                return ResolvedPredicate.constant(True)
+            return ResolvedPredicate.compare(Op.GE, *self._code_at(cut))
+        raise ValueError(f"cannot resolve operator {op}")
+
+    def encode_literal(self, pred: Predicate) -> ResolvedPredicate:
+        if pred.op is not Op.BETWEEN:
+            return self._resolve_one(pred.op, pred.value)
+        lo = self._resolve_one(Op.GE, pred.value)
+        hi = self._resolve_one(Op.LE, pred.value_high)
+        if (lo.is_trivial and not lo.trivial) or (hi.is_trivial and not hi.trivial):
+            return ResolvedPredicate.constant(False)
+        if lo.is_trivial and hi.is_trivial:
+            return ResolvedPredicate.constant(True)
+        if lo.is_trivial:
+            return hi
+        if hi.is_trivial:
+            return lo
+        return ResolvedPredicate.between(lo.code, lo.length, hi.code, hi.length)

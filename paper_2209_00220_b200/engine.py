@@ -1,0 +1,302 @@
+"""Layout dispatch and query execution (mirror of reference engine.py).
+
+The dispatch point (engine.py:172-221) is where device layouts plug in.
+``execute`` (engine.py:311-353) runs every conjunction as ONE fused device
+pass (bsb_conj_scan: predicate i sees the running result as its input mask
+and blocks already ruled out skip later columns entirely), ORs disjunction
+arms on the device, compacts the selection once and gathers + decodes each
+projected column with the lookup kernels.
+
+In scope: "byteslice" and "ppvbs" numeric columns.  CSV ingest (file I/O)
+is replaced by ``ingest_arrays`` over in-memory columns; the baseline
+layouts (bitpacked, vbp, pevbp) are out of scope.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .advisor import ColumnAdvice, advise_column
+from .bitvector import DeviceBitVector, ResultBitVector, as_device_bits
+from .byteslice import (ByteSliceColumn, build_byteslice, byteslice_size_report,
+                        lookup_byteslice_rows, scan_byteslice)
+from .datagen import PRNG_NAME
+from .device import device, stream
+from .dictionary import ColumnKind, Dictionary, FrequencyTable, freq_table_and_ranks
+from .predicate import DEFAULT_LANES, LaneConfig, Op, Predicate, ResolvedPredicate
+from .vbs import VbsColumn, build_vbs, lookup_vbs_rows, scan_vbs, vbs_size_report
+
+__all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
+           "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",
+           "lookup_decode", "lookup_decode_rows", "execute", "ingest_arrays", "size_report",
+           "conj_scan"]
+
+LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
+DEVICE_LAYOUTS = ("byteslice", "ppvbs")
+FORMAT_VERSION = 1
+
+_SCHEME_FOR = {"byteslice": "fixed", "ppvbs": "prefix_preserving"}
+
+
+class DataError(Exception):
+    """Input data problem: NULLs, bad literals, unknown columns."""
+
+
+@dataclass(frozen=True)
+class ColumnSpec:
+    name: str
+    kind: ColumnKind
+    layout: str | None = None
+
+    def __post_init__(self):
+        if self.layout is not None and self.layout not in LAYOUTS:
+            raise ValueError(f"unknown layout {self.layout!r}")
+
+
+@dataclass
+class Schema:
+    columns: list
+
+    def __post_init__(self):
+        names = [c.name for c in self.columns]
+        if len(set(names)) != len(names):
+            raise ValueError("duplicate column names in schema")
+
+
+@dataclass
+class Query:
+    groups: list
+    projection: list
+
+    @classmethod
+    def conjunction(cls, predicates, projection) -> "Query":
+        return cls([list(predicates)], list(projection))
+
+
+@dataclass
+class QueryResult:
+    n_selected: int
+    columns: dict
+    timings: list
+    selection: object
+
+
+@dataclass
+class StoredColumn:
+    name: str
+    kind: ColumnKind
+    scheme: str
+    layout: str
+    dictionary: Dictionary
+    column: object
+
+
+@dataclass
+class Store:
+    manifest: dict
+    columns: dict
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.manifest["n_rows"])
+
+
+def _require_device_layout(layout: str):
+    if layout not in DEVICE_LAYOUTS:
+        if layout in LAYOUTS:
+            raise ValueError(f"layout {layout!r} is outside the device path "
+                             "(baseline layouts are out of scope; see DESIGN.md)")
+        raise ValueError(f"unknown layout {layout!r}")
+
+
+def build_layout(layout: str, dictionary: Dictionary, ranks, lanes: LaneConfig = DEFAULT_LANES):
+    """engine.py:172-188 for the device layouts."""
+    _require_device_layout(layout)
+    if layout == "ppvbs":
+        codes, lens = dictionary.row_codes_device(ranks)
+        return build_vbs(codes, lens, lanes)
+    r = ranks if isinstance(ranks, torch.Tensor) else np.asarray(ranks, dtype=np.int64)
+    return build_byteslice(r, dictionary.assignment.width_bits, lanes)
+
+
+def scan_layout(layout: str, column, pred, mask=None, threads: int = 1):
+    """engine.py:191-201."""
+    _require_device_layout(layout)
+    if layout == "byteslice":
+        return scan_byteslice(column, pred, mask, threads)
+    return scan_vbs(column, pred, mask, threads)
+
+
+def lookup_decode_rows(stored: StoredColumn, rows: torch.Tensor, out_dtype=torch.int64):
+    """Device gather + decode of a row-id tensor (any order)."""
+    if stored.layout == "ppvbs":
+        sp, vals = stored.dictionary.dev_decode
+        return lookup_vbs_rows(stored.column, rows, sp, vals, out_dtype)
+    _require_device_layout(stored.layout)
+    return lookup_byteslice_rows(stored.column, rows, stored.dictionary.dev_values, out_dtype)
+
+
+def lookup_decode(stored: StoredColumn, selection) -> np.ndarray:
+    """engine.py:204-221: selected rows of one column, decoded to values."""
+    rows = as_device_bits(selection).row_ids()
+    if rows.numel() == 0:
+        return stored.dictionary.table.values[:0]
+    return lookup_decode_rows(stored, rows).cpu().numpy()
+
+
+def size_report(stored: StoredColumn) -> dict:
+    if stored.layout == "ppvbs":
+        return vbs_size_report(stored.column)
+    return byteslice_size_report(stored.column)
+
+
+def conj_scan(columns, preds, mask=None) -> DeviceBitVector:
+    """Fused conjunction over (layout, column) pairs and resolved predicates.
+
+    More than BSB_MAX_CONJ predicates are chained 8 at a time, each chunk
+    taking the previous result as its input mask (same semantics).
+    """
+    if len(columns) != len(preds):
+        raise ValueError("one predicate per column")
+    lib = _lib.load()
+    n = None
+    for layout, col in columns:
+        _require_device_layout(layout)
+        n = col.n_rows if n is None else n
+        if col.n_rows != n:
+            raise ValueError("columns differ in row count")
+    running = None if mask is None else as_device_bits(mask)
+    if not columns:
+        return running
+    for c0 in range(0, len(columns), _lib.MAX_CONJ):
+        chunk = list(zip(columns, preds))[c0:c0 + _lib.MAX_CONJ]
+        refs = (_lib.BsbColumnRef * len(chunk))()
+        cps = (_lib.BsbPred * len(chunk))()
+        keep = []
+        for i, ((layout, col), p) in enumerate(chunk):
+            refs[i].layout = _lib.LAYOUT_PPVBS if layout == "ppvbs" else _lib.LAYOUT_BYTESLICE
+            if layout == "ppvbs":
+                refs[i].vbs = ctypes.pointer(col._desc)
+            else:
+                refs[i].byteslice = ctypes.pointer(col._desc)
+            keep.append(refs[i])
+            cps[i] = p.to_c()
+        dev = device()
+        out = torch.empty(-(-n // 32), dtype=torch.int32, device=dev)
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        _lib.check(lib.bsb_conj_scan(len(chunk), refs, cps,
+                                     None if running is None else running.dwords.data_ptr(),
+                                     out.data_ptr(), cnt.data_ptr(), stream()), "conj_scan")
+        running = DeviceBitVector(n, out, cnt)
+    return running
+
+
+def _resolve(stored: StoredColumn, pred: Predicate) -> ResolvedPredicate:
+    try:
+        return stored.dictionary.encode_literal(pred)
+    except (TypeError, ValueError) as exc:
+        raise DataError(f"predicate on {pred.column!r}: {exc}") from None
+
+
+def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64) -> QueryResult:
+    """engine.py:311-353 with fused device conjunctions."""
+    for name in query.projection:
+        if name not in store.columns:
+            raise DataError(f"unknown projection column {name!r}")
+    for group in query.groups:
+        for pred in group:
+            if pred.column not in store.columns:
+                raise DataError(f"unknown predicate column {pred.column!r}")
+    timings = []
+    arms = []
+    for group in query.groups:
+        cols, preds = [], []
+        for pred in group:
+            st = store.columns[pred.column]
+            cols.append((st.layout, st.column))
+            preds.append(_resolve(st, pred))
+        t0 = time.perf_counter()
+        if cols:
+            running = conj_scan(cols, preds)
+        else:
+            running = DeviceBitVector.ones(store.n_rows)  # engine.py:333-334
+        torch.cuda.current_stream().synchronize()
+        timings.append({"column": ",".join(p.column for p in group), "phase": "scan",
+                        "op": "AND", "seconds": time.perf_counter() - t0})
+        arms.append(running)
+    selection = arms[0]
+    for extra in arms[1:]:
+        selection = selection | extra
+    n_sel = selection.count()
+    out = {}
+    rows = selection.row_ids() if n_sel else None
+    for name in query.projection:
+        st = store.columns[name]
+        if n_sel == 0:
+            out[name] = st.dictionary.table.values[:0]
+            timings.append({"column": name, "phase": "lookup", "op": "", "seconds": 0.0})
+            continue
+        t0 = time.perf_counter()
+        out[name] = lookup_decode_rows(st, rows, out_dtype).cpu().numpy()
+        timings.append({"column": name, "phase": "lookup", "op": "",
+                        "seconds": time.perf_counter() - t0})
+    return QueryResult(n_sel, out, timings, selection)
+
+
+def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "advisor", *,
+                  advise_cost="wall", advise_count: int = 100, subsample: int | None = None,
+                  lanes: LaneConfig = DEFAULT_LANES):
+    """engine.py:239-297 over in-memory columns {name: values} (no CSV I/O).
+
+    Per column: advise (unless the schema forces a layout), build the
+    frequency table + ranks in one device sort, assign codes, build the
+    device layout.  Returns (Store, report rows).
+    """
+    if policy not in ("advisor", "forced"):
+        raise ValueError(f"unknown layout policy {policy!r}")
+    specs = schema.columns if schema is not None else [
+        ColumnSpec(k, ColumnKind.NUMERIC) for k in columns]
+    n_rows = None
+    stored, entries, report = {}, [], []
+    for spec in specs:
+        vals = columns[spec.name]
+        n = vals.numel() if isinstance(vals, torch.Tensor) else len(vals)
+        if n_rows is not None and n != n_rows:
+            raise DataError("columns differ in row count")
+        n_rows = n
+        layout, advice, advise_s = spec.layout, None, 0.0
+        if layout is None:
+            if policy == "forced":
+                raise DataError(f"column {spec.name!r}: forced policy needs a layout")
+            t0 = time.perf_counter()
+            advice = advise_column(spec.name, vals, spec.kind, count=advise_count,
+                                   cost=advise_cost, subsample=subsample, lanes=lanes)
+            advise_s = time.perf_counter() - t0
+            layout = advice.chosen
+        _require_device_layout(layout)
+        t0 = time.perf_counter()
+        u, c, ranks = freq_table_and_ranks(vals)
+        table = FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), spec.kind)
+        d = Dictionary.build(table, _SCHEME_FOR[layout])
+        col = build_layout(layout, d, ranks, lanes)
+        torch.cuda.current_stream().synchronize()
+        encode_s = time.perf_counter() - t0
+        stored[spec.name] = StoredColumn(spec.name, spec.kind, _SCHEME_FOR[layout], layout, d,
+                                         col)
+        e = {"name": spec.name, "kind": spec.kind.value, "scheme": _SCHEME_FOR[layout],
+             "layout": layout, "n_distinct": table.n}
+        if advice is not None and not advice.degenerate:
+            e["advice"] = {"chosen": advice.chosen, "auc_byteslice": advice.auc_byteslice,
+                           "auc_ppvbs": advice.auc_ppvbs}
+        entries.append(e)
+        report.append({"column": spec.name, "layout": layout, "n_distinct": table.n,
+                       "encode_s": encode_s, "advise_s": advise_s})
+    manifest = {"format_version": FORMAT_VERSION, "n_rows": n_rows, "prng": PRNG_NAME,
+                "lane_count": lanes.lane_count, "columns": entries}
+    return Store(manifest, stored), report

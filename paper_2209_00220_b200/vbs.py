@@ -1,0 +1,239 @@
+"""PP-VBS (variable byte slices) on the B200 (mirror of reference vbs.py:42-517).
+
+Device layout = the reference's arrays: BS_1 (swizzled per 32-row block like
+ByteSlice, padded to 1024-row tiles), packed deep slices BS_j in row order,
+one uint32 existence word per block per deep slice, and the int64 block
+directory.  Scans use a per-tile warp prefix over existence popcounts instead
+of reading the directory; lookups read the directory.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bitvector import DeviceBitVector, as_device_bits
+from .device import device, host_u32, host_u64, stream, to_dev_i64, to_dev_u8, to_dev_u64
+from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
+from .stats import LazyScanStats, LookupStats, ScanStats
+
+__all__ = ["VbsColumn", "build_vbs", "scan_vbs", "lookup_vbs", "lookup_vbs_rows",
+           "vbs_size_report"]
+
+DEEP_PAD = 64
+
+
+@dataclass
+class VbsColumn:
+    """Device-resident PP-VBS column."""
+
+    n_rows: int
+    max_len: int
+    lanes: LaneConfig
+    stride: int
+    bs1: torch.Tensor                     # uint8 [stride], swizzled blocks
+    deep: list                            # deep[j] (j=1..K-1): uint8 packed slice j+1
+    exist: list                           # exist[j]: int32 [stride/32] words of slice j+1
+    block_dir: list                       # block_dir[j]: int64 [stride/32 + 1]
+    level_rows: list                      # rows owning byte j (j = 1..K), reference counts
+    _desc: _lib.BsbVbs = field(default=None, repr=False)
+
+    def __post_init__(self):
+        d = _lib.BsbVbs()
+        d.n_rows = self.n_rows
+        d.stride = self.stride
+        d.max_len = self.max_len
+        d.bs1 = self.bs1.data_ptr()
+        for j in range(1, self.max_len):
+            d.deep[j] = self.deep[j].data_ptr()
+            d.exist[j] = self.exist[j].data_ptr()
+            d.block_dir[j] = self.block_dir[j].data_ptr()
+            d.deep_len[j] = self.level_rows[j]
+        self._desc = d
+
+    @property
+    def desc_ref(self):
+        return ctypes.byref(self._desc)
+
+    @property
+    def n_blocks(self) -> int:
+        return -(-self.n_rows // 32)
+
+    def slice_len(self, j: int) -> int:
+        return self.n_rows if j == 1 else int(self.level_rows[j - 1])
+
+    # reference-layout views (host copies) --------------------------------
+    @property
+    def slices(self) -> list:
+        npad = self.n_blocks * 32
+        first = torch.empty(npad, dtype=torch.uint8, device=self.bs1.device)
+        _lib.check(_lib.load().bsb_vbs_export_bs1(self.desc_ref, first.data_ptr(), stream()),
+                   "export")
+        out = [first.cpu().numpy()]
+        for j in range(1, self.max_len):
+            out.append(self.deep[j][: self.level_rows[j]].cpu().numpy())
+        return out
+
+    def mask_words(self, j: int) -> np.ndarray:
+        """Existence words of slice j (j >= 2), one per block (vbs.py:58-61)."""
+        return host_u32(self.exist[j - 1][: self.n_blocks])
+
+    @property
+    def exist_bits(self) -> list:
+        return [self.mask_words(j).view(np.uint8) for j in range(2, self.max_len + 1)]
+
+    @property
+    def block_dir_host(self) -> np.ndarray:
+        nb = self.n_blocks
+        rows = [self.block_dir[j][: nb + 1].cpu().numpy() for j in range(1, self.max_len)]
+        return np.stack(rows) if rows else np.zeros((0, nb + 1), np.int64)
+
+
+def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES) -> VbsColumn:
+    """vbs.py:68-114 on the device: plan (validate, K, level sizes) + build."""
+    lanes.require_device()
+    codes = row_codes if isinstance(row_codes, torch.Tensor) else np.asarray(row_codes)
+    lens = row_lengths if isinstance(row_lengths, torch.Tensor) else np.asarray(row_lengths)
+    n = codes.numel() if isinstance(codes, torch.Tensor) else len(codes)
+    nl = lens.numel() if isinstance(lens, torch.Tensor) else len(lens)
+    if n == 0:
+        raise ValueError("empty column")
+    if nl != n:
+        raise ValueError("codes and lengths differ in length")
+    if not isinstance(lens, torch.Tensor):
+        if lens.min() < 1 or lens.max() > 8:
+            raise ValueError("code lengths must be 1..8 bytes")
+    lib = _lib.load()
+    dc = to_dev_u64(codes)
+    dl = to_dev_u8(lens)
+    K = ctypes.c_int32(0)
+    lr = (ctypes.c_int64 * _lib.MAX_LEVELS)()
+    _lib.check(lib.bsb_vbs_plan(dc.data_ptr(), dl.data_ptr(), n, ctypes.byref(K), lr,
+                                stream()), "build_vbs")
+    K = int(K.value)
+    stride = int(lib.bsb_stride_for(n))
+    nbpad = stride // 32
+    dev = device()
+    bs1 = torch.empty(stride, dtype=torch.uint8, device=dev)
+    deep, exist, bdir = [None], [None], [None]
+    for j in range(1, K):
+        deep.append(torch.empty(int(lr[j]) + DEEP_PAD, dtype=torch.uint8, device=dev))
+        exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
+        bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev))
+    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, [int(x) for x in lr[:K]])
+    _lib.check(lib.bsb_vbs_build(dc.data_ptr(), dl.data_ptr(), col.desc_ref, stream()),
+               "build_vbs")
+    return col
+
+
+def _mask_bytes(col: VbsColumn, live: int, length: int) -> int:
+    """vbs.py:286-287: existence words charged per live block."""
+    return live * 4 * (min(length + 1, col.max_len) - 1)
+
+
+def _scan_stats(col: VbsColumn, pred: ResolvedPredicate, mask) -> ScanStats:
+    lib = _lib.load()
+    nb = col.n_blocks
+    dev = col.bs1.device
+    st = torch.zeros(_lib.STATS_WORDS, dtype=torch.int64, device=dev)
+    depth = torch.zeros(max(nb, 1), dtype=torch.int8, device=dev)
+    out = torch.empty(nb, dtype=torch.int32, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    cp = pred.to_c()
+    _lib.check(lib.bsb_vbs_scan(col.desc_ref, ctypes.byref(cp),
+                                None if mask is None else mask.dwords.data_ptr(),
+                                out.data_ptr(), cnt.data_ptr(), st.data_ptr(), depth.data_ptr(),
+                                stream()), "scan_vbs(stats)")
+    h = st.cpu().numpy()
+    K = col.max_len
+    if pred.is_trivial:
+        skipped, mb = nb, 0
+    elif pred.op is Op.BETWEEN:
+        s1, s2 = int(h[17]), int(h[19])
+        skipped = min(s1, s2)
+        mb = _mask_bytes(col, nb - s1, pred.length) + _mask_bytes(col, nb - s2, pred.length2)
+    else:
+        skipped = int(h[17])
+        mb = _mask_bytes(col, nb - skipped, pred.length)
+    return ScanStats(levels=K, blocks_total=nb, blocks_skipped=skipped,
+                     words_loaded=h[0:K].copy(), bytes_loaded=h[8:8 + K].copy(),
+                     mask_bytes=mb, block_depth=depth[:nb].cpu().numpy())
+
+
+def scan_vbs(col: VbsColumn, pred: ResolvedPredicate, mask=None, threads: int = 1):
+    """vbs.py:292-324: Alg. 3 on the device.  Returns (DeviceBitVector, ScanStats).
+
+    A literal longer than the column's longest code raises ValueError (the
+    reference fails with IndexError at vbs.py:274).  ``threads`` is ignored.
+    """
+    m = None
+    if mask is not None:
+        m = as_device_bits(mask)
+        if m.n_rows != col.n_rows:
+            raise ValueError("input mask length mismatch")
+    lib = _lib.load()
+    out = torch.empty(col.n_blocks, dtype=torch.int32, device=col.bs1.device)
+    cnt = torch.empty(1, dtype=torch.int64, device=col.bs1.device)
+    cp = pred.to_c()
+    _lib.check(lib.bsb_vbs_scan(col.desc_ref, ctypes.byref(cp),
+                                None if m is None else m.dwords.data_ptr(), out.data_ptr(),
+                                cnt.data_ptr(), None, None, stream()), "scan_vbs")
+    return DeviceBitVector(col.n_rows, out, cnt), LazyScanStats(
+        lambda: _scan_stats(col, pred, m))
+
+
+def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
+                    out_dtype=torch.int64, level_counts=None):
+    """Device lookup of a row-id list: padded codes, or decoded values when
+    the dictionary's sorted padded codes / values are given."""
+    lib = _lib.load()
+    rows = to_dev_i64(rows)
+    n = rows.numel()
+    lc = None if level_counts is None else level_counts.data_ptr()
+    if sorted_padded is None:
+        out = torch.empty(n, dtype=torch.int64, device=rows.device)
+        _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, rows.data_ptr(), n, out.data_ptr(),
+                                           None, None, 0, None, None, lc, stream()),
+                   "lookup_vbs")
+        return out
+    out = torch.empty(n, dtype=out_dtype, device=rows.device)
+    p64 = out.data_ptr() if out_dtype == torch.int64 else None
+    p32 = out.data_ptr() if out_dtype == torch.int32 else None
+    _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, rows.data_ptr(), n, None,
+                                       sorted_padded.data_ptr(), dict_values.data_ptr(),
+                                       sorted_padded.numel(), p64, p32, lc, stream()),
+               "lookup_vbs")
+    return out
+
+
+def lookup_vbs(col: VbsColumn, selection):
+    """vbs.py:331-371: padded codes of the selected rows, ascending row order."""
+    if selection.n_rows != col.n_rows:
+        raise ValueError("selection length mismatch")
+    sel = as_device_bits(selection)
+    rows = sel.row_ids()
+    n = rows.numel()
+    if n == 0:
+        return np.zeros(0, np.uint64), LookupStats()
+    lc = torch.zeros(_lib.MAX_LEVELS, dtype=torch.int64, device=rows.device)
+    codes = lookup_vbs_rows(col, rows, level_counts=lc)
+    counts = lc.cpu().numpy()
+    levels = int(np.flatnonzero(counts)[-1]) + 1
+    nz_words = int((sel.dwords != 0).sum().item())
+    st = LookupStats(levels_touched=levels, bytes_loaded=int(counts.sum()),
+                     mask_bytes=nz_words * (col.max_len - 1) * 4)
+    return host_u64(codes), st
+
+
+def vbs_size_report(col: VbsColumn) -> dict:
+    """vbs.py:505-517."""
+    sb = [col.slice_len(j) for j in range(1, col.max_len + 1)]
+    mb = ((col.n_rows + 7) // 8) * (col.max_len - 1)
+    db = col.n_blocks * (col.max_len - 1) * 4
+    data = sum(sb) + mb
+    return {"slice_bytes": sb, "mask_bytes": mb, "directory_bytes": db,
+            "total_bytes": data + db, "avg_bits_per_code": 8.0 * data / col.n_rows}

@@ -1,0 +1,366 @@
+"""Parity of the CUDA path against the reference's golden vectors and the
+CPU oracle.  Everything here calls through the C ABI on a B200; the bar is
+bit-exactness (bitvectors, counts, stats, looked-up codes and values)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from golden_io import load, stats_of
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected only on GPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2209_00220_b200 as B  # noqa: E402
+from paper_2209_00220_b200 import engine as E  # noqa: E402
+from paper_2209_00220_b200.predicate import Op, Predicate, ResolvedPredicate  # noqa: E402
+
+
+def rp(t):
+    op, code, length, code2, length2, trivial = t
+    if trivial is not None:
+        return ResolvedPredicate.constant(trivial)
+    if op == "BETWEEN":
+        return ResolvedPredicate.between(code, length, code2, length2)
+    return ResolvedPredicate.compare(Op[op], code, length)
+
+
+def op_pred(t):
+    op, code, length, code2, length2, trivial = t
+    if trivial is not None:
+        return O.pred_const(trivial)
+    if op == "BETWEEN":
+        return O.pred_between(code, length, code2, length2)
+    return O.pred_compare(op, code, length)
+
+
+def check_stats(st, want):
+    assert st.levels == want["levels"]
+    assert st.blocks_total == want["blocks_total"]
+    assert st.blocks_skipped == want["blocks_skipped"]
+    assert list(st.words_loaded) == want["words_loaded"].tolist()
+    assert list(st.bytes_loaded) == want["bytes_loaded"].tolist()
+    assert st.mask_bytes == want["mask_bytes"]
+    assert st.total_bytes == want["total_bytes"]
+    assert st.block_depth.tolist() == want["block_depth"].tolist()
+
+
+# --------------------------------------------------------------- datagen
+
+
+def test_gen_zipf_matches_reference():
+    data, meta = load("zipf")
+    for i, m in enumerate(meta):
+        got = B.gen_zipf(B.ZipfSpec(m["s"], m["d"], m["n"], m["seed"]))
+        assert np.array_equal(got, data[f"{i}/values"])
+
+
+# ------------------------------------------------------------- ByteSlice
+
+
+def test_byteslice_golden():
+    data, meta = load("bs")
+    for ci, m in enumerate(meta):
+        codes = data[f"{ci}/codes"]
+        col = B.build_byteslice(codes, m["w"])
+        assert np.array_equal(col.slices, data[f"{ci}/slices"]), ci
+        mask = B.ResultBitVector(m["n"], data[f"{ci}/mask"])
+        for pi, t in enumerate(m["preds"]):
+            for mi, msk in enumerate((None, mask)):
+                key = f"{ci}/p{pi}m{mi}/"
+                bv, st = B.scan_byteslice(col, rp(t), msk)
+                want = data[key + "words"]
+                assert np.array_equal(bv.words, want), key
+                assert bv.count() == O.words_count(want)
+                if pi % 3 == 0 or t[0] == "BETWEEN" or t[5] is not None:
+                    check_stats(st, stats_of(data, key))
+        sel = B.ResultBitVector(m["n"], data[f"{ci}/sel"])
+        got, lst = B.lookup_byteslice(col, sel)
+        assert np.array_equal(got, data[f"{ci}/lookup"])
+        assert [lst.levels_touched, lst.bytes_loaded, lst.mask_bytes] == \
+            data[f"{ci}/lookup_stats"].tolist()
+
+
+def test_byteslice_random_large_between_and_masks():
+    rng = np.random.default_rng(123)
+    for w, n in ((16, (1 << 20) + 7), (20, 300_001), (32, 70_000), (9, 4097), (64, 5000)):
+        hi_bound = (1 << w) if w < 64 else (1 << 63)
+        codes = rng.integers(0, hi_bound, size=n, dtype=np.uint64)
+        col = B.build_byteslice(codes, w)
+        planes = O.bs_build(codes, w)
+        K = planes.shape[0]
+        mask = rng.random(n) < 0.7
+        mw = O.bools_to_words(mask)
+        for _ in range(6):
+            a, b = sorted(int(x) for x in rng.choice(codes, 2))
+            for p in (O.pred_between(a, K, b, K), O.pred_compare("LT", b, K),
+                      O.pred_compare("EQ", a, K), O.pred_compare("NE", a, K)):
+                rpred = rp(list(p))
+                for m_o, m_d in ((None, None), (mw, B.ResultBitVector(n, mw))):
+                    want, _ = O.bs_scan(planes, w, n, p, m_o)
+                    bv, _ = B.scan_byteslice(col, rpred, m_d)
+                    assert np.array_equal(bv.words, want)
+                    assert bv.count() == O.words_count(want)
+
+
+def test_byteslice_row_lookup_unsorted_duplicates():
+    rng = np.random.default_rng(5)
+    n, w = 100_003, 24
+    codes = rng.integers(0, 1 << w, size=n, dtype=np.uint64)
+    col = B.build_byteslice(codes, w)
+    rows = rng.integers(0, n, size=50_000)
+    got = B.lookup_byteslice_rows(col, torch.from_numpy(rows)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), codes[rows])
+    # decode through a rank -> value table
+    table = torch.from_numpy(rng.integers(-2**40, 2**40, size=1 << w)).cuda()
+    vals = B.lookup_byteslice_rows(col, torch.from_numpy(rows), table).cpu().numpy()
+    assert np.array_equal(vals, table.cpu().numpy()[codes[rows].astype(np.int64)])
+
+
+def test_byteslice_errors():
+    with pytest.raises(ValueError):
+        B.build_byteslice([], 8)
+    with pytest.raises(ValueError):
+        B.build_byteslice([1], 0)
+    with pytest.raises(ValueError):
+        B.build_byteslice([256], 8)
+    with pytest.raises(ValueError):
+        B.build_byteslice([1, 2], 8, B.LaneConfig(16))
+    col = B.build_byteslice([5, 6], 4)
+    with pytest.raises(ValueError):
+        B.scan_byteslice(col, ResolvedPredicate.compare(Op.EQ, 5, 1),
+                         B.ResultBitVector.zeros(3))
+    out, st = B.lookup_byteslice(col, B.ResultBitVector.zeros(2))
+    assert out.tolist() == [] and st.total_bytes == 0
+
+
+# ----------------------------------------------------------------- PP-VBS
+
+
+def test_vbs_golden():
+    data, meta = load("vbs")
+    for ci, m in enumerate(meta):
+        col = B.build_vbs(data[f"{ci}/codes"], data[f"{ci}/lens"])
+        K = col.max_len
+        assert K == m["K"]
+        sl = col.slices
+        assert np.array_equal(sl[0], data[f"{ci}/bs1"])
+        for j in range(2, K + 1):
+            assert np.array_equal(sl[j - 1], data[f"{ci}/bs{j}"])
+            assert np.array_equal(col.mask_words(j), data[f"{ci}/m{j}"])
+        assert np.array_equal(col.block_dir_host, data[f"{ci}/dir"])
+        mask = B.ResultBitVector(m["n"], data[f"{ci}/mask"])
+        for pi, t in enumerate(m["preds"]):
+            for mi, msk in enumerate((None, mask)):
+                key = f"{ci}/p{pi}m{mi}/"
+                bv, st = B.scan_vbs(col, rp(t), msk)
+                want = data[key + "words"]
+                assert np.array_equal(bv.words, want), key
+                assert bv.count() == O.words_count(want)
+                check_stats(st, stats_of(data, key))
+        for si in range(3):
+            sel = B.ResultBitVector(m["n"], data[f"{ci}/sel{si}"])
+            got, lst = B.lookup_vbs(col, sel)
+            assert np.array_equal(got, data[f"{ci}/lookup{si}"])
+            assert [lst.levels_touched, lst.bytes_loaded, lst.mask_bytes] == \
+                data[f"{ci}/lookup_stats{si}"].tolist()
+
+
+def _ppe_column(s, d, n, seed):
+    vals = O.gen_zipf(s, d, n, seed)
+    od = O.OracleDict.from_values(vals, "prefix_preserving")
+    codes, lens = od.row_codes(od.encode_rows(vals))
+    return vals, od, codes, lens
+
+
+def test_vbs_zipf_between_windows_vs_oracle():
+    """cfg2-shaped (Zipf 1.2 over 2^20, scaled to 2^20 rows), the four
+    BETWEEN windows of SURVEY.md §8(d), fused single pass vs oracle legs."""
+    n = 1 << 20
+    vals, od, codes, lens = _ppe_column(1.2, 20, n, 42)
+    col = B.build_vbs(codes, lens)
+    ocol = O.vbs_build(codes, lens)
+    srt = np.sort(vals)
+    q = lambda x: int(srt[min(n - 1, int(x * n))])  # noqa: E731
+    for p in (0.001, 0.01, 0.1, 0.5):
+        mm = min(p, 0.25)
+        opred = od.encode_literal("BETWEEN", q(1 - p - mm), q(1 - mm))
+        want, _ = O.vbs_scan(ocol, opred)
+        bv, _ = B.scan_vbs(col, rp(list(opred)))
+        assert np.array_equal(bv.words, want), p
+        assert np.array_equal(O.words_to_bools(want, n),
+                              O.naive_filter(vals, "BETWEEN", q(1 - p - mm), q(1 - mm)))
+
+
+def test_vbs_random_codes_all_ops_masks_vs_oracle():
+    rng = np.random.default_rng(77)
+    for n, K in ((50_001, 3), (20_000, 8), (3000, 5), (33, 2), (1, 1)):
+        lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+        byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+        byts[:, 0] |= np.uint64(1)
+        codes = np.zeros(n, np.uint64)
+        for k in range(8):
+            use = lens > k
+            codes[use] |= byts[use, k] << np.uint64(8 * k)
+        col = B.build_vbs(codes, lens)
+        ocol = O.vbs_build(codes, lens)
+        mw = O.bools_to_words(rng.random(n) < 0.5)
+        for _ in range(4):
+            r = int(rng.integers(0, n))
+            lit, ll = int(codes[r]), int(lens[r])
+            for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                p = O.pred_compare(op, lit, ll)
+                for m_o in (None, mw):
+                    want, st_w = O.vbs_scan(ocol, p, m_o)
+                    bv, st = B.scan_vbs(col, rp(list(p)),
+                                        None if m_o is None else B.ResultBitVector(n, m_o))
+                    assert np.array_equal(bv.words, want), (n, K, op)
+            a, b = sorted(rng.integers(0, n, 2).tolist())
+            pa = int(codes[a]) << (8 * (ocol.K - int(lens[a])))
+            pb = int(codes[b]) << (8 * (ocol.K - int(lens[b])))
+            if pa > pb:
+                a, b = b, a
+            p = O.pred_between(int(codes[a]), int(lens[a]), int(codes[b]), int(lens[b]))
+            want, st_w = O.vbs_scan(ocol, p, mw)
+            bv, st = B.scan_vbs(col, rp(list(p)), B.ResultBitVector(n, mw))
+            assert np.array_equal(bv.words, want)
+            assert st.total_bytes == st_w.total_bytes
+            assert st.block_depth.tolist() == st_w.block_depth.tolist()
+
+
+def test_vbs_row_lookup_decode_vs_oracle():
+    n = 200_000
+    vals, od, codes, lens = _ppe_column(1.0, 20, n, 4)
+    col = B.build_vbs(codes, lens)
+    ocol = O.vbs_build(codes, lens)
+    rng = np.random.default_rng(6)
+    rows = rng.integers(0, n, size=100_000)
+    got = B.lookup_vbs_rows(col, torch.from_numpy(rows)).cpu().numpy().view(np.uint64)
+    want, _ = O.vbs_lookup(ocol, rows)
+    assert np.array_equal(got, want)
+    table = B.FrequencyTable(od.values, od.weights, B.ColumnKind.NUMERIC)
+    d = B.Dictionary.build(table, "prefix_preserving")
+    sp, dv = d.dev_decode
+    v = B.lookup_vbs_rows(col, torch.from_numpy(rows), sp, dv).cpu().numpy()
+    assert np.array_equal(v, vals[rows])
+    v32 = B.lookup_vbs_rows(col, torch.from_numpy(np.sort(rows)), sp, dv,
+                            out_dtype=torch.int32).cpu().numpy()
+    assert np.array_equal(v32, vals[np.sort(rows)].astype(np.int32))
+
+
+def test_vbs_errors():
+    col = B.build_vbs([1, 2], [1, 1])
+    with pytest.raises(ValueError):
+        B.scan_vbs(col, ResolvedPredicate.compare(Op.EQ, 0x0101, 2))
+    with pytest.raises(ValueError):
+        B.build_vbs([0x1FF], [1])
+    with pytest.raises(ValueError):
+        B.build_vbs([1], [9])
+    with pytest.raises(ValueError):
+        B.build_vbs([1, 2], [1])
+    # decode of a code the dictionary does not hold -> LookupError
+    d = B.Dictionary.build(B.FrequencyTable(np.arange(3), np.array([3, 2, 1]),
+                                            B.ColumnKind.NUMERIC), "prefix_preserving")
+    bad = B.build_vbs([9], [1])
+    sp, dv = d.dev_decode
+    with pytest.raises(LookupError):
+        B.lookup_vbs_rows(bad, torch.zeros(1, dtype=torch.int64), sp, dv)
+
+
+# --------------------------------------------- encoders, advisor, engine
+
+
+def test_freq_table_and_encode_rows_vs_oracle():
+    rng = np.random.default_rng(8)
+    for vals in (O.gen_zipf(1.2, 20, 1 << 20, 42), rng.integers(-10**12, 10**12, 50_000),
+                 rng.integers(-3, 3, 1000), np.array([7]), np.arange(70_000)[::-1].copy()):
+        t = B.build_frequency_table(vals, B.ColumnKind.NUMERIC)
+        u, c = O.freq_table(vals)
+        assert np.array_equal(t.values, u) and np.array_equal(t.weights, c)
+        d = B.Dictionary.build(t, "fixed")
+        assert np.array_equal(d.encode_rows(vals), np.searchsorted(u, vals))
+    with pytest.raises(KeyError):
+        d.encode_rows(np.array([123456789]))
+
+
+def test_advisor_bytes_mode_matches_reference():
+    data, meta = load("advisor")
+    for i, m in enumerate(meta):
+        a = B.advise_column("c", data[f"{i}/values"], B.ColumnKind.NUMERIC,
+                            count=m["count"], cost="bytes", subsample=m["subsample"])
+        assert a.chosen == m["chosen"]
+        assert a.auc_byteslice == m["auc_bs"] and a.auc_ppvbs == m["auc_vbs"]
+        assert [(p.selectivity, p.time) for p in a.points_byteslice] == \
+            [tuple(x) for x in data[f"{i}/pts_bs"].tolist()]
+        assert [(p.selectivity, p.time) for p in a.points_ppvbs] == \
+            [tuple(x) for x in data[f"{i}/pts_vbs"].tolist()]
+
+
+def test_advisor_wall_mode_picks_and_tie():
+    rng = np.random.default_rng(9)
+    uni = rng.integers(0, 1 << 12, size=1 << 20, dtype=np.int64)
+    sk = B.gen_zipf(B.ZipfSpec(1.5, 12, 1 << 20, seed=9))
+    assert B.advise_column("u", uni, B.ColumnKind.NUMERIC, count=20, cost="bytes").chosen \
+        == "byteslice"
+    assert B.advise_column("z", sk, B.ColumnKind.NUMERIC, count=20, cost="bytes").chosen \
+        == "ppvbs"
+    tie = B.advise_column("t", uni[:4096], B.ColumnKind.NUMERIC, count=5,
+                          cost=lambda run: 1.0)
+    assert tie.chosen == "byteslice"
+    w = B.advise_column("u", uni, B.ColumnKind.NUMERIC, count=10, cost="wall")
+    assert w.auc_byteslice > 0 and w.auc_ppvbs > 0
+    deg = B.advise_column("c", np.zeros(100, np.int64), B.ColumnKind.NUMERIC)
+    assert deg.degenerate and deg.chosen == "byteslice"
+
+
+def test_fixture_query_192_through_engine():
+    f, _ = load("fixture")
+    schema = E.Schema([E.ColumnSpec("qty", B.ColumnKind.NUMERIC, "byteslice"),
+                       E.ColumnSpec("amount", B.ColumnKind.NUMERIC, "ppvbs")])
+    store, _ = E.ingest_arrays({"qty": f["qty"], "amount": f["amount"]}, schema,
+                               policy="forced")
+    q = E.execute(store, E.Query.conjunction(
+        [Predicate("amount", Op.LE, 4), Predicate("qty", Op.GT, 50)], ["amount", "qty"]))
+    assert q.n_selected == 192
+    assert np.array_equal(q.selection.words, f["selection"])
+    assert np.array_equal(q.columns["amount"], f["proj_amount"])
+    assert np.array_equal(q.columns["qty"], f["proj_qty"])
+
+
+def test_conjunction_fused_equals_pipelined_oracle():
+    rng = np.random.default_rng(10)
+    n = 300_007
+    cols = {"u16": rng.integers(0, 1 << 16, n), "z12": O.gen_zipf(1.0, 12, n, 11),
+            "u24": rng.integers(0, 1 << 24, n), "z16": O.gen_zipf(1.5, 16, n, 12)}
+    layouts = {"u16": "byteslice", "z12": "ppvbs", "u24": "byteslice", "z16": "ppvbs"}
+    schema = E.Schema([E.ColumnSpec(k, B.ColumnKind.NUMERIC, v) for k, v in layouts.items()])
+    store, _ = E.ingest_arrays(cols, schema, policy="forced")
+    srt = {k: np.sort(v) for k, v in cols.items()}
+    qq = lambda k, x: int(srt[k][min(n - 1, int(x * n))])  # noqa: E731
+    preds = [Predicate("u16", Op.LT, 32768),
+             Predicate("z12", Op.BETWEEN, qq("z12", 0.2), qq("z12", 0.9)),
+             Predicate("u24", Op.GE, qq("u24", 0.6)), Predicate("z16", Op.LE, qq("z16", 0.7))]
+    res = E.execute(store, E.Query([preds, [Predicate("u16", Op.EQ, 5)]], ["u24", "z12"]))
+    want = np.ones(n, bool)
+    for p in preds:
+        want &= O.naive_filter(cols[p.column], p.op.name, p.value, p.value_high)
+    want |= cols["u16"] == 5
+    assert np.array_equal(res.selection.to_bools(), want)
+    assert res.n_selected == int(want.sum())
+    assert np.array_equal(res.columns["u24"], cols["u24"][want])
+    assert np.array_equal(res.columns["z12"], cols["z12"][want])
+
+
+def test_device_bitvector_ops():
+    rng = np.random.default_rng(12)
+    for n in (1, 31, 32, 33, 1000, 100_001):
+        a = B.ResultBitVector.from_bools(rng.random(n) < 0.3)
+        b = B.ResultBitVector.from_bools(rng.random(n) < 0.6)
+        da, db = a.to_device(), b.to_device()
+        assert (da & db) == (a & b) and (da | db) == (a | b) and (~da) == (~a)
+        assert da.count() == a.count()
+        assert np.array_equal(da.to_indices(), a.to_indices())
+        assert np.array_equal(da.row_ids(5).cpu().numpy(), a.to_indices() + 5)
