@@ -1,0 +1,22 @@
+#!/usr/bin/env bash
+# Profiling recipe run on the GPU box (see /opt/skills/guides/B200_PROFILING.md).
+#   1. plain bench (profile mode) must exit 0 first
+#   2. launch list: every kernel with its device time (cold-cache, serialised)
+#   3. one `ncu --set full` capture of each scan kernel of the timed region
+# Outputs land in gpurun_out/; summaries worth keeping are copied to profiles/.
+set -euo pipefail
+OUT=${OUT:-gpurun_out}
+mkdir -p "$OUT"
+CMD="python bench.py --profile --steps 3 --warmup 1"
+$CMD > "$OUT/profile_plain.log" 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'bsb|scan|conj|lookup|cub' \
+    --csv --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
+# timed-region launches: skip the stats/parity-guard launches (8 stats legs x2 for
+# BETWEEN + 8 parity) and the warm-up step; capture one of each layout's kernel
+ncu --set full --clock-control none --import-source on \
+    -k regex:'scan_kernel<1, 1, 0>' -s 4 -c 1 -o "$OUT/prof_vbs" $CMD \
+    > "$OUT/ncu_vbs.log" 2>&1
+ncu --set full --clock-control none --import-source on \
+    -k regex:'scan_kernel<0, 1, 0>' -s 4 -c 1 -o "$OUT/prof_bs" $CMD \
+    > "$OUT/ncu_bs.log" 2>&1
+echo done
