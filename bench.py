@@ -429,7 +429,9 @@ def col_bytes(col) -> int:
         return col.planes.numel()
     b = col.bs1.numel()
     for j in range(1, col.max_len):
-        b += col.deep[j].numel() + col.exist[j].numel() * 4 + col.block_dir[j].numel() * 8
+        b += col.deep[j].numel() + col.exist[j].numel() * 4
+        if col.block_dir[j] is not None:
+            b += col.block_dir[j].numel() * 8
     return b
 
 
@@ -446,6 +448,10 @@ def measure_e2e(data, scans, steps, n, world):
     dev_v = [torch.empty_like(col_v.bs1)]
     for j in range(1, col_v.max_len):
         for t in (col_v.deep[j], col_v.exist[j], col_v.block_dir[j]):
+            if t is None:  # rank2 columns keep only the level-2 directory
+                host_v.append(None)
+                dev_v.append(None)
+                continue
             host_v.append(t.cpu().pin_memory())
             dev_v.append(torch.empty_like(t))
     host_b = col_b.planes.cpu().pin_memory()
@@ -454,16 +460,18 @@ def measure_e2e(data, scans, steps, n, world):
     cv = VbsColumn(col_v.n_rows, K, col_v.lanes, col_v.stride, dev_v[0],
                    [None] + [dev_v[1 + 3 * (j - 1)] for j in range(1, K)],
                    [None] + [dev_v[2 + 3 * (j - 1)] for j in range(1, K)],
-                   [None] + [dev_v[3 + 3 * (j - 1)] for j in range(1, K)], col_v.level_rows)
+                   [None] + [dev_v[3 + 3 * (j - 1)] for j in range(1, K)], col_v.level_rows,
+                   col_v.deep_mode)
     cb = ByteSliceColumn(col_b.n_rows, col_b.width_bits, col_b.lanes, col_b.stride, dev_b)
     nw = -(-n // 32)
     out_h = [torch.empty(nw, dtype=torch.int32).pin_memory() for _ in scans]
     cnt_h = torch.empty(len(scans), dtype=torch.int64).pin_memory()
-    h2d = sum(t.numel() * t.element_size() for t in host_v) + host_b.numel()
+    pairs = [(h, d) for h, d in zip(host_v, dev_v) if h is not None]
+    h2d = sum(h.numel() * h.element_size() for h, _ in pairs) + host_b.numel()
     d2h = len(scans) * (nw * 4 + 8)
 
     def step():
-        for h, d in zip(host_v, dev_v):
+        for h, d in pairs:
             d.copy_(h, non_blocking=True)
         dev_b.copy_(host_b, non_blocking=True)
         for i, (layout, p, _c, pred, _a, _s) in enumerate(scans):

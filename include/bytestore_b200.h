@@ -80,19 +80,26 @@ typedef struct bsb_byteslice {
 
 /* Device-resident PP-VBS column (reference vbs.py:42-65).
  * bs1:        first byte of every row, `stride` bytes, swizzled like ByteSlice.
- * deep[j]:    slice j+1 (j = 1..max_len-1): bytes of rows whose code has a
- *             (j+1)-th byte, packed in row order exactly like the reference
- *             (vbs.py:98-100); allocation padded by >= 64 bytes.
  * exist[j]:   uint32 existence word per block of slice j+1 (vbs.py:101-104),
- *             `stride/32` words.
- * block_dir[j]: int64[stride/32 + 1]: bytes of slice j+1 before block b
- *             (vbs.py:105-106).
- * Index 0 of deep/exist/block_dir is unused (level 1 is bs1). */
+ *             `stride/32` words (row space, exactly the reference's M_{j+1}).
+ * deep_mode selects how the deep slices (levels 2..max_len) are stored:
+ *  BSB_DEEP_PACKED (0): deep[j] = slice j+1 packed in row order exactly like
+ *             the reference (vbs.py:98-100); block_dir[j] = int64[stride/32+1]
+ *             bytes of slice j+1 before block b (vbs.py:105-106).
+ *  BSB_DEEP_RANK2 (1): every deep slice holds one byte per "deep row" (rows
+ *             whose code has >= 2 bytes), in row order; rows shorter than the
+ *             level hold a 0 pad byte.  All levels share block_dir[1] (the
+ *             level-2 directory); block_dir[j>1] are unused.  The scan then
+ *             works in one packed space per block for all deep levels.
+ * deep allocations are padded by >= 64 bytes.  Index 0 of deep/exist/
+ * block_dir is unused (level 1 is bs1). */
+#define BSB_DEEP_PACKED 0
+#define BSB_DEEP_RANK2 1
 typedef struct bsb_vbs {
   int64_t n_rows;
   int64_t stride;
   int32_t max_len;
-  int32_t reserved;
+  int32_t deep_mode;
   const uint8_t* bs1;
   const uint8_t* deep[BSB_MAX_LEVELS];
   const uint32_t* exist[BSB_MAX_LEVELS];
@@ -158,6 +165,11 @@ int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const bsb_vbs* col
                   void* stream);
 /* Reference (unswizzled) first slice, uint8[ceil(n/32)*32] -- parity helper. */
 int bsb_vbs_export_bs1(const bsb_vbs* col, uint8_t* out, void* stream);
+/* Reference-packed slice `level` (2..max_len) into out_bytes (level_rows
+ * bytes) and its reference block directory into out_dir (int64[nb+1]), for
+ * either deep_mode -- parity helper. */
+int bsb_vbs_export_level(const bsb_vbs* col, int32_t level, uint8_t* out_bytes,
+                         int64_t* out_dir, void* stream);
 
 /* scan_vbs (vbs.py:292-324): Alg. 3 with the existence shortcut.  Same
  * argument contract as bsb_byteslice_scan.  A literal longer than max_len

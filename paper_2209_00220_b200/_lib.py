@@ -25,6 +25,7 @@ STATS_WORDS = 24
 OK, EINVAL, ERANGE, ENOTFOUND, ECUDA, EKEY = 0, 1, 2, 3, 4, 5
 OP_CODES = {"EQ": 0, "NE": 1, "LT": 2, "LE": 3, "GT": 4, "GE": 5, "BETWEEN": 6}
 LAYOUT_BYTESLICE, LAYOUT_PPVBS = 0, 1
+DEEP_PACKED, DEEP_RANK2 = 0, 1
 
 
 class BsbPred(ctypes.Structure):
@@ -39,7 +40,7 @@ class BsbByteSlice(ctypes.Structure):
 
 class BsbVbs(ctypes.Structure):
     _fields_ = [("n_rows", c_int64), ("stride", c_int64), ("max_len", c_int32),
-                ("reserved", c_int32), ("bs1", c_void_p), ("deep", c_void_p * MAX_LEVELS),
+                ("deep_mode", c_int32), ("bs1", c_void_p), ("deep", c_void_p * MAX_LEVELS),
                 ("exist", c_void_p * MAX_LEVELS), ("block_dir", c_void_p * MAX_LEVELS),
                 ("deep_len", c_int64 * MAX_LEVELS)]
 
@@ -64,6 +65,7 @@ _SIGS = {
     "bsb_vbs_plan": (c_int32, [_P, _P, c_int64, POINTER(c_int32), POINTER(c_int64), _P]),
     "bsb_vbs_build": (c_int32, [_P, _P, POINTER(BsbVbs), _P]),
     "bsb_vbs_export_bs1": (c_int32, [POINTER(BsbVbs), _P, _P]),
+    "bsb_vbs_export_level": (c_int32, [POINTER(BsbVbs), c_int32, _P, _P, _P]),
     "bsb_vbs_scan": (c_int32, [POINTER(BsbVbs), POINTER(BsbPred), _P, _P, _P, _P, _P, _P]),
     "bsb_vbs_lookup_rows": (c_int32, [POINTER(BsbVbs), _P, c_int64, _P, _P, _P, c_int64, _P, _P,
                                       _P, _P]),

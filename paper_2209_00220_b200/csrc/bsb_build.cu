@@ -158,7 +158,7 @@ __global__ void vbs_exist_kernel(const uint64_t* __restrict__ codes,
 }
 
 __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
-                                   const uint8_t* __restrict__ lens, int64_t n, int K,
+                                   const uint8_t* __restrict__ lens, int64_t n, int K, int mode,
                                    uint8_t* const* deep, const uint32_t* const* exist,
                                    const int64_t* const* dir) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
@@ -168,12 +168,46 @@ __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
     const uint64_t c = codes[r];
     const int64_t b = r >> 5;
     const uint32_t below = (1u << (r & 31)) - 1u;
-    for (int j = 2; j <= (int)l; ++j) {
-      const uint32_t w = exist[j - 1][b];
-      const int64_t pos = dir[j - 1][b] + __popc(w & below);
-      deep[j - 1][pos] = (uint8_t)(c >> (8 * (l - j)));
+    if (mode == BSB_DEEP_RANK2) {
+      // one slot per deep row in every deep slice; shorter codes pad with 0
+      const int64_t pos = dir[1][b] + __popc(exist[1][b] & below);
+      for (int j = 2; j <= K; ++j)
+        deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
+    } else {
+      for (int j = 2; j <= (int)l; ++j) {
+        const uint32_t w = exist[j - 1][b];
+        const int64_t pos = dir[j - 1][b] + __popc(w & below);
+        deep[j - 1][pos] = (uint8_t)(c >> (8 * (l - j)));
+      }
     }
   }
+}
+
+// Reference-packed bytes of one deep level from either device packing.
+__global__ void vbs_export_level_kernel(int64_t n, int level, int mode,
+                                        const uint8_t* __restrict__ deep_l,
+                                        const uint32_t* __restrict__ exist_l,
+                                        const uint32_t* __restrict__ exist_2,
+                                        const int64_t* __restrict__ dir_src,
+                                        const int64_t* __restrict__ ref_dir,
+                                        uint8_t* __restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = r >> 5;
+    const uint32_t below = (1u << (r & 31)) - 1u;
+    const uint32_t w = exist_l[b];
+    if (!((w >> (r & 31)) & 1u)) continue;
+    const int64_t src = mode == BSB_DEEP_RANK2 ? dir_src[b] + __popc(exist_2[b] & below)
+                                               : dir_src[b] + __popc(w & below);
+    out[ref_dir[b] + __popc(w & below)] = deep_l[src];
+  }
+}
+
+__global__ void popc_words_kernel(const uint32_t* __restrict__ w, int64_t nb,
+                                  int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __popc(w[i]);
 }
 
 __global__ void vbs_export_kernel(const uint8_t* __restrict__ bs1, int64_t npad,
@@ -277,8 +311,11 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   const int64_t nbpad = col->stride / 32;
   PtrTable h;
   std::memset(&h, 0, sizeof(h));
+  const int mode = col->deep_mode;
+  if (mode != BSB_DEEP_PACKED && mode != BSB_DEEP_RANK2) return BSB_EINVAL;
   for (int j = 1; j < K; ++j) {
-    if (!col->deep[j] || !col->exist[j] || !col->block_dir[j]) return BSB_EINVAL;
+    const bool need_dir = mode == BSB_DEEP_PACKED || j == 1;
+    if (!col->deep[j] || !col->exist[j] || (need_dir && !col->block_dir[j])) return BSB_EINVAL;
     h.deep[j] = const_cast<uint8_t*>(col->deep[j]);
     h.exist[j] = const_cast<uint32_t*>(col->exist[j]);
     h.dir[j] = const_cast<int64_t*>(col->block_dir[j]);
@@ -294,6 +331,7 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   BSB_LAUNCH_CHECK();
   // block_dir[j] = [0, inclusive prefix of per-block counts]
   for (int j = 1; j < K; ++j) {
+    if (mode == BSB_DEEP_RANK2 && j > 1) break;  // one shared level-2 directory
     BSB_CUDA(cudaMemsetAsync(h.dir[j], 0, sizeof(int64_t), s));
     size_t tmp_bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, counts + (int64_t)(j - 1) * nbpad,
@@ -306,7 +344,7 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
     BSB_CUDA(cudaFreeAsync(tmp, s));
   }
   if (K > 1) {
-    vbs_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(codes, lens, n, K, dt->deep,
+    vbs_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(codes, lens, n, K, mode, dt->deep,
                                                          (const uint32_t* const*)dt->exist,
                                                          (const int64_t* const*)dt->dir);
     BSB_LAUNCH_CHECK();
@@ -323,5 +361,32 @@ extern "C" int bsb_vbs_export_bs1(const bsb_vbs* col, uint8_t* out, void* stream
   cudaStream_t s = as_stream(stream);
   vbs_export_kernel<<<grid_for(npad, 256), 256, 0, s>>>(col->bs1, npad, out);
   BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}
+
+extern "C" int bsb_vbs_export_level(const bsb_vbs* col, int32_t level, uint8_t* out_bytes,
+                                    int64_t* out_dir, void* stream) {
+  if (!col || !out_bytes || !out_dir || level < 2 || level > col->max_len) return BSB_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  const int64_t n = col->n_rows;
+  const int64_t nb = (n + 31) / 32;
+  int64_t* cnt = nullptr;
+  BSB_CUDA(cudaMallocAsync(&cnt, nb * sizeof(int64_t), s));
+  popc_words_kernel<<<grid_for(nb, 256), 256, 0, s>>>(col->exist[level - 1], nb, cnt);
+  BSB_LAUNCH_CHECK();
+  BSB_CUDA(cudaMemsetAsync(out_dir, 0, sizeof(int64_t), s));
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, out_dir + 1, nb, s);
+  void* tmp = nullptr;
+  BSB_CUDA(cudaMallocAsync(&tmp, tb + 16, s));
+  cub::DeviceScan::InclusiveSum(tmp, tb, cnt, out_dir + 1, nb, s);
+  BSB_LAUNCH_CHECK();
+  const bool rank2 = col->deep_mode == BSB_DEEP_RANK2;
+  vbs_export_level_kernel<<<grid_for(n, 256), 256, 0, s>>>(
+      n, level, col->deep_mode, col->deep[level - 1], col->exist[level - 1], col->exist[1],
+      rank2 ? col->block_dir[1] : col->block_dir[level - 1], out_dir, out_bytes);
+  BSB_LAUNCH_CHECK();
+  BSB_CUDA(cudaFreeAsync(tmp, s));
+  BSB_CUDA(cudaFreeAsync(cnt, s));
   return BSB_OK;
 }

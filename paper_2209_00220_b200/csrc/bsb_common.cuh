@@ -170,6 +170,17 @@ __device__ __forceinline__ uint32_t expand_apply(const ExpandNet& net, uint32_t 
   return x & net.m0;
 }
 
+// Hacker's Delight "compress" (pext) reusing the same stage masks.
+__device__ __forceinline__ uint32_t compress_apply(const ExpandNet& net, uint32_t x) {
+  x &= net.m0;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const uint32_t t = x & net.mv[i];
+    x = (x ^ t) | (t >> (1 << i));
+  }
+  return x;
+}
+
 // Warp-inclusive prefix sum (lane order).
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   const int lane = threadIdx.x & 31;

@@ -46,6 +46,7 @@ struct VbsLookupDesc {
   const uint32_t* exist[kMaxLevels];
   const int64_t* dir[kMaxLevels];
   int K;
+  int mode;
 };
 
 // lookup_vbs (vbs.py:331-371) + decode_padded (dictionary.py:403-411)
@@ -70,13 +71,19 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
     uint64_t code = (uint64_t)__ldg(d.bs1 + (b * 32 + swz(lr))) << (8 * (K - 1));
     const uint32_t below = (1u << lr) - 1u;
     lc[0] += 1;
+    int64_t pos2 = 0;
+    if (d.mode == BSB_DEEP_RANK2 && K >= 2) {
+      const uint32_t w2 = __ldg(d.exist[1] + b);
+      if ((w2 >> lr) & 1u) pos2 = __ldg(d.dir[1] + b) + __popc(w2 & below);
+    }
     for (int j = 2; j <= K; ++j) {
       const uint32_t w = __ldg(d.exist[j - 1] + b);
       if (!((w >> lr) & 1u)) break;  // lengths are nested: no deeper byte
 #pragma unroll
       for (int q = 1; q < kMaxLevels; ++q)
         if (q == j - 1) lc[q] += 1;
-      const int64_t pos = __ldg(d.dir[j - 1] + b) + __popc(w & below);
+      const int64_t pos = d.mode == BSB_DEEP_RANK2 ? pos2
+                                                   : __ldg(d.dir[j - 1] + b) + __popc(w & below);
       code |= (uint64_t)__ldg(d.deep[j - 1] + pos) << (8 * (K - j));
     }
     if (out_padded) out_padded[i] = code;
@@ -237,6 +244,7 @@ extern "C" int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int6
   std::memset(&d, 0, sizeof(d));
   d.bs1 = col->bs1;
   d.K = col->max_len;
+  d.mode = col->deep_mode;
   for (int j = 0; j < kMaxLevels; ++j) {
     d.deep[j] = col->deep[j];
     d.exist[j] = col->exist[j];

@@ -50,7 +50,29 @@ __device__ __forceinline__ void flush_stats(const ScanArgs& a, StatAcc& st) {
               (unsigned long long)s);
 }
 
-template <int LAYOUT, bool BETWEEN, bool STATS>
+template <int LAYOUT>
+__device__ __forceinline__ void fetch_tile(const ScanArgs& a, int64_t tile, int64_t b,
+                                           uint32_t valid, TileIn& t) {
+  if (LAYOUT == BSB_LAYOUT_BYTESLICE)
+    fetch_bs(a.bs, b, valid, t);
+  else
+    fetch_vbs(a.vbs, tile, b, valid, t);
+}
+
+template <bool MASKED>
+__device__ __forceinline__ uint32_t mask_raw(const ScanArgs& a, int64_t b) {
+  if (!MASKED) return kFull;
+  return b < a.nb ? __ldg(a.mask + b) : 0u;
+}
+
+__device__ __forceinline__ uint32_t tile_valid(int64_t tile, int64_t b, int64_t n_rows) {
+  return ((tile + 1) * kTileRows <= n_rows) ? kFull : tail_valid(b, n_rows);
+}
+
+// Persistent grid-stride kernel: one warp per tile, the next tile's level-1
+// operands (and two tiles ahead, its input-mask word) are fetched while the
+// current tile is scanned.
+template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED>
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -62,19 +84,34 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const __grid_constan
     for (int j = 0; j < kMaxLevels; ++j) st.words[j] = st.bytes[j] = 0;
     st.skipped = 0;
   }
-  for (int64_t tile = warp; tile < a.ntiles; tile += nwarps) {
+  int64_t tile = warp;
+  uint32_t vN = 0, mraw = kFull;
+  TileIn inN;
+  if (tile < a.ntiles) {
+    const int64_t b0 = tile * 32 + lane;
+    vN = tile_valid(tile, b0, a.n_rows) & mask_raw<MASKED>(a, b0);
+    fetch_tile<LAYOUT>(a, tile, b0, vN, inN);
+    mraw = mask_raw<MASKED>(a, (tile + nwarps) * 32 + lane);
+  }
+  for (; tile < a.ntiles; tile += nwarps) {
     const int64_t b = tile * 32 + lane;
-    const bool inb = b < a.nb;
-    uint32_t valid = tail_valid(b, a.n_rows);
-    if (a.mask != nullptr && inb) valid &= __ldg(a.mask + b);
-    if (STATS && inb && valid == 0) st.skipped += 1;
+    const uint32_t valid = vN;
+    const TileIn in = inN;
+    const int64_t nt = tile + nwarps;
+    if (nt < a.ntiles) {
+      const int64_t bn = nt * 32 + lane;
+      vN = tile_valid(nt, bn, a.n_rows) & mraw;
+      fetch_tile<LAYOUT>(a, nt, bn, vN, inN);
+      mraw = mask_raw<MASKED>(a, (nt + nwarps) * 32 + lane);
+    }
+    if (STATS && b < a.nb && valid == 0) st.skipped += 1;
     int depth = 0;
     uint32_t res;
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
-      res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, &st, &depth);
+      res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
-      res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, &st, &depth);
-    if (inb) {
+      res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, in, &st, &depth);
+    if (b < a.nb) {
       a.out[b] = res;
       if (STATS && a.depth != nullptr) {
         if (a.depth_max) {
@@ -178,8 +215,12 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   const bool stats = a.stats != nullptr;
   BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
-    if (between) return launch_scan(scan_kernel<LAYOUT, true, false>, a, s);
-    return launch_scan(scan_kernel<LAYOUT, false, false>, a, s);
+    if (a.mask) {
+      if (between) return launch_scan(scan_kernel<LAYOUT, true, false, true>, a, s);
+      return launch_scan(scan_kernel<LAYOUT, false, false, true>, a, s);
+    }
+    if (between) return launch_scan(scan_kernel<LAYOUT, true, false, false>, a, s);
+    return launch_scan(scan_kernel<LAYOUT, false, false, false>, a, s);
   }
   // Stats path: reproduce the reference's two pipelined legs exactly
   // (vbs.py:299-304, stats.py:47-67).
@@ -190,7 +231,8 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   if (!between) {
     a.skipped_slot = 17;
     a.depth_max = 0;
-    int rc = launch_scan(scan_kernel<LAYOUT, false, true>, a, s);
+    int rc = a.mask ? launch_scan(scan_kernel<LAYOUT, false, true, true>, a, s)
+                : launch_scan(scan_kernel<LAYOUT, false, true, false>, a, s);
     BSB_CUDA(cudaStreamSynchronize(s));
     return rc;
   }
@@ -207,7 +249,8 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   BSB_CUDA(cudaMallocAsync(&dummy, 8, s));
   BSB_CUDA(cudaMemsetAsync(dummy, 0, 8, s));
   leg1.count = dummy;
-  int rc = launch_scan(scan_kernel<LAYOUT, false, true>, leg1, s);
+  int rc = leg1.mask ? launch_scan(scan_kernel<LAYOUT, false, true, true>, leg1, s)
+                   : launch_scan(scan_kernel<LAYOUT, false, true, false>, leg1, s);
   if (rc) return rc;
   ScanArgs leg2 = a;
   leg2.A = a.B;
@@ -215,7 +258,7 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   leg2.mask = tmp;
   leg2.skipped_slot = 19;
   leg2.depth_max = 1;
-  rc = launch_scan(scan_kernel<LAYOUT, false, true>, leg2, s);
+  rc = launch_scan(scan_kernel<LAYOUT, false, true, true>, leg2, s);
   if (rc) return rc;
   BSB_CUDA(cudaFreeAsync(tmp, s));
   BSB_CUDA(cudaFreeAsync(dummy, s));
@@ -264,6 +307,7 @@ static void fill_vbs_desc(VbsDesc& d, const bsb_vbs* col) {
   std::memset(&d, 0, sizeof(d));
   d.bs1 = col->bs1;
   d.K = col->max_len;
+  d.mode = col->deep_mode;
   for (int j = 0; j < kMaxLevels; ++j) {
     d.deep[j] = col->deep[j];
     d.exist[j] = col->exist[j];
@@ -332,18 +376,23 @@ __global__ void __launch_bounds__(kScanThreads) conj_kernel(const __grid_constan
   for (int64_t tile = warp; tile < a.ntiles; tile += nwarps) {
     const int64_t b = tile * 32 + lane;
     const bool inb = b < a.nb;
-    uint32_t z = tail_valid(b, a.n_rows);
-    if (a.mask != nullptr && inb) z &= __ldg(a.mask + b);
+    uint32_t z = tile_valid(tile, b, a.n_rows);
+    if (a.mask != nullptr) z &= inb ? __ldg(a.mask + b) : 0u;
     for (int i = 0; i < a.k; ++i) {
       if (!__any_sync(kFull, z != 0)) break;  // whole tile already ruled out
       const ConjItem& it = a.item[i];
+      TileIn in;
       if (it.layout == BSB_LAYOUT_BYTESLICE) {
-        z = it.between ? scan_tile_bs<true, false>(it.bs, it.A, it.B, b, z, nullptr, nullptr)
-                       : scan_tile_bs<false, false>(it.bs, it.A, it.B, b, z, nullptr, nullptr);
-      } else {
+        fetch_bs(it.bs, b, z, in);
         z = it.between
-                ? scan_tile_vbs<true, false>(it.vbs, it.A, it.B, tile, b, z, nullptr, nullptr)
-                : scan_tile_vbs<false, false>(it.vbs, it.A, it.B, tile, b, z, nullptr, nullptr);
+                ? scan_tile_bs<true, false>(it.bs, it.A, it.B, b, z, in, nullptr, nullptr)
+                : scan_tile_bs<false, false>(it.bs, it.A, it.B, b, z, in, nullptr, nullptr);
+      } else {
+        fetch_vbs(it.vbs, tile, b, z, in);
+        z = it.between ? scan_tile_vbs<true, false>(it.vbs, it.A, it.B, tile, b, z, in, nullptr,
+                                                    nullptr)
+                       : scan_tile_vbs<false, false>(it.vbs, it.A, it.B, tile, b, z, in,
+                                                     nullptr, nullptr);
       }
     }
     if (inb) a.out[b] = z;

@@ -11,6 +11,11 @@
 // A fused BETWEEN evaluates GE(lo) and LE(hi) in one pass over the slices;
 // the result equals the reference's pipelined legs (vbs.py:299-304) because
 // hi-leg lanes are only dropped once they are known to fail the lo leg.
+//
+// Latency structure: the caller hands in the tile's level-1 bytes (and for
+// PP-VBS the level-2 existence word and tile bases), prefetched one tile
+// ahead by the persistent kernels.  Each deeper level costs one dependent
+// round trip: its run bytes and the next existence word are issued together.
 #pragma once
 
 #include "bsb_common.cuh"
@@ -36,6 +41,7 @@ struct VbsDesc {
   const uint32_t* exist[kMaxLevels];
   const int64_t* dir[kMaxLevels];
   int32_t K;
+  int32_t mode;  // BSB_DEEP_PACKED / BSB_DEEP_RANK2
 };
 
 // Per-lane statistics accumulators (reference stats.py:18-45).
@@ -53,16 +59,68 @@ __device__ __forceinline__ void stat_level(StatAcc* st, int j, int64_t nbytes) {
   }
 }
 
+// Level-1 operands of one tile, fetched ahead of use.
+struct TileIn {
+  uint32_t w[8];   // the lane's 32 swizzled bytes of level 1
+  uint32_t m2;     // PP-VBS: existence word of level 2 (every lane)
+  int64_t base;    // PP-VBS packed: lane i holds dir[i+2][tile*32]; rank2: dir2[tile*32]
+};
+
+__device__ __forceinline__ void fetch_bs(const BsDesc& d, int64_t b, uint32_t valid, TileIn& t) {
+  if (valid) {
+    ldg256(d.slices + b * 32, t.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t.w[i] = 0;
+  }
+}
+
+__device__ __forceinline__ void fetch_vbs(const VbsDesc& d, int64_t tile, int64_t b,
+                                          uint32_t valid, TileIn& t) {
+  const int lane = threadIdx.x & 31;
+  if (valid) {
+    ldg256(d.bs1 + b * 32, t.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t.w[i] = 0;
+  }
+  t.m2 = d.K >= 2 ? __ldg(d.exist[1] + b) : 0u;
+  if (d.mode == BSB_DEEP_RANK2)
+    t.base = d.K >= 2 ? __ldg(d.dir[1] + tile * 32) : 0;
+  else
+    t.base = (lane + 2 <= d.K) ? __ldg(d.dir[lane + 1] + tile * 32) : 0;
+}
+
 // ---------------------------------------------------------------- ByteSlice
-// Returns the lane's result word.  `depth_out` (STATS) = deepest level loaded.
 template <bool BETWEEN, bool STATS>
 __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, const Leg& B,
-                                                 int64_t b, uint32_t valid, StatAcc* st,
-                                                 int* depth_out) {
+                                                 int64_t b, uint32_t valid, const TileIn& in,
+                                                 StatAcc* st, int* depth_out) {
   uint32_t zeqA = valid, zgtA = 0, zeqB = valid, zgtB = 0;
   int depth = 0;
+  // level 1: every lane, branch free (invalid lanes carry zero state)
+  {
+    uint32_t gA, eA, gB, eB;
+    if (BETWEEN && A.byte[0] != B.byte[0]) {
+      cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+    } else {
+      cmp_block(in.w, A.lv[0], gA, eA);
+      gB = gA;
+      eB = eA;
+    }
+    if (STATS && valid) {
+      depth = 1;
+      stat_level<STATS>(st, 0, 32);
+    }
+    zgtA = zeqA & gA;
+    zeqA &= eA & ~gA;
+    if (BETWEEN) {
+      zgtB = zeqB & gB;
+      zeqB &= eB & ~gB & (zeqA | zgtA);  // drop lanes already known to fail GE(lo)
+    }
+  }
   const uint8_t* base = d.slices + b * 32;
-  for (int j = 0; j < d.K; ++j) {
+  for (int j = 1; j < d.K; ++j) {
     const bool act = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
     if (!__any_sync(kFull, act)) break;
     if (act) {
@@ -79,12 +137,10 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
         } else {
           cmp_block2(w, A.lv[j], B.lv[j], gA, eA, gB, eB);
         }
-        eA &= ~gA;
-        eB &= ~gB;
         zgtA |= zeqA & gA;
-        zeqA &= eA;
+        zeqA &= eA & ~gA;
         zgtB |= zeqB & gB;
-        zeqB &= eB & (zeqA | zgtA);  // drop lanes already known to fail GE(lo)
+        zeqB &= eB & ~gB & (zeqA | zgtA);
       } else {
         uint32_t g, e;
         cmp_block(w, A.lv[j], g, e);
@@ -100,6 +156,7 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
 
 // ------------------------------------------------------------------ PP-VBS
 // Transition after comparing level j (1-based) -- reference vbs.py:272-284.
+// Works on row-space masks and, unchanged, on packed deep-row masks.
 __device__ __forceinline__ void vbs_transition(int j, int len, int K, uint32_t g, uint32_t e,
                                                uint32_t nxt, uint32_t& zeq, uint32_t& zgt,
                                                uint32_t& eqf) {
@@ -119,122 +176,211 @@ __device__ __forceinline__ void vbs_transition(int j, int len, int K, uint32_t g
   }
 }
 
-// Load the packed level bytes [start, start+cnt) of one block as u32 words.
-__device__ __forceinline__ void load_run(const uint8_t* deep, int64_t start, int cnt,
-                                         uint32_t (&R)[8]) {
+// Packed bytes [start, start+cnt) of one block: up to five 8-byte aligned
+// loads, then byte alignment with PRMT on demand.
+struct Run {
+  uint32_t u[10];
+  uint32_t sel;
+  int qs;
+};
+__device__ __forceinline__ void load_run(const uint8_t* deep, int64_t start, int cnt, bool act,
+                                         Run& r) {
   const uint64_t* p = reinterpret_cast<const uint64_t*>(deep + (start & ~int64_t(7)));
   const int o = (int)(start & 7);
-  const int nld = (o + cnt + 7) >> 3;
-  uint64_t q[5];
+  const int nld = act ? ((o + cnt + 7) >> 3) : 0;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) q[k] = (k < nld) ? __ldg(p + k) : 0ull;
-  const unsigned sh = 8u * o;
+  for (int k = 0; k < 5; ++k) {
+    const uint64_t v = (k < nld) ? __ldg(p + k) : 0ull;
+    r.u[2 * k] = (uint32_t)v;
+    r.u[2 * k + 1] = (uint32_t)(v >> 32);
+  }
+  r.qs = o >> 2;
+  r.sel = 0x3210u + 0x1111u * (uint32_t)(o & 3);
+}
+__device__ __forceinline__ uint32_t run_word(const Run& r, int i) {
+  const uint32_t a = r.qs ? r.u[i + 1] : r.u[i];
+  const uint32_t b = r.qs ? r.u[i + 2] : r.u[i + 1];
+  return __byte_perm(a, b, r.sel);
+}
+
+// Packed compare of a run (nwmax uniform words) against one or two literal
+// bytes; bits >= cnt are garbage and masked by the caller.
+template <bool TWO>
+__device__ __forceinline__ void cmp_run(const Run& r, int nwmax, LevelLit A, LevelLit B,
+                                        uint32_t& gA, uint32_t& eA, uint32_t& gB,
+                                        uint32_t& eB) {
+  uint32_t ga = 0, ea = 0, gb = 0, eb = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint64_t v = sh ? ((q[i] >> sh) | (q[i + 1] << (64u - sh))) : q[i];
-    R[2 * i] = (uint32_t)v;
-    R[2 * i + 1] = (uint32_t)(v >> 32);
+  for (int i = 0; i < 8; ++i) {
+    if (i >= nwmax) break;
+    const uint32_t w = run_word(r, i);
+    const uint32_t ev = __byte_perm(w, 0, 0x4240);
+    const uint32_t od = __byte_perm(w, 0, 0x4341);
+    ga |= nib4(__byte_perm(ev + A.cgt, od + A.cgt, 0x7351)) << (4 * i);
+    ea |= nib4(__byte_perm(ev + A.cge, od + A.cge, 0x7351)) << (4 * i);
+    if (TWO) {
+      gb |= nib4(__byte_perm(ev + B.cgt, od + B.cgt, 0x7351)) << (4 * i);
+      eb |= nib4(__byte_perm(ev + B.cge, od + B.cge, 0x7351)) << (4 * i);
+    }
+  }
+  gA = ga;
+  eA = ea & ~ga;
+  if (TWO) {
+    gB = gb;
+    eB = eb & ~gb;
+  } else {
+    gB = ga;
+    eB = eA;
   }
 }
 
+// Level 1 of PP-VBS (all lanes, branch free) + its transitions.
 template <bool BETWEEN, bool STATS>
-__device__ __forceinline__ uint32_t scan_tile_vbs(const VbsDesc& d, const Leg& A,
-                                                  const Leg& B, int64_t tile, int64_t b,
-                                                  uint32_t valid, StatAcc* st,
-                                                  int* depth_out) {
+__device__ __forceinline__ void vbs_level1(const Leg& A, const Leg& B, int K, uint32_t valid,
+                                           const TileIn& in, uint32_t& zeqA, uint32_t& zgtA,
+                                           uint32_t& eqfA, uint32_t& zeqB, uint32_t& zgtB,
+                                           uint32_t& eqfB, StatAcc* st, int& depth) {
+  uint32_t gA, eA, gB, eB;
+  if (BETWEEN && A.byte[0] != B.byte[0]) {
+    cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+  } else {
+    cmp_block(in.w, A.lv[0], gA, eA);
+    gB = gA;
+    eB = eA;
+  }
+  eA &= ~gA;
+  eB &= ~gB;
+  if (STATS && valid) {
+    depth = 1;
+    stat_level<STATS>(st, 0, 32);
+  }
+  vbs_transition(1, A.len, K, gA, eA, in.m2, zeqA, zgtA, eqfA);
+  if (BETWEEN) {
+    vbs_transition(1, B.len, K, gB, eB, in.m2, zeqB, zgtB, eqfB);
+    zeqB &= zeqA | zgtA | eqfA;
+  }
+}
+
+// PP-VBS, deep slices in reference packing (one expand per level).
+template <bool BETWEEN, bool STATS>
+__device__ __forceinline__ uint32_t scan_tile_vbs_packed(const VbsDesc& d, const Leg& A,
+                                                         const Leg& B, int64_t tile, int64_t b,
+                                                         uint32_t valid, const TileIn& in,
+                                                         StatAcc* st, int* depth_out) {
   const int K = d.K;
   uint32_t zeqA = valid, zgtA = 0, eqfA = 0;
   uint32_t zeqB = valid, zgtB = 0, eqfB = 0;
   const int maxlen = BETWEEN ? (A.len > B.len ? A.len : B.len) : A.len;
   int depth = 0;
-  uint32_t mcur = 0;  // existence word of the current level (all lanes)
-
-  for (int j = 1; j <= maxlen; ++j) {
+  vbs_level1<BETWEEN, STATS>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB, st, depth);
+  uint32_t mcur = in.m2;
+  for (int j = 2; j <= maxlen; ++j) {
     const bool act = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
     if (!__any_sync(kFull, act)) break;
-    uint32_t gA = 0, eA = 0, gB = 0, eB = 0;
-    if (j == 1) {
-      if (act) {
-        uint32_t w[8];
-        ldg256(d.bs1 + b * 32, w);
-        depth = 1;
-        stat_level<STATS>(st, 0, 32);
-        if (BETWEEN && A.byte[0] != B.byte[0]) {
-          cmp_block2(w, A.lv[0], B.lv[0], gA, eA, gB, eB);
-        } else {
-          cmp_block(w, A.lv[0], gA, eA);
-          gB = gA;
-          eB = eA;
-        }
-        eA &= ~gA;
-        eB &= ~gB;
-      }
-    } else {
-      // bytes of this block at level j: BS_j[dir_j[tile*32] + prefix .. + cnt)
-      const int cnt = __popc(mcur);
-      const uint32_t incl = warp_incl_scan((uint32_t)cnt);
-      const int64_t base = __ldg(d.dir[j - 1] + tile * 32);
-      const int64_t start = base + (int64_t)(incl - cnt);
-      const int nw = (cnt + 3) >> 2;
-      const int nwmax = __reduce_max_sync(kFull, act ? nw : 0);
-      if (act) {
-        depth = j;
-        stat_level<STATS>(st, j - 1, cnt);
-        uint32_t R[8];
-        load_run(d.deep[j - 1], start, cnt, R);
-        uint32_t pgA = 0, peA = 0, pgB = 0, peB = 0;
-        const bool same = !BETWEEN || (A.byte[j - 1] == B.byte[j - 1]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < nwmax) {
-            uint32_t g4, e4;
-            cmp_word_packed(R[i], A.lv[j - 1], g4, e4);
-            pgA |= g4 << (4 * i);
-            peA |= e4 << (4 * i);
-            if (BETWEEN && !same) {
-              cmp_word_packed(R[i], B.lv[j - 1], g4, e4);
-              pgB |= g4 << (4 * i);
-              peB |= e4 << (4 * i);
-            }
-          }
-        }
-        const uint32_t lowm = cnt >= 32 ? kFull : ((1u << cnt) - 1u);
-        pgA &= lowm;
-        peA &= lowm & ~pgA;
-        const ExpandNet net = expand_setup(mcur);
-        gA = pgA ? expand_apply(net, pgA) : 0u;
-        eA = peA ? expand_apply(net, peA) : 0u;
-        if (BETWEEN) {
-          if (same) {
-            gB = gA;
-            eB = eA;
-          } else {
-            pgB &= lowm;
-            peB &= lowm & ~pgB;
-            gB = pgB ? expand_apply(net, pgB) : 0u;
-            eB = peB ? expand_apply(net, peB) : 0u;
-          }
-        }
-      }
-    }
-    // existence word of level j+1 for every lane (transition + next prefix)
-    uint32_t nxt = 0;
-    if (j < K) {
-      const uint32_t* ex = d.exist[j];
-      nxt = (valid != 0 || true) ? __ldg(ex + b) : 0u;
+    const int cnt = __popc(mcur);
+    const uint32_t incl = warp_incl_scan((uint32_t)cnt);
+    const int64_t start = __shfl_sync(kFull, in.base, j - 2) + (int64_t)(incl - cnt);
+    Run run;
+    load_run(d.deep[j - 1], start, cnt, act, run);
+    const uint32_t nxt = (j < K) ? __ldg(d.exist[j] + b) : 0u;
+    const int nwmax = __reduce_max_sync(kFull, act ? ((cnt + 3) >> 2) : 0);
+    uint32_t pgA, peA, pgB, peB;
+    if (BETWEEN && A.byte[j - 1] != B.byte[j - 1])
+      cmp_run<true>(run, nwmax, A.lv[j - 1], B.lv[j - 1], pgA, peA, pgB, peB);
+    else
+      cmp_run<false>(run, nwmax, A.lv[j - 1], A.lv[j - 1], pgA, peA, pgB, peB);
+    const uint32_t lowm = cnt >= 32 ? kFull : ((1u << cnt) - 1u);
+    const ExpandNet net = expand_setup(mcur);
+    const uint32_t gA = expand_apply(net, pgA & lowm), eA = expand_apply(net, peA & lowm);
+    uint32_t gB = gA, eB = eA;
+    if (BETWEEN) {
+      gB = expand_apply(net, pgB & lowm);
+      eB = expand_apply(net, peB & lowm);
     }
     if (act) {
-      vbs_transition(j, A.len, K, gA, eA, nxt, zeqA, zgtA, eqfA);
-      if (BETWEEN) {
-        vbs_transition(j, B.len, K, gB, eB, nxt, zeqB, zgtB, eqfB);
-        zeqB &= zeqA | zgtA | eqfA;  // drop lanes known to fail GE(lo)
-      }
+      depth = j;
+      stat_level<STATS>(st, j - 1, cnt);
+    }
+    vbs_transition(j, A.len, K, gA, eA, nxt, zeqA, zgtA, eqfA);
+    if (BETWEEN) {
+      vbs_transition(j, B.len, K, gB, eB, nxt, zeqB, zgtB, eqfB);
+      zeqB &= zeqA | zgtA | eqfA;
     }
     mcur = nxt;
   }
   if (STATS) *depth_out = depth;
   if (BETWEEN) return valid & (zgtA | eqfA) & ~zgtB;
   return finalize_op(A.op, zgtA, eqfA, valid);
+}
+
+// PP-VBS, deep slices in level-2 rank space (BSB_DEEP_RANK2): all deep levels
+// share one packed space per block, so the row-space <-> packed conversion
+// (one butterfly setup) happens once per block instead of once per level.
+template <bool BETWEEN, bool STATS>
+__device__ __forceinline__ uint32_t scan_tile_vbs_rank2(const VbsDesc& d, const Leg& A,
+                                                        const Leg& B, int64_t tile, int64_t b,
+                                                        uint32_t valid, const TileIn& in,
+                                                        StatAcc* st, int* depth_out) {
+  const int K = d.K;
+  uint32_t zeqA = valid, zgtA = 0, eqfA = 0;
+  uint32_t zeqB = valid, zgtB = 0, eqfB = 0;
+  const int maxlen = BETWEEN ? (A.len > B.len ? A.len : B.len) : A.len;
+  int depth = 0;
+  vbs_level1<BETWEEN, STATS>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB, st, depth);
+  const bool any_deep = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
+  if (maxlen >= 2 && __any_sync(kFull, any_deep)) {
+    const ExpandNet net = expand_setup(in.m2);
+    uint32_t pzA = compress_apply(net, zeqA);
+    uint32_t pzB = BETWEEN ? compress_apply(net, zeqB) : 0u;
+    // deep rows already known to pass GE(lo) at level 1 (row-space results)
+    const uint32_t passA1 = BETWEEN ? compress_apply(net, zgtA | eqfA) : 0u;
+    uint32_t pgtA = 0, peqA = 0, pgtB = 0, peqB = 0;
+    const int c2 = __popc(in.m2);
+    const uint32_t incl = warp_incl_scan((uint32_t)c2);
+    const int64_t start = in.base + (int64_t)(incl - c2);
+    const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
+    const int nwmax = __reduce_max_sync(kFull, any_deep ? ((c2 + 3) >> 2) : 0);
+    int rc = c2;  // bytes of the current level (reference accounting)
+    for (int j = 2; j <= maxlen; ++j) {
+      const bool act = BETWEEN ? ((pzA | pzB) != 0) : (pzA != 0);
+      if (!__any_sync(kFull, act)) break;
+      Run run;
+      load_run(d.deep[j - 1], start, c2, act, run);
+      const uint32_t mnext = (j < K && act) ? __ldg(d.exist[j] + b) : 0u;
+      uint32_t pgA, peA, pgB, peB;
+      if (BETWEEN && A.byte[j - 1] != B.byte[j - 1])
+        cmp_run<true>(run, nwmax, A.lv[j - 1], B.lv[j - 1], pgA, peA, pgB, peB);
+      else
+        cmp_run<false>(run, nwmax, A.lv[j - 1], A.lv[j - 1], pgA, peA, pgB, peB);
+      const uint32_t rnext = compress_apply(net, mnext);  // M_{j+1} in packed space
+      if (act) {
+        depth = j;
+        stat_level<STATS>(st, j - 1, rc);
+      }
+      rc = __popc(rnext);
+      vbs_transition(j, A.len, K, pgA & lowm, peA & lowm, rnext, pzA, pgtA, peqA);
+      if (BETWEEN) {
+        vbs_transition(j, B.len, K, pgB & lowm, peB & lowm, rnext, pzB, pgtB, peqB);
+        pzB &= pzA | pgtA | peqA | passA1;
+      }
+    }
+    zgtA |= expand_apply(net, pgtA);
+    eqfA |= expand_apply(net, peqA);
+    if (BETWEEN) zgtB |= expand_apply(net, pgtB);
+  }
+  if (STATS) *depth_out = depth;
+  if (BETWEEN) return valid & (zgtA | eqfA) & ~zgtB;
+  return finalize_op(A.op, zgtA, eqfA, valid);
+}
+
+template <bool BETWEEN, bool STATS>
+__device__ __forceinline__ uint32_t scan_tile_vbs(const VbsDesc& d, const Leg& A,
+                                                  const Leg& B, int64_t tile, int64_t b,
+                                                  uint32_t valid, const TileIn& in,
+                                                  StatAcc* st, int* depth_out) {
+  if (d.mode == BSB_DEEP_RANK2)
+    return scan_tile_vbs_rank2<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
+  return scan_tile_vbs_packed<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
 }
 
 }  // namespace bsb

@@ -40,6 +40,7 @@ class VbsColumn:
     exist: list                           # exist[j]: int32 [stride/32] words of slice j+1
     block_dir: list                       # block_dir[j]: int64 [stride/32 + 1]
     level_rows: list                      # rows owning byte j (j = 1..K), reference counts
+    deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED or DEEP_RANK2 (see header)
     _desc: _lib.BsbVbs = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -47,12 +48,14 @@ class VbsColumn:
         d.n_rows = self.n_rows
         d.stride = self.stride
         d.max_len = self.max_len
+        d.deep_mode = self.deep_mode
         d.bs1 = self.bs1.data_ptr()
         for j in range(1, self.max_len):
             d.deep[j] = self.deep[j].data_ptr()
             d.exist[j] = self.exist[j].data_ptr()
-            d.block_dir[j] = self.block_dir[j].data_ptr()
-            d.deep_len[j] = self.level_rows[j]
+            if self.block_dir[j] is not None:
+                d.block_dir[j] = self.block_dir[j].data_ptr()
+            d.deep_len[j] = self.deep[j].numel() - DEEP_PAD
         self._desc = d
 
     @property
@@ -74,9 +77,18 @@ class VbsColumn:
         _lib.check(_lib.load().bsb_vbs_export_bs1(self.desc_ref, first.data_ptr(), stream()),
                    "export")
         out = [first.cpu().numpy()]
-        for j in range(1, self.max_len):
-            out.append(self.deep[j][: self.level_rows[j]].cpu().numpy())
+        for j in range(2, self.max_len + 1):
+            out.append(self._export_level(j)[0])
         return out
+
+    def _export_level(self, j: int):
+        """Reference packing (bytes, block_dir) of slice j, from either mode."""
+        nb = self.n_blocks
+        by = torch.empty(max(self.level_rows[j - 1], 1), dtype=torch.uint8, device=self.bs1.device)
+        dr = torch.empty(nb + 1, dtype=torch.int64, device=self.bs1.device)
+        _lib.check(_lib.load().bsb_vbs_export_level(self.desc_ref, j, by.data_ptr(),
+                                                    dr.data_ptr(), stream()), "export")
+        return by[: self.level_rows[j - 1]].cpu().numpy(), dr.cpu().numpy()
 
     def mask_words(self, j: int) -> np.ndarray:
         """Existence words of slice j (j >= 2), one per block (vbs.py:58-61)."""
@@ -88,13 +100,31 @@ class VbsColumn:
 
     @property
     def block_dir_host(self) -> np.ndarray:
+        """Reference block directory (K-1, nb+1) int64 (vbs.py:95, :105-106)."""
         nb = self.n_blocks
-        rows = [self.block_dir[j][: nb + 1].cpu().numpy() for j in range(1, self.max_len)]
+        rows = [self._export_level(j)[1] for j in range(2, self.max_len + 1)]
         return np.stack(rows) if rows else np.zeros((0, nb + 1), np.int64)
 
 
-def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES) -> VbsColumn:
-    """vbs.py:68-114 on the device: plan (validate, K, level sizes) + build."""
+RANK2_MAX_OVERHEAD = 1.25
+
+
+def choose_deep_mode(level_rows, K: int) -> int:
+    """RANK2 stores every deep slice with one byte per deep row; use it when
+    the pad bytes cost at most 25% over the reference packing."""
+    if K <= 2:
+        return _lib.DEEP_RANK2
+    exact = sum(int(level_rows[j]) for j in range(1, K))
+    padded = (K - 1) * int(level_rows[1])
+    return _lib.DEEP_RANK2 if padded <= RANK2_MAX_OVERHEAD * exact else _lib.DEEP_PACKED
+
+
+def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
+              deep_mode: str = "auto") -> VbsColumn:
+    """vbs.py:68-114 on the device: plan (validate, K, level sizes) + build.
+
+    deep_mode: "auto" | "packed" (reference packing) | "rank2" (one byte per
+    deep row in every deep slice; see include/bytestore_b200.h)."""
     lanes.require_device()
     codes = row_codes if isinstance(row_codes, torch.Tensor) else np.asarray(row_codes)
     lens = row_lengths if isinstance(row_lengths, torch.Tensor) else np.asarray(row_lengths)
@@ -118,13 +148,22 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES) -> VbsC
     stride = int(lib.bsb_stride_for(n))
     nbpad = stride // 32
     dev = device()
+    level_rows = [int(x) for x in lr[:K]]
+    if deep_mode == "auto":
+        mode = choose_deep_mode(level_rows, K)
+    elif deep_mode in ("packed", "rank2"):
+        mode = _lib.DEEP_PACKED if deep_mode == "packed" else _lib.DEEP_RANK2
+    else:
+        raise ValueError(f"unknown deep_mode {deep_mode!r}")
     bs1 = torch.empty(stride, dtype=torch.uint8, device=dev)
     deep, exist, bdir = [None], [None], [None]
     for j in range(1, K):
-        deep.append(torch.empty(int(lr[j]) + DEEP_PAD, dtype=torch.uint8, device=dev))
+        size = level_rows[1] if mode == _lib.DEEP_RANK2 else level_rows[j]
+        deep.append(torch.empty(size + DEEP_PAD, dtype=torch.uint8, device=dev))
         exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
-        bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev))
-    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, [int(x) for x in lr[:K]])
+        need_dir = mode == _lib.DEEP_PACKED or j == 1
+        bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev) if need_dir else None)
+    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode)
     _lib.check(lib.bsb_vbs_build(dc.data_ptr(), dl.data_ptr(), col.desc_ref, stream()),
                "build_vbs")
     return col

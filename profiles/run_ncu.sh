@@ -13,10 +13,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'bsb|scan|con
     --csv --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
 # timed-region launches: skip the stats/parity-guard launches (8 stats legs x2 for
 # BETWEEN + 8 parity) and the warm-up step; capture one of each layout's kernel
-ncu --set full --clock-control none --import-source on \
-    -k regex:'scan_kernel<1, 1, 0>' -s 4 -c 1 -o "$OUT/prof_vbs" $CMD \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k regex:'scan_kernel<.int.1, .bool.1, .bool.0>' -s 4 -c 1 -o "$OUT/prof_vbs" $CMD \
     > "$OUT/ncu_vbs.log" 2>&1
-ncu --set full --clock-control none --import-source on \
-    -k regex:'scan_kernel<0, 1, 0>' -s 4 -c 1 -o "$OUT/prof_bs" $CMD \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k regex:'scan_kernel<.int.0, .bool.1, .bool.0>' -s 4 -c 1 -o "$OUT/prof_bs" $CMD \
     > "$OUT/ncu_bs.log" 2>&1
 echo done

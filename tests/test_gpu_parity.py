@@ -140,10 +140,11 @@ def test_byteslice_errors():
 # ----------------------------------------------------------------- PP-VBS
 
 
-def test_vbs_golden():
+@pytest.mark.parametrize("mode", ["packed", "rank2"])
+def test_vbs_golden(mode):
     data, meta = load("vbs")
     for ci, m in enumerate(meta):
-        col = B.build_vbs(data[f"{ci}/codes"], data[f"{ci}/lens"])
+        col = B.build_vbs(data[f"{ci}/codes"], data[f"{ci}/lens"], deep_mode=mode)
         K = col.max_len
         assert K == m["K"]
         sl = col.slices
@@ -176,12 +177,13 @@ def _ppe_column(s, d, n, seed):
     return vals, od, codes, lens
 
 
-def test_vbs_zipf_between_windows_vs_oracle():
+@pytest.mark.parametrize("mode", ["packed", "rank2"])
+def test_vbs_zipf_between_windows_vs_oracle(mode):
     """cfg2-shaped (Zipf 1.2 over 2^20, scaled to 2^20 rows), the four
     BETWEEN windows of SURVEY.md §8(d), fused single pass vs oracle legs."""
     n = 1 << 20
     vals, od, codes, lens = _ppe_column(1.2, 20, n, 42)
-    col = B.build_vbs(codes, lens)
+    col = B.build_vbs(codes, lens, deep_mode=mode)
     ocol = O.vbs_build(codes, lens)
     srt = np.sort(vals)
     q = lambda x: int(srt[min(n - 1, int(x * n))])  # noqa: E731
@@ -195,7 +197,8 @@ def test_vbs_zipf_between_windows_vs_oracle():
                               O.naive_filter(vals, "BETWEEN", q(1 - p - mm), q(1 - mm)))
 
 
-def test_vbs_random_codes_all_ops_masks_vs_oracle():
+@pytest.mark.parametrize("mode", ["packed", "rank2"])
+def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
     rng = np.random.default_rng(77)
     for n, K in ((50_001, 3), (20_000, 8), (3000, 5), (33, 2), (1, 1)):
         lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
@@ -205,7 +208,7 @@ def test_vbs_random_codes_all_ops_masks_vs_oracle():
         for k in range(8):
             use = lens > k
             codes[use] |= byts[use, k] << np.uint64(8 * k)
-        col = B.build_vbs(codes, lens)
+        col = B.build_vbs(codes, lens, deep_mode=mode)
         ocol = O.vbs_build(codes, lens)
         mw = O.bools_to_words(rng.random(n) < 0.5)
         for _ in range(4):
@@ -231,10 +234,11 @@ def test_vbs_random_codes_all_ops_masks_vs_oracle():
             assert st.block_depth.tolist() == st_w.block_depth.tolist()
 
 
-def test_vbs_row_lookup_decode_vs_oracle():
+@pytest.mark.parametrize("mode", ["packed", "rank2"])
+def test_vbs_row_lookup_decode_vs_oracle(mode):
     n = 200_000
     vals, od, codes, lens = _ppe_column(1.0, 20, n, 4)
-    col = B.build_vbs(codes, lens)
+    col = B.build_vbs(codes, lens, deep_mode=mode)
     ocol = O.vbs_build(codes, lens)
     rng = np.random.default_rng(6)
     rows = rng.integers(0, n, size=100_000)
