@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--rows-log2", type=int, default=28)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--deep-mode", default="auto",
+                    help="PP-VBS deep layout: auto|packed|rank2|planes|sliced")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clocks/e2e/cpu baseline")
     return ap.parse_args()
@@ -110,7 +112,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- column build
-def build_cfg2(n: int):
+def build_cfg2(n: int, deep_mode: str = "auto"):
     """Generate + encode the cfg2 column on the device (untimed)."""
     import torch
 
@@ -129,7 +131,7 @@ def build_cfg2(n: int):
     d_ppe = Dictionary.build(table, "prefix_preserving")
     d_fix = Dictionary.build(table, "fixed")
     codes, lens = d_ppe.row_codes_device(ranks)
-    col_v = build_vbs(codes, lens)
+    col_v = build_vbs(codes, lens, deep_mode=deep_mode)
     col_b = build_byteslice(ranks, d_fix.assignment.width_bits)
     del codes, lens
     torch.cuda.synchronize()
@@ -279,7 +281,7 @@ def run_b200(args):
     _lib.load()
 
     n = 1 << args.rows_log2
-    data = build_cfg2(n)
+    data = build_cfg2(n, args.deep_mode)
     col_v, col_b = data["col_v"], data["col_b"]
     table = data["table"]
     wins = window_bounds(table.values, table.weights, n)
@@ -429,9 +431,13 @@ def col_bytes(col) -> int:
         return col.planes.numel()
     b = col.bs1.numel()
     for j in range(1, col.max_len):
-        b += col.deep[j].numel() + col.exist[j].numel() * 4
+        if col.deep[j] is not None:
+            b += col.deep[j].numel() * col.deep[j].element_size()
+        b += col.exist[j].numel() * 4
         if col.block_dir[j] is not None:
             b += col.block_dir[j].numel() * 8
+        if col.rexist is not None and col.rexist[j] is not None:
+            b += col.rexist[j].numel() * 4
     return b
 
 
@@ -454,6 +460,11 @@ def measure_e2e(data, scans, steps, n, world):
                 continue
             host_v.append(t.cpu().pin_memory())
             dev_v.append(torch.empty_like(t))
+    host_r, dev_r = [None], [None]
+    for j in range(1, col_v.max_len):
+        t = col_v.rexist[j] if col_v.rexist is not None else None
+        host_r.append(None if t is None else t.cpu().pin_memory())
+        dev_r.append(None if t is None else torch.empty_like(t))
     host_b = col_b.planes.cpu().pin_memory()
     dev_b = torch.empty_like(col_b.planes)
     K = col_v.max_len
@@ -461,12 +472,12 @@ def measure_e2e(data, scans, steps, n, world):
                    [None] + [dev_v[1 + 3 * (j - 1)] for j in range(1, K)],
                    [None] + [dev_v[2 + 3 * (j - 1)] for j in range(1, K)],
                    [None] + [dev_v[3 + 3 * (j - 1)] for j in range(1, K)], col_v.level_rows,
-                   col_v.deep_mode)
+                   col_v.deep_mode, dev_r)
     cb = ByteSliceColumn(col_b.n_rows, col_b.width_bits, col_b.lanes, col_b.stride, dev_b)
     nw = -(-n // 32)
     out_h = [torch.empty(nw, dtype=torch.int32).pin_memory() for _ in scans]
     cnt_h = torch.empty(len(scans), dtype=torch.int64).pin_memory()
-    pairs = [(h, d) for h, d in zip(host_v, dev_v) if h is not None]
+    pairs = [(h, d) for h, d in zip(host_v + host_r, dev_v + dev_r) if h is not None]
     h2d = sum(h.numel() * h.element_size() for h, _ in pairs) + host_b.numel()
     d2h = len(scans) * (nw * 4 + 8)
 

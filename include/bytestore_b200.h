@@ -91,10 +91,23 @@ typedef struct bsb_byteslice {
  *             level hold a 0 pad byte.  All levels share block_dir[1] (the
  *             level-2 directory); block_dir[j>1] are unused.  The scan then
  *             works in one packed space per block for all deep levels.
+ *  BSB_DEEP_PLANES (2): like RANK2 but levels are paired into big-endian
+ *             uint16 planes indexed by deep row: deep[p+1] = plane p holding
+ *             bytes (2p+2, 2p+3) (p = 0..ceil((max_len-1)/2)-1, 0-padded);
+ *             rexist[j] (j = 2..max_len-1) = bitmap over deep rows of "code
+ *             has byte j+1".  Scanned cooperatively, one deep row per lane.
+ *  BSB_DEEP_SLICED (3): the deep rows form their own ByteSlice-like column:
+ *             deep[j] (j = 1..max_len-1) holds byte j+1 of every deep row in
+ *             32-deep-row "deep blocks", swizzled like bs1 (0-padded for rows
+ *             without that byte); rexist[j] (j = 2..max_len-1) holds one uint32
+ *             per deep block: bit i = deep row 32k+i has byte j+1.  Scanned with
+ *             the ByteSlice SWAR compare, one lane per deep block.
  * deep allocations are padded by >= 64 bytes.  Index 0 of deep/exist/
- * block_dir is unused (level 1 is bs1). */
+ * block_dir/rexist is unused (level 1 is bs1). */
 #define BSB_DEEP_PACKED 0
 #define BSB_DEEP_RANK2 1
+#define BSB_DEEP_PLANES 2
+#define BSB_DEEP_SLICED 3
 typedef struct bsb_vbs {
   int64_t n_rows;
   int64_t stride;
@@ -105,6 +118,7 @@ typedef struct bsb_vbs {
   const uint32_t* exist[BSB_MAX_LEVELS];
   const int64_t* block_dir[BSB_MAX_LEVELS];
   int64_t deep_len[BSB_MAX_LEVELS];
+  const uint32_t* rexist[BSB_MAX_LEVELS];
 } bsb_vbs;
 
 /* One column reference for the fused conjunction (engine.py:322-332). */

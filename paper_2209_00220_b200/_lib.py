@@ -25,7 +25,7 @@ STATS_WORDS = 24
 OK, EINVAL, ERANGE, ENOTFOUND, ECUDA, EKEY = 0, 1, 2, 3, 4, 5
 OP_CODES = {"EQ": 0, "NE": 1, "LT": 2, "LE": 3, "GT": 4, "GE": 5, "BETWEEN": 6}
 LAYOUT_BYTESLICE, LAYOUT_PPVBS = 0, 1
-DEEP_PACKED, DEEP_RANK2 = 0, 1
+DEEP_PACKED, DEEP_RANK2, DEEP_PLANES, DEEP_SLICED = 0, 1, 2, 3
 
 
 class BsbPred(ctypes.Structure):
@@ -42,7 +42,7 @@ class BsbVbs(ctypes.Structure):
     _fields_ = [("n_rows", c_int64), ("stride", c_int64), ("max_len", c_int32),
                 ("deep_mode", c_int32), ("bs1", c_void_p), ("deep", c_void_p * MAX_LEVELS),
                 ("exist", c_void_p * MAX_LEVELS), ("block_dir", c_void_p * MAX_LEVELS),
-                ("deep_len", c_int64 * MAX_LEVELS)]
+                ("deep_len", c_int64 * MAX_LEVELS), ("rexist", c_void_p * MAX_LEVELS)]
 
 
 class BsbColumnRef(ctypes.Structure):

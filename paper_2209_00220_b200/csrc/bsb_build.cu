@@ -160,7 +160,7 @@ __global__ void vbs_exist_kernel(const uint64_t* __restrict__ codes,
 __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
                                    const uint8_t* __restrict__ lens, int64_t n, int K, int mode,
                                    uint8_t* const* deep, const uint32_t* const* exist,
-                                   const int64_t* const* dir) {
+                                   const int64_t* const* dir, uint32_t* const* rexist) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const unsigned l = lens[r];
@@ -173,6 +173,26 @@ __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
       const int64_t pos = dir[1][b] + __popc(exist[1][b] & below);
       for (int j = 2; j <= K; ++j)
         deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
+    } else if (mode == BSB_DEEP_SLICED) {
+      // deep rows as a swizzled ByteSlice column + per-deep-block existence words
+      const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
+      const int64_t pos = (q & ~int64_t(31)) + swz((int)(q & 31));
+      for (int j = 2; j <= K; ++j)
+        deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
+      for (int j = 3; j <= (int)l; ++j)
+        atomicOr(rexist[j - 1] + (q >> 5), 1u << (q & 31));
+    } else if (mode == BSB_DEEP_PLANES) {
+      // big-endian uint16 planes of bytes (2p+2, 2p+3) + deep-row existence bitmaps
+      const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
+      const int np = K >> 1;
+      for (int p = 0; p < np; ++p) {
+        const int jh = 2 * p + 2, jl = 2 * p + 3;
+        const uint32_t hi = jh <= (int)l ? (uint32_t)((c >> (8 * (l - jh))) & 0xFF) : 0u;
+        const uint32_t lo = jl <= (int)l ? (uint32_t)((c >> (8 * (l - jl))) & 0xFF) : 0u;
+        reinterpret_cast<uint16_t*>(deep[p + 1])[q] = (uint16_t)((hi << 8) | lo);
+      }
+      for (int j = 3; j <= (int)l; ++j)
+        atomicOr(rexist[j - 1] + (q >> 5), 1u << (q & 31));
     } else {
       for (int j = 2; j <= (int)l; ++j) {
         const uint32_t w = exist[j - 1][b];
@@ -197,9 +217,18 @@ __global__ void vbs_export_level_kernel(int64_t n, int level, int mode,
     const uint32_t below = (1u << (r & 31)) - 1u;
     const uint32_t w = exist_l[b];
     if (!((w >> (r & 31)) & 1u)) continue;
-    const int64_t src = mode == BSB_DEEP_RANK2 ? dir_src[b] + __popc(exist_2[b] & below)
-                                               : dir_src[b] + __popc(w & below);
-    out[ref_dir[b] + __popc(w & below)] = deep_l[src];
+    const int64_t src = mode != BSB_DEEP_PACKED ? dir_src[b] + __popc(exist_2[b] & below)
+                                                : dir_src[b] + __popc(w & below);
+    uint8_t byte;
+    if (mode == BSB_DEEP_SLICED) {
+      byte = deep_l[(src & ~int64_t(31)) + swz((int)(src & 31))];
+    } else if (mode == BSB_DEEP_PLANES) {
+      const uint16_t v = reinterpret_cast<const uint16_t*>(deep_l)[src];
+      byte = ((level - 2) & 1) ? (uint8_t)(v & 0xFF) : (uint8_t)(v >> 8);
+    } else {
+      byte = deep_l[src];
+    }
+    out[ref_dir[b] + __popc(w & below)] = byte;
   }
 }
 
@@ -221,6 +250,7 @@ struct PtrTable {
   uint8_t* deep[kMaxLevels];
   uint32_t* exist[kMaxLevels];
   int64_t* dir[kMaxLevels];
+  uint32_t* rexist[kMaxLevels];
 };
 
 }  // namespace bsb
@@ -312,13 +342,18 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   PtrTable h;
   std::memset(&h, 0, sizeof(h));
   const int mode = col->deep_mode;
-  if (mode != BSB_DEEP_PACKED && mode != BSB_DEEP_RANK2) return BSB_EINVAL;
+  if (mode < BSB_DEEP_PACKED || mode > BSB_DEEP_SLICED) return BSB_EINVAL;
   for (int j = 1; j < K; ++j) {
     const bool need_dir = mode == BSB_DEEP_PACKED || j == 1;
-    if (!col->deep[j] || !col->exist[j] || (need_dir && !col->block_dir[j])) return BSB_EINVAL;
+    const bool need_deep = mode != BSB_DEEP_PLANES || j <= (K >> 1);
+    const bool need_rex = (mode == BSB_DEEP_PLANES || mode == BSB_DEEP_SLICED) && j >= 2;
+    if ((need_deep && !col->deep[j]) || !col->exist[j] || (need_dir && !col->block_dir[j]) ||
+        (need_rex && !col->rexist[j]))
+      return BSB_EINVAL;
     h.deep[j] = const_cast<uint8_t*>(col->deep[j]);
     h.exist[j] = const_cast<uint32_t*>(col->exist[j]);
     h.dir[j] = const_cast<int64_t*>(col->block_dir[j]);
+    h.rexist[j] = const_cast<uint32_t*>(col->rexist[j]);
   }
   PtrTable* dt = nullptr;
   int64_t* counts = nullptr;
@@ -331,7 +366,7 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   BSB_LAUNCH_CHECK();
   // block_dir[j] = [0, inclusive prefix of per-block counts]
   for (int j = 1; j < K; ++j) {
-    if (mode == BSB_DEEP_RANK2 && j > 1) break;  // one shared level-2 directory
+    if (mode != BSB_DEEP_PACKED && j > 1) break;  // one shared level-2 directory
     BSB_CUDA(cudaMemsetAsync(h.dir[j], 0, sizeof(int64_t), s));
     size_t tmp_bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, counts + (int64_t)(j - 1) * nbpad,
@@ -346,7 +381,8 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   if (K > 1) {
     vbs_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(codes, lens, n, K, mode, dt->deep,
                                                          (const uint32_t* const*)dt->exist,
-                                                         (const int64_t* const*)dt->dir);
+                                                         (const int64_t* const*)dt->dir,
+                                                         dt->rexist);
     BSB_LAUNCH_CHECK();
   }
   BSB_CUDA(cudaFreeAsync(counts, s));
@@ -381,10 +417,12 @@ extern "C" int bsb_vbs_export_level(const bsb_vbs* col, int32_t level, uint8_t* 
   BSB_CUDA(cudaMallocAsync(&tmp, tb + 16, s));
   cub::DeviceScan::InclusiveSum(tmp, tb, cnt, out_dir + 1, nb, s);
   BSB_LAUNCH_CHECK();
-  const bool rank2 = col->deep_mode == BSB_DEEP_RANK2;
+  const bool shared_dir = col->deep_mode != BSB_DEEP_PACKED;
+  const uint8_t* src = col->deep_mode == BSB_DEEP_PLANES ? col->deep[((level - 2) >> 1) + 1]
+                                                         : col->deep[level - 1];
   vbs_export_level_kernel<<<grid_for(n, 256), 256, 0, s>>>(
-      n, level, col->deep_mode, col->deep[level - 1], col->exist[level - 1], col->exist[1],
-      rank2 ? col->block_dir[1] : col->block_dir[level - 1], out_dir, out_bytes);
+      n, level, col->deep_mode, src, col->exist[level - 1], col->exist[1],
+      shared_dir ? col->block_dir[1] : col->block_dir[level - 1], out_dir, out_bytes);
   BSB_LAUNCH_CHECK();
   BSB_CUDA(cudaFreeAsync(tmp, s));
   BSB_CUDA(cudaFreeAsync(cnt, s));

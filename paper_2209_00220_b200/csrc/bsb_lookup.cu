@@ -72,7 +72,7 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
     const uint32_t below = (1u << lr) - 1u;
     lc[0] += 1;
     int64_t pos2 = 0;
-    if (d.mode == BSB_DEEP_RANK2 && K >= 2) {
+    if (d.mode != BSB_DEEP_PACKED && K >= 2) {
       const uint32_t w2 = __ldg(d.exist[1] + b);
       if ((w2 >> lr) & 1u) pos2 = __ldg(d.dir[1] + b) + __popc(w2 & below);
     }
@@ -82,9 +82,18 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
 #pragma unroll
       for (int q = 1; q < kMaxLevels; ++q)
         if (q == j - 1) lc[q] += 1;
-      const int64_t pos = d.mode == BSB_DEEP_RANK2 ? pos2
-                                                   : __ldg(d.dir[j - 1] + b) + __popc(w & below);
-      code |= (uint64_t)__ldg(d.deep[j - 1] + pos) << (8 * (K - j));
+      uint64_t byte;
+      if (d.mode == BSB_DEEP_SLICED) {
+        byte = __ldg(d.deep[j - 1] + ((pos2 & ~int64_t(31)) + swz((int)(pos2 & 31))));
+      } else if (d.mode == BSB_DEEP_PLANES) {
+        const uint16_t v = __ldg(reinterpret_cast<const uint16_t*>(d.deep[((j - 2) >> 1) + 1]) + pos2);
+        byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
+      } else {
+        const int64_t pos = d.mode == BSB_DEEP_RANK2 ? pos2
+                                                     : __ldg(d.dir[j - 1] + b) + __popc(w & below);
+        byte = __ldg(d.deep[j - 1] + pos);
+      }
+      code |= byte << (8 * (K - j));
     }
     if (out_padded) out_padded[i] = code;
     if (sorted_padded) {

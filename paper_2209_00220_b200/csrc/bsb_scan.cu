@@ -73,7 +73,8 @@ __device__ __forceinline__ uint32_t tile_valid(int64_t tile, int64_t b, int64_t 
 // operands (and two tiles ahead, its input-mask word) are fetched while the
 // current tile is scanned.
 template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
+    scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const __grid_constan
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
       res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
-      res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, in, &st, &depth);
+      res = scan_tile_vbs<BETWEEN, STATS, LAYOUT - 1>(a.vbs, a.A, a.B, tile, b, valid, in, &st,
+                                                     &depth);
     if (b < a.nb) {
       a.out[b] = res;
       if (STATS && a.depth != nullptr) {
@@ -155,11 +157,11 @@ static void fill_leg(Leg& L, int op, uint64_t code, int len, int levels) {
   std::memset(&L, 0, sizeof(L));
   L.op = op;
   L.len = len;
-  for (int j = 0; j < kMaxLevels; ++j) {
+  for (int j = 0; j <= kMaxLevels; ++j) {
     uint32_t byte = 0;
     if (j < levels) byte = (uint32_t)((code >> (8 * (levels - 1 - j))) & 0xFF);
     L.byte[j] = byte;
-    L.lv[j] = make_level_lit(byte);
+    if (j < kMaxLevels) L.lv[j] = make_level_lit(byte);
   }
 }
 
@@ -312,7 +314,26 @@ static void fill_vbs_desc(VbsDesc& d, const bsb_vbs* col) {
     d.deep[j] = col->deep[j];
     d.exist[j] = col->exist[j];
     d.dir[j] = col->block_dir[j];
+    d.rexist[j] = col->rexist[j];
   }
+}
+
+namespace bsb {
+int vbs_rows_scan(const VbsDesc& d, int64_t n_rows, const bsb_pred* p, const uint32_t* mask,
+                  uint32_t* out, uint64_t* count, int64_t* stats, int8_t* depth,
+                  cudaStream_t s);
+int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B, bool between,
+                    const uint32_t* mask, uint32_t* out, unsigned long long* count,
+                    cudaStream_t s);
+}
+
+// The cooperative plane scan needs every multi-byte literal to end in a
+// non-zero byte (always true for dictionary codes).
+static bool planes_fast_ok(const bsb_pred* p) {
+  auto ok = [](uint64_t code, int len) { return len < 2 || (code & 0xFF) != 0; };
+  if (p->trivial >= 0) return true;
+  if (p->op == BSB_BETWEEN) return ok(p->code, p->length) && ok(p->code2, p->length2);
+  return ok(p->code, p->length);
 }
 
 extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
@@ -345,7 +366,20 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
   a.count = reinterpret_cast<unsigned long long*>(count);
   a.stats = stats;
   a.depth = depth;
-  return scan_dispatch<BSB_LAYOUT_PPVBS>(a, pred, K, s);
+  if ((col->deep_mode == BSB_DEEP_PLANES && (stats != nullptr || !planes_fast_ok(pred))) ||
+      (col->deep_mode == BSB_DEEP_SLICED && stats != nullptr))
+    return vbs_rows_scan(a.vbs, a.n_rows, pred, mask, out_words, count, stats, depth, s);
+  switch (col->deep_mode) {
+    case BSB_DEEP_PACKED: return scan_dispatch<1 + BSB_DEEP_PACKED>(a, pred, K, s);
+    case BSB_DEEP_RANK2: return scan_dispatch<1 + BSB_DEEP_RANK2>(a, pred, K, s);
+    case BSB_DEEP_PLANES:
+      return K <= 5 ? scan_dispatch<1 + BSB_DEEP_PLANES>(a, pred, K, s)
+                    : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
+    case BSB_DEEP_SLICED:
+      return vbs_sliced_scan(a.vbs, a.n_rows, a.A, a.B, pred->op == BSB_BETWEEN, mask,
+                             out_words, a.count, s);
+    default: return BSB_EINVAL;
+  }
 }
 
 // ------------------------------------------------------ fused conjunction
@@ -405,12 +439,43 @@ __global__ void __launch_bounds__(kScanThreads) conj_kernel(const __grid_constan
 
 }  // namespace bsb
 
+// Chain of single scans, each fed the previous result (engine.py:322-332);
+// used when a predicate cannot run inside the fused kernel.
+static int conj_chain(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
+                      const uint32_t* mask, uint32_t* out_words, uint64_t* count,
+                      int64_t nb, cudaStream_t s) {
+  uint32_t* tmp = nullptr;
+  BSB_CUDA(cudaMallocAsync(&tmp, (size_t)nb * 4 + 4, s));
+  const uint32_t* running = mask;
+  for (int i = 0; i < k; ++i) {
+    // the last scan writes out_words; earlier ones alternate through tmp/out
+    uint32_t* dst = ((k - 1 - i) % 2 == 0) ? out_words : tmp;
+    int rc = cols[i].layout == BSB_LAYOUT_BYTESLICE
+                 ? bsb_byteslice_scan(cols[i].byteslice, &preds[i], running, dst, count,
+                                      nullptr, nullptr, s)
+                 : bsb_vbs_scan(cols[i].vbs, &preds[i], running, dst, count, nullptr,
+                                nullptr, s);
+    if (rc) return rc;
+    running = dst;
+  }
+  BSB_CUDA(cudaFreeAsync(tmp, s));
+  return BSB_OK;
+}
+
 extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
                              const uint32_t* mask, uint32_t* out_words, uint64_t* count,
                              void* stream) {
   if (k < 0 || k > BSB_MAX_CONJ || (k > 0 && (!cols || !preds)) || !out_words || !count)
     return BSB_EINVAL;
   cudaStream_t s = as_stream(stream);
+  for (int i = 0; i < k; ++i) {
+    if (cols[i].layout == BSB_LAYOUT_PPVBS && cols[i].vbs &&
+        cols[i].vbs->deep_mode == BSB_DEEP_PLANES && !planes_fast_ok(&preds[i])) {
+      const int64_t n = cols[0].layout == BSB_LAYOUT_BYTESLICE ? cols[0].byteslice->n_rows
+                                                               : cols[0].vbs->n_rows;
+      return conj_chain(k, cols, preds, mask, out_words, count, (n + 31) / 32, s);
+    }
+  }
   ConjArgs a;
   std::memset(&a, 0, sizeof(a));
   int64_t n = -1;

@@ -1,0 +1,291 @@
+// bsb_vbs_sliced.cu -- PP-VBS scan for the SLICED deep layout, three tiles
+// per warp iteration.
+//
+// Phase 1 (lane = row block, one tile after another): level 1 with the SWAR
+// compare on the prefetched first-slice sector and the reference transitions
+// (vbs.py:258-284); the tied rows of each block are compressed into deep-row
+// order (one butterfly set-up per block) and OR-ed into per-deep-block
+// candidate words; the block's level-1 state and butterfly masks go to shared
+// memory.
+// Phase 2 (lane = deep block): the super-tile's deep rows form ~27 deep
+// blocks for the cfg2 column, so the warp runs Alg. 3 levels 2..len over them
+// at ~85% lane utilisation: one 256-bit load + SWAR compare per live deep
+// block per level, early stop per deep block, transitions with the deep-row
+// existence words.
+// Phase 3 (lane = row block): each block expands its window of the deep
+// results back to row space, finalises the operator and writes its word.
+#include <cstdlib>
+#include <cstring>
+
+#include "bsb_scan_impl.cuh"
+
+namespace bsb {
+
+constexpr int kSuperTiles = 3;                    // tiles per warp iteration
+constexpr int kSuperBlocks = kSuperTiles * 32;    // row blocks per iteration
+constexpr int kMaxDeepBlocks = kSuperBlocks + 4;  // deep blocks touched (+ guard)
+constexpr int kSlicedThreads = 256;
+constexpr int kSlicedWarps = kSlicedThreads / 32;
+
+struct SlicedArgs {
+  int64_t n_rows, nb, ntiles;
+  VbsDesc d;
+  Leg A, B;
+  const uint32_t* mask;
+  uint32_t* out;
+  unsigned long long* count;
+};
+
+struct SlicedSmem {
+  // per row block: level-1 state + butterfly stage masks
+  uint32_t valid[kSuperBlocks], zgtA[kSuperBlocks], eqfA[kSuperBlocks], zeqA[kSuperBlocks];
+  uint32_t zgtB[kSuperBlocks], zeqB[kSuperBlocks], m2[kSuperBlocks], off[kSuperBlocks];
+  uint32_t mv[5][kSuperBlocks];
+  // per deep block: candidates in, results out
+  uint32_t cA[kMaxDeepBlocks], cB[kMaxDeepBlocks], rP[kMaxDeepBlocks], rQ[kMaxDeepBlocks];
+};
+
+template <bool BETWEEN, bool MASKED, int MINB>
+__global__ void __launch_bounds__(kSlicedThreads, MINB)
+    vbs_sliced_kernel(const __grid_constant__ SlicedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SlicedSmem& sm = reinterpret_cast<SlicedSmem*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const VbsDesc& d = a.d;
+  const int K = d.K;
+  const Leg& A = a.A;
+  const Leg& B = a.B;
+  const int lenA = A.len, lenB = BETWEEN ? B.len : 0;
+  const int maxlen = lenA > lenB ? lenA : lenB;
+  const int64_t nsuper = (a.ntiles + kSuperTiles - 1) / kSuperTiles;
+  unsigned long long cnt = 0;
+
+  auto tile_valid_word = [&](int64_t tile, int64_t b) -> uint32_t {
+    if (tile >= a.ntiles) return 0u;
+    uint32_t v = ((tile + 1) * kTileRows <= a.n_rows) ? kFull : tail_valid(b, a.n_rows);
+    if (MASKED) v &= b < a.nb ? __ldg(a.mask + b) : 0u;
+    return v;
+  };
+
+  // prefetch pipeline over the flattened tile sequence of this warp
+  int64_t st = warp;
+  int u = 0;
+  TileIn inN;
+  uint32_t vN = 0;
+  if (st < nsuper) {
+    const int64_t t0 = st * kSuperTiles;
+    vN = tile_valid_word(t0, t0 * 32 + lane);
+    fetch_vbs(d, t0 < a.ntiles ? t0 : 0, t0 * 32 + lane, vN, inN);
+  }
+  for (; st < nsuper; st += nwarps) {
+    int64_t dfirst = 0;  // global deep row of the super-tile's first deep row
+    int64_t db0 = 0;
+    int soff = 0;        // running deep-row offset from db0 * 32
+    // ---------------- phase 1: level 1, three tiles
+    for (u = 0; u < kSuperTiles; ++u) {
+      const int64_t tile = st * kSuperTiles + u;
+      const int64_t b = tile * 32 + lane;
+      const uint32_t valid = vN;
+      const TileIn in = inN;
+      // prefetch the next tile in this warp's sequence
+      int64_t ntile = (u + 1 < kSuperTiles) ? tile + 1 : (st + nwarps) * kSuperTiles;
+      if (ntile < a.ntiles) {
+        vN = tile_valid_word(ntile, ntile * 32 + lane);
+        fetch_vbs(d, ntile, ntile * 32 + lane, vN, inN);
+      } else {
+        vN = 0;
+        inN.m2 = 0;  // past the column: no deep rows
+      }
+      uint32_t zeqA = valid, zgtA = 0, eqfA = 0, zeqB = valid, zgtB = 0, eqfB = 0;
+      int depth = 0;
+      vbs_level1<BETWEEN, false>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB,
+                                 nullptr, depth);
+      const int c2 = __popc(in.m2);
+      const uint32_t incl = warp_incl_scan((uint32_t)c2);
+      if (u == 0) {
+        dfirst = __shfl_sync(kFull, in.base, 0);
+        db0 = dfirst >> 5;
+        soff = (int)(dfirst & 31);
+      }
+      const int o = soff + (int)(incl - (uint32_t)c2);
+      const ExpandNet net = expand_setup(in.m2);
+      const uint32_t pA = compress_apply(net, zeqA);
+      const uint32_t pB = BETWEEN ? compress_apply(net, zeqB) : 0u;
+      const int i = u * 32 + lane;
+      sm.valid[i] = valid;
+      sm.zgtA[i] = zgtA;
+      sm.eqfA[i] = eqfA;
+      sm.zeqA[i] = zeqA;
+      sm.zgtB[i] = zgtB;
+      sm.zeqB[i] = zeqB;
+      sm.m2[i] = in.m2;
+      sm.off[i] = (uint32_t)o;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sm.mv[k][i] = net.mv[k];
+      if (u == 0) {
+        for (int k = lane; k < kMaxDeepBlocks; k += 32) {
+          sm.cA[k] = 0;
+          sm.cB[k] = 0;
+        }
+      }
+      __syncwarp();
+      const int wi = o >> 5, sb = o & 31;
+      const bool spill = sb != 0 && sb + c2 > 32;
+      if (pA && wi < kMaxDeepBlocks) {
+        atomicOr(&sm.cA[wi], pA << sb);
+        if (spill && wi + 1 < kMaxDeepBlocks) atomicOr(&sm.cA[wi + 1], pA >> (32 - sb));
+      }
+      if (BETWEEN && pB && wi < kMaxDeepBlocks) {
+        atomicOr(&sm.cB[wi], pB << sb);
+        if (spill && wi + 1 < kMaxDeepBlocks) atomicOr(&sm.cB[wi + 1], pB >> (32 - sb));
+      }
+      soff += (int)__shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    // ---------------- phase 2: deep blocks, one per lane
+    const int ndt = (soff + 31) >> 5;
+    if (maxlen >= 2) {
+      for (int t0 = 0; t0 < ndt; t0 += 32) {
+        const int t = t0 + lane;
+        const bool has = t < ndt && t < kMaxDeepBlocks;
+        uint32_t zA = has ? sm.cA[t] : 0u, zB = (BETWEEN && has) ? sm.cB[t] : 0u;
+        uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
+        const int64_t dbk = db0 + t;
+        for (int j = 2; j <= maxlen; ++j) {
+          const bool act = BETWEEN ? ((zA | zB) != 0) : (zA != 0);
+          if (!__any_sync(kFull, act)) break;
+          uint32_t w[8];
+          if (act) {
+            ldg256(d.deep[j - 1] + dbk * 32, w);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) w[q] = 0;
+          }
+          const uint32_t nxt = (j < K && act) ? __ldg(d.rexist[j] + dbk) : 0u;
+          uint32_t gA, eA, gB, eB;
+          if (BETWEEN && A.byte[j - 1] != B.byte[j - 1]) {
+            cmp_block2(w, A.lv[j - 1], B.lv[j - 1], gA, eA, gB, eB);
+          } else {
+            cmp_block(w, A.lv[j - 1], gA, eA);
+            gB = gA;
+            eB = eA;
+          }
+          eA &= ~gA;
+          eB &= ~gB;
+          vbs_transition(j, lenA, K, gA, eA, nxt, zA, gtA, eqA);
+          if (BETWEEN) vbs_transition(j, lenB, K, gB, eB, nxt, zB, gtB, eqB);
+        }
+        if (has) {
+          sm.rP[t] = BETWEEN ? (gtA | eqA) : gtA;
+          sm.rQ[t] = BETWEEN ? gtB : eqA;
+        }
+      }
+    }
+    for (int k = ndt + lane; k < kMaxDeepBlocks; k += 32) {
+      sm.rP[k] = 0;
+      sm.rQ[k] = 0;
+    }
+    __syncwarp();
+    // ---------------- phase 3: back to row space
+#pragma unroll 1
+    for (u = 0; u < kSuperTiles; ++u) {
+      const int64_t tile = st * kSuperTiles + u;
+      if (tile >= a.ntiles) break;
+      const int64_t b = tile * 32 + lane;
+      const int i = u * 32 + lane;
+      const uint32_t valid = sm.valid[i];
+      uint32_t zgtA = sm.zgtA[i], eqfA = sm.eqfA[i], zgtB = sm.zgtB[i];
+      const uint32_t zeqA = sm.zeqA[i], zeqB = sm.zeqB[i];
+      if (maxlen >= 2) {
+        const uint32_t m2 = sm.m2[i];
+        const int o = (int)sm.off[i];
+        const int c2 = __popc(m2);
+        const int wi = o >> 5, sb = o & 31;
+        const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
+        uint32_t pP = 0, pQ = 0;
+        if (wi + 1 < kMaxDeepBlocks) {
+          pP = __funnelshift_r(sm.rP[wi], sm.rP[wi + 1], sb) & lowm;
+          pQ = __funnelshift_r(sm.rQ[wi], sm.rQ[wi + 1], sb) & lowm;
+        }
+        ExpandNet net;
+        net.m0 = m2;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) net.mv[k] = sm.mv[k][i];
+        const uint32_t eP = expand_apply(net, pP), eQ = expand_apply(net, pQ);
+        if (BETWEEN) {
+          zgtA |= zeqA & eP;
+          zgtB |= zeqB & eQ;
+        } else {
+          zgtA |= zeqA & eP;
+          eqfA |= zeqA & eQ;
+        }
+      }
+      const uint32_t res = BETWEEN ? (valid & (zgtA | eqfA) & ~zgtB)
+                                   : finalize_op(A.op, zgtA, eqfA, valid);
+      if (b < a.nb) a.out[b] = res;
+      cnt += __popc(res);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int dd = 16; dd > 0; dd >>= 1) cnt += __shfl_xor_sync(kFull, cnt, dd);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
+template <bool BETWEEN, bool MASKED, int MINB>
+static int launch_sliced_k(const SlicedArgs& a, cudaStream_t s) {
+  auto kern = vbs_sliced_kernel<BETWEEN, MASKED, MINB>;
+  const size_t smem = sizeof(SlicedSmem) * kSlicedWarps;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSlicedThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t nsuper = (a.ntiles + kSuperTiles - 1) / kSuperTiles;
+  int64_t want = (nsuper + kSlicedWarps - 1) / kSlicedWarps;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  kern<<<grid, kSlicedThreads, smem, s>>>(a);
+  BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}
+
+// Occupancy variant: 4 resident CTAs (64 registers) by default;
+// BSB_SLICED_MINB=3 selects the 80-register build (tuning experiments).
+template <bool BETWEEN, bool MASKED>
+static int launch_sliced(const SlicedArgs& a, cudaStream_t s) {
+  static int minb = -1;
+  if (minb < 0) {
+    const char* e = std::getenv("BSB_SLICED_MINB");
+    minb = (e && std::atoi(e) == 3) ? 3 : 4;
+  }
+  if (minb == 3) return launch_sliced_k<BETWEEN, MASKED, 3>(a, s);
+  return launch_sliced_k<BETWEEN, MASKED, 4>(a, s);
+}
+
+// Non-stats scan of a SLICED column (BETWEEN fused).  Legs as in ScanArgs.
+int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B, bool between,
+                    const uint32_t* mask, uint32_t* out, unsigned long long* count,
+                    cudaStream_t s) {
+  SlicedArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_rows = n_rows;
+  a.nb = (n_rows + 31) / 32;
+  a.ntiles = (a.nb + 31) / 32;
+  a.d = d;
+  a.A = A;
+  a.B = B;
+  a.mask = mask;
+  a.out = out;
+  a.count = count;
+  BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
+  if (between) return mask ? launch_sliced<true, true>(a, s) : launch_sliced<true, false>(a, s);
+  return mask ? launch_sliced<false, true>(a, s) : launch_sliced<false, false>(a, s);
+}
+
+}  // namespace bsb

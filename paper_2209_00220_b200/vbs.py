@@ -40,7 +40,8 @@ class VbsColumn:
     exist: list                           # exist[j]: int32 [stride/32] words of slice j+1
     block_dir: list                       # block_dir[j]: int64 [stride/32 + 1]
     level_rows: list                      # rows owning byte j (j = 1..K), reference counts
-    deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED or DEEP_RANK2 (see header)
+    deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED / DEEP_RANK2 / DEEP_PLANES (header)
+    rexist: list = None                   # PLANES: deep-row bitmaps of byte j+1 (j>=2)
     _desc: _lib.BsbVbs = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -51,11 +52,14 @@ class VbsColumn:
         d.deep_mode = self.deep_mode
         d.bs1 = self.bs1.data_ptr()
         for j in range(1, self.max_len):
-            d.deep[j] = self.deep[j].data_ptr()
+            if self.deep[j] is not None:
+                d.deep[j] = self.deep[j].data_ptr()
+                d.deep_len[j] = self.deep[j].numel() * self.deep[j].element_size() - DEEP_PAD
             d.exist[j] = self.exist[j].data_ptr()
             if self.block_dir[j] is not None:
                 d.block_dir[j] = self.block_dir[j].data_ptr()
-            d.deep_len[j] = self.deep[j].numel() - DEEP_PAD
+            if self.rexist is not None and self.rexist[j] is not None:
+                d.rexist[j] = self.rexist[j].data_ptr()
         self._desc = d
 
     @property
@@ -109,14 +113,21 @@ class VbsColumn:
 RANK2_MAX_OVERHEAD = 1.25
 
 
+SLICED_MAX_OVERHEAD = 1.30
+
+
 def choose_deep_mode(level_rows, K: int) -> int:
-    """RANK2 stores every deep slice with one byte per deep row; use it when
-    the pad bytes cost at most 25% over the reference packing."""
-    if K <= 2:
-        return _lib.DEEP_RANK2
+    """SLICED (deep rows as their own swizzled ByteSlice column; the fastest
+    scan, measured on B200) when its pad bytes cost <= 30% over the reference
+    packing -- true for PPE dictionaries, whose deep codes are mostly full
+    length -- else the reference packing.  RANK2 / PLANES stay selectable."""
+    if K < 2:
+        return _lib.DEEP_PACKED
     exact = sum(int(level_rows[j]) for j in range(1, K))
-    padded = (K - 1) * int(level_rows[1])
-    return _lib.DEEP_RANK2 if padded <= RANK2_MAX_OVERHEAD * exact else _lib.DEEP_PACKED
+    cnt2 = int(level_rows[1])
+    if (K - 1) * (-(-cnt2 // 32) * 32) <= SLICED_MAX_OVERHEAD * exact:
+        return _lib.DEEP_SLICED
+    return _lib.DEEP_PACKED
 
 
 def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
@@ -124,7 +135,8 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
     """vbs.py:68-114 on the device: plan (validate, K, level sizes) + build.
 
     deep_mode: "auto" | "packed" (reference packing) | "rank2" (one byte per
-    deep row in every deep slice; see include/bytestore_b200.h)."""
+    deep row in every deep slice) | "planes" (paired uint16 levels per deep
+    row); see include/bytestore_b200.h."""
     lanes.require_device()
     codes = row_codes if isinstance(row_codes, torch.Tensor) else np.asarray(row_codes)
     lens = row_lengths if isinstance(row_lengths, torch.Tensor) else np.asarray(row_lengths)
@@ -149,21 +161,38 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
     nbpad = stride // 32
     dev = device()
     level_rows = [int(x) for x in lr[:K]]
+    modes = {"packed": _lib.DEEP_PACKED, "rank2": _lib.DEEP_RANK2, "planes": _lib.DEEP_PLANES,
+             "sliced": _lib.DEEP_SLICED}
     if deep_mode == "auto":
         mode = choose_deep_mode(level_rows, K)
-    elif deep_mode in ("packed", "rank2"):
-        mode = _lib.DEEP_PACKED if deep_mode == "packed" else _lib.DEEP_RANK2
+    elif deep_mode in modes:
+        mode = modes[deep_mode] if K >= 2 else _lib.DEEP_PACKED
     else:
         raise ValueError(f"unknown deep_mode {deep_mode!r}")
     bs1 = torch.empty(stride, dtype=torch.uint8, device=dev)
-    deep, exist, bdir = [None], [None], [None]
+    deep, exist, bdir, rex = [None], [None], [None], [None]
+    cnt2 = level_rows[1] if K >= 2 else 0
     for j in range(1, K):
-        size = level_rows[1] if mode == _lib.DEEP_RANK2 else level_rows[j]
-        deep.append(torch.empty(size + DEEP_PAD, dtype=torch.uint8, device=dev))
+        if mode == _lib.DEEP_SLICED:
+            # byte j+1 of every deep row, swizzled 32-deep-row blocks
+            deep.append(torch.zeros(-(-cnt2 // 32) * 32 + DEEP_PAD, dtype=torch.uint8,
+                                    device=dev))
+            rex.append(torch.zeros(cnt2 // 32 + 2, dtype=torch.int32, device=dev)
+                       if j >= 2 else None)
+        elif mode == _lib.DEEP_PLANES:
+            # plane j-1 (bytes 2j, 2j+1) for j <= K//2; uint16 per deep row
+            deep.append(torch.empty(cnt2 + DEEP_PAD, dtype=torch.int16, device=dev)
+                        if j <= K // 2 else None)
+            rex.append(torch.zeros(cnt2 // 32 + 2, dtype=torch.int32, device=dev)
+                       if j >= 2 else None)
+        else:
+            size = cnt2 if mode == _lib.DEEP_RANK2 else level_rows[j]
+            deep.append(torch.empty(size + DEEP_PAD, dtype=torch.uint8, device=dev))
+            rex.append(None)
         exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
         need_dir = mode == _lib.DEEP_PACKED or j == 1
         bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev) if need_dir else None)
-    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode)
+    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode, rex)
     _lib.check(lib.bsb_vbs_build(dc.data_ptr(), dl.data_ptr(), col.desc_ref, stream()),
                "build_vbs")
     return col

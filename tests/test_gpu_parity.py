@@ -140,7 +140,7 @@ def test_byteslice_errors():
 # ----------------------------------------------------------------- PP-VBS
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2"])
+@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_golden(mode):
     data, meta = load("vbs")
     for ci, m in enumerate(meta):
@@ -177,7 +177,7 @@ def _ppe_column(s, d, n, seed):
     return vals, od, codes, lens
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2"])
+@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_zipf_between_windows_vs_oracle(mode):
     """cfg2-shaped (Zipf 1.2 over 2^20, scaled to 2^20 rows), the four
     BETWEEN windows of SURVEY.md §8(d), fused single pass vs oracle legs."""
@@ -197,7 +197,7 @@ def test_vbs_zipf_between_windows_vs_oracle(mode):
                               O.naive_filter(vals, "BETWEEN", q(1 - p - mm), q(1 - mm)))
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2"])
+@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
     rng = np.random.default_rng(77)
     for n, K in ((50_001, 3), (20_000, 8), (3000, 5), (33, 2), (1, 1)):
@@ -234,7 +234,7 @@ def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
             assert st.block_depth.tolist() == st_w.block_depth.tolist()
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2"])
+@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_row_lookup_decode_vs_oracle(mode):
     n = 200_000
     vals, od, codes, lens = _ppe_column(1.0, 20, n, 4)
