@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--rows-log2", type=int, default=28)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lookup", action="store_true")
+    ap.add_argument("--lookup-steps", type=int, default=10)
     ap.add_argument("--deep-mode", default="auto",
                     help="PP-VBS deep layout: auto|packed|rank2|planes|sliced")
     ap.add_argument("--profile", action="store_true",
@@ -388,6 +390,10 @@ def run_b200(args):
     out = None
     if rank == 0:
         e2e = None if args.profile else measure_e2e(data, scans, args.e2e_steps, n, world)
+        lookups = None
+        if not args.profile and not args.no_lookup:
+            torch.cuda.empty_cache()
+            lookups = measure_lookups(max(3, args.lookup_steps), args.rows_log2)
         cpu = None
         if world == 1 and not args.profile and not args.no_cpu_baseline:
             cpu = cpu_baseline(n, 1 << 22, os.cpu_count() or 1)
@@ -412,6 +418,7 @@ def run_b200(args):
             "layouts": {k: {"gcodes_s": round(v["gcodes_s"], 2), "hbm_gbs": round(v["gbs"], 1),
                             "frac": round(v["frac"], 4), "windows": v["windows"]}
                         for k, v in by_layout.items()},
+            "lookup": lookups,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": len(scans) * args.steps,
@@ -423,6 +430,118 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return out
+
+
+def measure_lookups(steps: int, log2n: int = 28):
+    """cfg3 (BASELINE.json configs[2]): 2^28-row ByteSlice column of 24-bit
+    uniform codes (identity codes = values) and a 2^28-row Zipf(1.0)/2^20
+    PP-VBS column; lookups of 2^24 random row ids (unsorted and sorted) and of
+    the rows selected by 1% / 20% random bitvectors, reconstructing int32
+    values (PP-VBS: fused decode through the dictionary).  Seeds follow
+    SURVEY.md §8(d)."""
+    import torch
+
+    from paper_2209_00220_b200 import ColumnKind, Dictionary, FrequencyTable, ZipfSpec
+    from paper_2209_00220_b200.bitvector import DeviceBitVector
+    from paper_2209_00220_b200.byteslice import build_byteslice, lookup_byteslice_rows
+    from paper_2209_00220_b200.datagen import gen_zipf_device
+    from paper_2209_00220_b200.device import to_dev_u32
+    from paper_2209_00220_b200.dictionary import freq_table_and_ranks
+    from paper_2209_00220_b200.roofline import hbm_peak, lookup_alg_bytes_rows
+    from paper_2209_00220_b200.vbs import build_vbs, lookup_vbs_rows
+
+    n = 1 << log2n
+    m = 1 << (log2n - 4)
+    rng3 = np.random.default_rng(3)
+    codes = torch.from_numpy(rng3.integers(0, 1 << 24, n, dtype=np.int64)).cuda()
+    col_b = build_byteslice(codes, 24)
+    del codes
+    vals = gen_zipf_device(ZipfSpec(1.0, 20, n, seed=4))
+    u, c, ranks = freq_table_and_ranks(vals)
+    d = Dictionary.build(FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), ColumnKind.NUMERIC),
+                         "prefix_preserving")
+    cv, lv = d.row_codes_device(ranks)
+    col_v = build_vbs(cv, lv)
+    del cv, lv, ranks
+    ids = np.random.default_rng(5).integers(0, n, m)
+    sets = {"ids_unsorted": ids, "ids_sorted": np.sort(ids)}
+    bvs = {}
+    rng6 = np.random.default_rng(6)
+    for p in (0.01, 0.20):
+        flags = rng6.random(n) < p
+        words = np.packbits(flags, bitorder="little").view(np.uint32)
+        bvs[f"bits_{int(p * 100)}pct"] = (words, np.flatnonzero(flags))
+        del flags
+    peak, _ = hbm_peak(ROOT)
+    exist_v = [col_v.mask_words(j) for j in range(2, col_v.max_len + 1)]
+    out = {}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    import ctypes
+
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.device import stream
+    lib = _lib.load()
+    dec_v = d.dev_decoder
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+
+    for name, rows in list(sets.items()) + [(k, v[1]) for k, v in bvs.items()]:
+        is_bits = name.startswith("bits")
+        if is_bits:
+            dbits = DeviceBitVector(n, to_dev_u32(bvs[name][0]))
+            nsel = len(rows)
+            o64 = torch.empty(max(nsel, 1), dtype=torch.int64, device="cuda")
+            o32 = torch.empty(max(nsel, 1), dtype=torch.int32, device="cuda")
+        else:
+            drows = torch.from_numpy(rows).cuda()
+        for layout in ("byteslice", "ppvbs"):
+            if is_bits and layout == "byteslice":
+                # fused bitvector -> codes (identity codes: code = value)
+                fn = lambda: lib.bsb_byteslice_lookup_bits(
+                    col_b.desc_ref, dbits.dwords.data_ptr(), None, o64.data_ptr(), None,
+                    None, cnt.data_ptr(), stream())
+            elif is_bits:
+                # fused bitvector -> PP-VBS codes -> PPE tree decode -> int32 values
+                fn = lambda: lib.bsb_vbs_lookup_bits(
+                    col_v.desc_ref, dbits.dwords.data_ptr(), ctypes.byref(dec_v), None, None,
+                    o32.data_ptr(), cnt.data_ptr(), stream())
+            elif layout == "byteslice":
+                fn = lambda: lookup_byteslice_rows(col_b, drows)
+            else:
+                o32i = torch.empty(drows.numel(), dtype=torch.int32, device="cuda")
+                errw = torch.zeros(1, dtype=torch.int32, device="cuda")
+                fn = lambda: lib.bsb_vbs_lookup_rows_dec(
+                    col_v.desc_ref, drows.data_ptr(), drows.numel(), ctypes.byref(dec_v), None,
+                    None, o32i.data_ptr(), errw.data_ptr(), stream())
+            ms = timed(fn)
+            if is_bits and int(cnt.item()) != nsel:
+                raise RuntimeError(f"{layout}/{name}: fused lookup count mismatch")
+            if not is_bits and layout == "ppvbs" and int(errw.item()) != 0:
+                raise RuntimeError("ppvbs lookup: code not in dictionary")
+            K = col_b.n_slices if layout == "byteslice" else col_v.max_len
+            ob = 8 if layout == "byteslice" else 4
+            ab = lookup_alg_bytes_rows(
+                rows, K, layout, None if layout == "byteslice" else exist_v,
+                out_bytes=ob, id_bytes=0 if is_bits else 8,
+                table_bytes=0 if layout == "byteslice" else d.dev_decoder_bytes)
+            if is_bits:
+                ab += 4 * (-(-n // 32))
+            out[f"{layout}/{name}"] = {
+                "rows": int(len(rows)), "ms": round(ms, 4),
+                "mrows_s": round(len(rows) / (ms * 1e-3) / 1e6, 1),
+                "alg_gbs": round(ab / (ms * 1e-3) / 1e9, 1),
+                "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4)}
     return out
 
 

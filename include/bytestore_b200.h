@@ -206,6 +206,54 @@ int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
                         const int64_t* dict_values, int64_t n_dict, int64_t* out_values,
                         int32_t* out_values32, uint64_t* level_counts, void* stream);
 
+/* Decode of looked-up codes to values (dictionary.py:403-414).
+ *  kind 0: none (raw codes out)
+ *  kind 1: rank table: value = values[code]            (decode_ranks)
+ *  kind 2: sorted padded codes + values in that order   (decode_padded,
+ *          binary search; any dictionary)
+ *  kind 3: PPE tree (ppe_numerical dictionaries, <= 3 dependent lookups):
+ *          t1[256] rank of 1-byte codes; c1[256] child id of first bytes of
+ *          longer codes; t2[c1*256+b2] rank of 2-byte codes; c2[c1*256+b2]
+ *          leaf id of longer codes; leaf (start, size, beta): rank =
+ *          start + suffix - 1.  Entries of -1 mark codes not in the
+ *          dictionary (BSB_ENOTFOUND).  values = rank -> value. */
+typedef struct bsb_decode {
+  int32_t kind;
+  int32_t reserved;
+  const int64_t* values;
+  const uint64_t* sorted_padded;
+  int64_t n_dict;
+  const int32_t* t1;
+  const int32_t* c1;
+  const int32_t* t2;
+  const int32_t* c2;
+  const int64_t* leaf_start;
+  const int32_t* leaf_size;
+  const int32_t* leaf_beta;
+} bsb_decode;
+
+/* Fused bitvector-driven lookups (bitvector.py:71-72 + lookup_* + decode):
+ * the set rows of `words` (n_rows = column rows) in ascending order, written
+ * compactly to out_codes (uint64; ByteSlice right-aligned codes, PP-VBS padded
+ * codes) and/or, with a decoder, out_values (int64) / out_values32 (int32).
+ * No row-id array is materialised.  With n_out_dev given the call does not
+ * synchronise: the number of rows written goes to that device scalar, or
+ * UINT64_MAX when a code is not in the dictionary.  With n_out_dev NULL a
+ * decoding call synchronises and returns BSB_ENOTFOUND for such a code. */
+int bsb_byteslice_lookup_bits(const bsb_byteslice* col, const uint32_t* words,
+                              const bsb_decode* dec, uint64_t* out_codes, int64_t* out_values,
+                              int32_t* out_values32, uint64_t* n_out_dev, void* stream);
+int bsb_vbs_lookup_bits(const bsb_vbs* col, const uint32_t* words, const bsb_decode* dec,
+                        uint64_t* out_padded, int64_t* out_values, int32_t* out_values32,
+                        uint64_t* n_out_dev, void* stream);
+/* Row-id lookup of a PP-VBS column with a general decoder (kinds 0/2/3).
+ * With err_dev (caller-zeroed device word) given the call does not
+ * synchronise and *err_dev becomes nonzero for a code not in the dictionary;
+ * with err_dev NULL a decoding call synchronises and returns BSB_ENOTFOUND. */
+int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
+                            const bsb_decode* dec, uint64_t* out_padded, int64_t* out_values,
+                            int32_t* out_values32, uint32_t* err_dev, void* stream);
+
 /* ------------------------------------------------------------ bitvectors */
 /* ResultBitVector.to_indices (bitvector.py:71-72): ascending int64 row ids of
  * the set bits into rows_out (capacity >= popcount); count written to

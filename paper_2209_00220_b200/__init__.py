@@ -18,9 +18,11 @@ _LAZY = {
     "bitvector_and": "bitvector", "bitvector_or": "bitvector", "popcount_vector": "bitvector",
     "ByteSliceColumn": "byteslice", "build_byteslice": "byteslice",
     "scan_byteslice": "byteslice", "lookup_byteslice": "byteslice",
-    "lookup_byteslice_rows": "byteslice", "byteslice_size_report": "byteslice",
+    "lookup_byteslice_rows": "byteslice", "lookup_byteslice_bits": "byteslice",
+    "byteslice_size_report": "byteslice",
     "VbsColumn": "vbs", "build_vbs": "vbs", "scan_vbs": "vbs", "lookup_vbs": "vbs",
-    "lookup_vbs_rows": "vbs", "vbs_size_report": "vbs",
+    "lookup_vbs_rows": "vbs", "lookup_vbs_rows_dec": "vbs", "lookup_vbs_bits": "vbs",
+    "vbs_size_report": "vbs",
     "ColumnKind": "dictionary", "FrequencyTable": "dictionary", "CodeAssignment": "dictionary",
     "Dictionary": "dictionary", "build_frequency_table": "dictionary",
     "ppe_numerical": "dictionary", "fixed_assignment": "dictionary",

@@ -45,6 +45,13 @@ class BsbVbs(ctypes.Structure):
                 ("deep_len", c_int64 * MAX_LEVELS), ("rexist", c_void_p * MAX_LEVELS)]
 
 
+class BsbDecode(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("reserved", c_int32), ("values", c_void_p),
+                ("sorted_padded", c_void_p), ("n_dict", c_int64), ("t1", c_void_p),
+                ("c1", c_void_p), ("t2", c_void_p), ("c2", c_void_p), ("leaf_start", c_void_p),
+                ("leaf_size", c_void_p), ("leaf_beta", c_void_p)]
+
+
 class BsbColumnRef(ctypes.Structure):
     _fields_ = [("layout", c_int32), ("reserved", c_int32),
                 ("byteslice", POINTER(BsbByteSlice)), ("vbs", POINTER(BsbVbs))]
@@ -69,6 +76,12 @@ _SIGS = {
     "bsb_vbs_scan": (c_int32, [POINTER(BsbVbs), POINTER(BsbPred), _P, _P, _P, _P, _P, _P]),
     "bsb_vbs_lookup_rows": (c_int32, [POINTER(BsbVbs), _P, c_int64, _P, _P, _P, c_int64, _P, _P,
                                       _P, _P]),
+    "bsb_byteslice_lookup_bits": (c_int32, [POINTER(BsbByteSlice), _P, POINTER(BsbDecode), _P,
+                                            _P, _P, _P, _P]),
+    "bsb_vbs_lookup_bits": (c_int32, [POINTER(BsbVbs), _P, POINTER(BsbDecode), _P, _P, _P, _P,
+                                      _P]),
+    "bsb_vbs_lookup_rows_dec": (c_int32, [POINTER(BsbVbs), _P, c_int64, POINTER(BsbDecode), _P,
+                                          _P, _P, _P, _P]),
     "bsb_bits_to_rows": (c_int32, [_P, c_int64, _P, POINTER(c_int64), _P]),
     "bsb_bits_to_rows_async": (c_int32, [_P, c_int64, c_int64, _P, _P, _P]),
     "bsb_bits_combine": (c_int32, [c_int32, _P, _P, _P, c_int64, _P]),
@@ -141,5 +154,5 @@ def stream_ptr(stream=None):
 
 
 __all__ = ["load", "check", "ptr", "stream_ptr", "BsbPred", "BsbByteSlice", "BsbVbs",
-           "BsbColumnRef", "EXPORTED_SYMBOLS", "c_double", "c_int64", "c_int32", "c_uint8",
+           "BsbColumnRef", "BsbDecode", "EXPORTED_SYMBOLS", "c_double", "c_int64", "c_int32", "c_uint8",
            "c_uint64"]

@@ -22,7 +22,7 @@ from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
 __all__ = ["ByteSliceColumn", "build_byteslice", "scan_byteslice", "lookup_byteslice",
-           "lookup_byteslice_rows", "byteslice_size_report"]
+           "lookup_byteslice_rows", "lookup_byteslice_bits", "byteslice_size_report"]
 
 
 @dataclass
@@ -168,6 +168,34 @@ def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=
                                              rank_values.data_ptr(), p64, p32, stream()),
                "lookup_byteslice")
     return out
+
+
+def lookup_byteslice_bits(col: ByteSliceColumn, selection, decoder=None,
+                          out_dtype=torch.int64):
+    """Fused selection -> codes (or decoded values with a rank-table
+    decoder), ascending row order, no row-id array materialised."""
+    sel = as_device_bits(selection)
+    if sel.n_rows != col.n_rows:
+        raise ValueError("selection length mismatch")
+    n = sel.count()
+    dev = col.planes.device
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    out = torch.empty(max(n, 1), dtype=torch.int64 if decoder is None else out_dtype,
+                      device=dev)
+    if decoder is None:
+        _lib.check(lib.bsb_byteslice_lookup_bits(col.desc_ref, sel.dwords.data_ptr(), None,
+                                                 out.data_ptr(), None, None, cnt.data_ptr(),
+                                                 stream()), "lookup_byteslice")
+        return out[:n]
+    p64 = out.data_ptr() if out_dtype == torch.int64 else None
+    p32 = out.data_ptr() if out_dtype == torch.int32 else None
+    _lib.check(lib.bsb_byteslice_lookup_bits(col.desc_ref, sel.dwords.data_ptr(),
+                                             ctypes.byref(decoder), None, p64, p32,
+                                             cnt.data_ptr(), stream()), "lookup_byteslice")
+    if int(cnt.item()) == -1:
+        raise LookupError("lookup_byteslice: code not in dictionary")
+    return out[:n]
 
 
 def lookup_byteslice(col: ByteSliceColumn, selection):

@@ -20,6 +20,19 @@ void set_error(const char* where, cudaError_t err) {
 }
 void set_error_msg(const char* msg) { g_last_error = msg; }
 
+void ensure_init() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 int sm_count() {
   static int cached = -1;
   if (cached < 0) {

@@ -38,7 +38,14 @@ void set_error_msg(const char* msg);
     }                                                    \
   } while (0)
 
-inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// First use per process: keep freed stream-ordered allocations in the
+// device pool (release threshold = max) so per-call temporaries do not go
+// back to the driver at every synchronisation.
+void ensure_init();
+inline cudaStream_t as_stream(void* s) {
+  ensure_init();
+  return reinterpret_cast<cudaStream_t>(s);
+}
 
 // Grid sizing: persistent grid-stride kernels use (SMs x resident CTAs).
 int sm_count();

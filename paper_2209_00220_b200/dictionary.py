@@ -174,6 +174,66 @@ def compare_codes(code1: int, len1: int, code2: int, len2: int):
     return (1 if len1 > len2 else -1), m
 
 
+def ppe_decode_tree(codes, lens):
+    """Tables for decoding ppe_numerical codes in <= 3 dependent lookups.
+
+    ppe_numerical builds a 256-ary tree whose internal nodes sit at depth 0
+    and 1 only and whose depth-2 nodes are leaves enumerating a contiguous
+    rank range (dictionary.py:170-195); so a code of length L decodes as
+    t1[b1] (L = 1), t2[c1[b1], b2] (L = 2) or leaf_start + suffix - 1 of leaf
+    c2[c1[b1], b2] (L >= 3).  Every code is decoded through the tables before
+    they are accepted; returns None when the codes do not have that shape (the
+    caller then decodes by binary search over the sorted padded codes).
+    """
+    cd = np.asarray(codes, dtype=np.uint64)
+    L = np.asarray(lens).astype(np.int64)
+    D = len(cd)
+    if D == 0 or L.max() > 8:
+        return None
+    ranks = np.arange(D, dtype=np.int64)
+    sh1 = (np.uint64(8) * (L - 1).astype(np.uint64))
+    b1 = ((cd >> sh1) & np.uint64(0xFF)).astype(np.int64)
+    sh2 = (np.uint64(8) * np.maximum(L - 2, 0).astype(np.uint64))
+    b2 = ((cd >> sh2) & np.uint64(0xFF)).astype(np.int64)
+    one, two, three = L == 1, L == 2, L >= 3
+    t1 = np.full(256, -1, np.int32)
+    t1[b1[one]] = ranks[one]
+    c1 = np.full(256, -1, np.int32)
+    ub1 = np.unique(b1[~one])
+    c1[ub1] = np.arange(len(ub1), dtype=np.int32)
+    n1 = max(len(ub1), 1)
+    key = c1[b1].astype(np.int64) * 256 + b2
+    t2 = np.full(n1 * 256, -1, np.int32)
+    t2[key[two]] = ranks[two]
+    c2 = np.full(n1 * 256, -1, np.int32)
+    lkeys, inv = np.unique(key[three], return_inverse=True)
+    nl = len(lkeys)
+    c2[lkeys] = np.arange(nl, dtype=np.int32)
+    start = np.zeros(max(nl, 1), np.int64)
+    size = np.zeros(max(nl, 1), np.int32)
+    beta = np.zeros(max(nl, 1), np.int32)
+    if nl:
+        start[:nl] = np.iinfo(np.int64).max
+        np.minimum.at(start, inv, ranks[three])
+        size[:nl] = np.bincount(inv, minlength=nl)
+        beta[inv] = (L[three] - 2)
+    # decode every code through the tables and require the identity
+    got = np.full(D, -1, np.int64)
+    got[one] = t1[b1[one]]
+    got[two] = t2[key[two]]
+    if nl:
+        lf = c2[key[three]]
+        sfx = (cd[three] & ((np.uint64(1) << (np.uint64(8) * (L[three] - 2).astype(np.uint64)))
+                            - np.uint64(1))).astype(np.int64)
+        okb = beta[lf] == L[three] - 2
+        oks = (sfx >= 1) & (sfx <= size[lf])
+        got[three] = np.where(okb & oks, start[lf] + sfx - 1, -1)
+    if not np.array_equal(got, ranks):
+        return None
+    return {"t1": t1, "c1": c1, "t2": t2, "c2": c2, "leaf_start": start, "leaf_size": size,
+            "leaf_beta": beta}
+
+
 class Dictionary:
     """Value table plus one code assignment (dictionary.py:316-485)."""
 
@@ -238,6 +298,45 @@ class Dictionary:
         a = self.assignment
         return (torch.from_numpy(a.codes.view(np.int64)).to(device()),
                 torch.from_numpy(a.lengths).to(device()))
+
+    @cached_property
+    def dev_decoder(self):
+        """C-ABI decoder for the lookup kernels (include/bytestore_b200.h):
+        rank table for fixed codes, the PPE tree for ppe_numerical codes
+        (checked against every code on build), else sorted padded codes."""
+        dec = _lib.BsbDecode()
+        keep = {}
+        if self.assignment.scheme == "fixed":
+            keep["values"] = self.dev_values
+            dec.kind = 1
+            dec.values = keep["values"].data_ptr()
+        else:
+            tree = ppe_decode_tree(self.assignment.codes, self.assignment.lengths)
+            if tree is not None:
+                dev = device()
+                for k, v in tree.items():
+                    keep[k] = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+                keep["values"] = self.dev_values
+                dec.kind = 3
+                dec.values = keep["values"].data_ptr()
+                for k in tree:
+                    setattr(dec, k, keep[k].data_ptr())
+            else:
+                sp, vals = self.dev_decode
+                keep["sp"], keep["vals"] = sp, vals
+                dec.kind = 2
+                dec.values = vals.data_ptr()
+                dec.sorted_padded = sp.data_ptr()
+                dec.n_dict = sp.numel()
+        dec.n_dict = dec.n_dict or self.n
+        self._decoder_keep = keep
+        return dec
+
+    @property
+    def dev_decoder_bytes(self) -> int:
+        """Device bytes of the decoder tables (roofline: read once per launch)."""
+        self.dev_decoder
+        return sum(t.numel() * t.element_size() for t in self._decoder_keep.values())
 
     # row encoding / decoding -------------------------------------------
     def encode_rows_device(self, values) -> torch.Tensor:

@@ -25,16 +25,17 @@ from . import _lib
 from .advisor import ColumnAdvice, advise_column
 from .bitvector import DeviceBitVector, ResultBitVector, as_device_bits
 from .byteslice import (ByteSliceColumn, build_byteslice, byteslice_size_report,
-                        lookup_byteslice_rows, scan_byteslice)
+                        lookup_byteslice_bits, lookup_byteslice_rows, scan_byteslice)
 from .datagen import PRNG_NAME
 from .device import device, stream
 from .dictionary import ColumnKind, Dictionary, FrequencyTable, freq_table_and_ranks
 from .predicate import DEFAULT_LANES, LaneConfig, Op, Predicate, ResolvedPredicate
-from .vbs import VbsColumn, build_vbs, lookup_vbs_rows, scan_vbs, vbs_size_report
+from .vbs import (VbsColumn, build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs,
+                  vbs_size_report)
 
 __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
            "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",
-           "lookup_decode", "lookup_decode_rows", "execute", "ingest_arrays", "size_report",
+           "lookup_decode", "lookup_decode_rows", "lookup_decode_bits", "execute", "ingest_arrays", "size_report",
            "conj_scan"]
 
 LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
@@ -136,18 +137,28 @@ def scan_layout(layout: str, column, pred, mask=None, threads: int = 1):
 def lookup_decode_rows(stored: StoredColumn, rows: torch.Tensor, out_dtype=torch.int64):
     """Device gather + decode of a row-id tensor (any order)."""
     if stored.layout == "ppvbs":
-        sp, vals = stored.dictionary.dev_decode
-        return lookup_vbs_rows(stored.column, rows, sp, vals, out_dtype)
+        return lookup_vbs_rows_dec(stored.column, rows, stored.dictionary.dev_decoder,
+                                   out_dtype)
     _require_device_layout(stored.layout)
     return lookup_byteslice_rows(stored.column, rows, stored.dictionary.dev_values, out_dtype)
 
 
+def lookup_decode_bits(stored: StoredColumn, selection, out_dtype=torch.int64):
+    """Fused selection -> decoded values on the device (ascending rows)."""
+    if stored.layout == "ppvbs":
+        return lookup_vbs_bits(stored.column, selection, stored.dictionary.dev_decoder,
+                               out_dtype)
+    _require_device_layout(stored.layout)
+    return lookup_byteslice_bits(stored.column, selection, stored.dictionary.dev_decoder,
+                                 out_dtype)
+
+
 def lookup_decode(stored: StoredColumn, selection) -> np.ndarray:
     """engine.py:204-221: selected rows of one column, decoded to values."""
-    rows = as_device_bits(selection).row_ids()
-    if rows.numel() == 0:
+    sel = as_device_bits(selection)
+    if sel.count() == 0:
         return stored.dictionary.table.values[:0]
-    return lookup_decode_rows(stored, rows).cpu().numpy()
+    return lookup_decode_bits(stored, sel).cpu().numpy()
 
 
 def size_report(stored: StoredColumn) -> dict:
@@ -235,7 +246,6 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
         selection = selection | extra
     n_sel = selection.count()
     out = {}
-    rows = selection.row_ids() if n_sel else None
     for name in query.projection:
         st = store.columns[name]
         if n_sel == 0:
@@ -243,7 +253,7 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
             timings.append({"column": name, "phase": "lookup", "op": "", "seconds": 0.0})
             continue
         t0 = time.perf_counter()
-        out[name] = lookup_decode_rows(st, rows, out_dtype).cpu().numpy()
+        out[name] = lookup_decode_bits(st, selection, out_dtype).cpu().numpy()
         timings.append({"column": name, "phase": "lookup", "op": "",
                         "seconds": time.perf_counter() - t0})
     return QueryResult(n_sel, out, timings, selection)

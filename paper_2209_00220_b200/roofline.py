@@ -78,6 +78,6 @@ def lookup_alg_bytes_rows(rows: np.ndarray, K: int, layout: str, exist_words=Non
         alive = alive[has]
         if alive.size == 0:
             break
-        total += 32 * np.unique((alive >> 5) >> 2).size   # int64 dir: 4 per sector
+        total += 32 * np.unique((alive >> 5) >> 3).size   # u32 dir: 8 per sector
         total += 32 * np.unique(alive >> 5).size          # deep bytes of a block ~ 1 sector
     return int(total)

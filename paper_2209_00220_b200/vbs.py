@@ -22,7 +22,7 @@ from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
 __all__ = ["VbsColumn", "build_vbs", "scan_vbs", "lookup_vbs", "lookup_vbs_rows",
-           "vbs_size_report"]
+           "lookup_vbs_rows_dec", "lookup_vbs_bits", "vbs_size_report"]
 
 DEEP_PAD = 64
 
@@ -276,6 +276,53 @@ def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
                                        sorted_padded.numel(), p64, p32, lc, stream()),
                "lookup_vbs")
     return out
+
+
+def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64):
+    """Row-id lookup decoded through a C-ABI decoder (Dictionary.dev_decoder)."""
+    lib = _lib.load()
+    rows = to_dev_i64(rows)
+    n = rows.numel()
+    out = torch.empty(n, dtype=out_dtype, device=rows.device)
+    p64 = out.data_ptr() if out_dtype == torch.int64 else None
+    p32 = out.data_ptr() if out_dtype == torch.int32 else None
+    _lib.check(lib.bsb_vbs_lookup_rows_dec(col.desc_ref, rows.data_ptr(), n,
+                                           ctypes.byref(decoder), None, p64, p32, None,
+                                           stream()),
+               "lookup_vbs")
+    return out
+
+
+def lookup_vbs_bits(col: VbsColumn, selection, decoder=None, out_dtype=torch.int64):
+    """Fused selection -> values (or padded codes without a decoder), in
+    ascending row order; no row-id array is materialised."""
+    sel = as_device_bits(selection)
+    if sel.n_rows != col.n_rows:
+        raise ValueError("selection length mismatch")
+    n = sel.count()
+    dev = col.bs1.device
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    if decoder is None:
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        _lib.check(lib.bsb_vbs_lookup_bits(col.desc_ref, sel.dwords.data_ptr(), None,
+                                           out.data_ptr(), None, None, cnt.data_ptr(),
+                                           stream()), "lookup_vbs")
+        return out[:n]
+    out = torch.empty(max(n, 1), dtype=out_dtype, device=dev)
+    p64 = out.data_ptr() if out_dtype == torch.int64 else None
+    p32 = out.data_ptr() if out_dtype == torch.int32 else None
+    _lib.check(lib.bsb_vbs_lookup_bits(col.desc_ref, sel.dwords.data_ptr(),
+                                       ctypes.byref(decoder), None, p64, p32, cnt.data_ptr(),
+                                       stream()), "lookup_vbs")
+    _check_count(cnt, "lookup_vbs")
+    return out[:n]
+
+
+def _check_count(cnt: torch.Tensor, where: str):
+    """UINT64_MAX in the async count = a code not in the dictionary."""
+    if int(cnt.item()) == -1:
+        raise LookupError(f"{where}: padded code not in dictionary")
 
 
 def lookup_vbs(col: VbsColumn, selection):

@@ -255,6 +255,85 @@ def test_vbs_row_lookup_decode_vs_oracle(mode):
     assert np.array_equal(v32, vals[np.sort(rows)].astype(np.int32))
 
 
+def _sel_cases(n, rng):
+    yield np.zeros(n, bool)
+    yield np.ones(n, bool)
+    for p in (0.001, 0.05, 0.5):
+        yield rng.random(n) < p
+    f = np.zeros(n, bool)
+    f[-1] = True  # last (ragged) row only
+    yield f
+
+
+@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+def test_vbs_fused_bits_lookup_and_tree_decode(mode):
+    """bsb_vbs_lookup_bits (bitvector -> codes / values in one kernel) and
+    the PPE tree decoder equal the oracle's lookup + the row values."""
+    n = 150_001
+    vals, od, codes, lens = _ppe_column(1.0, 20, n, 9)
+    col = B.build_vbs(codes, lens, deep_mode=mode)
+    ocol = O.vbs_build(codes, lens)
+    d = B.Dictionary.build(B.FrequencyTable(od.values, od.weights, B.ColumnKind.NUMERIC),
+                           "prefix_preserving")
+    dec = d.dev_decoder
+    assert dec.kind == 3  # ppe_numerical dictionaries decode through the tree
+    rng = np.random.default_rng(10)
+    for flags in _sel_cases(n, rng):
+        rows = np.flatnonzero(flags)
+        bv = B.ResultBitVector(n, O.bools_to_words(flags))
+        got = B.lookup_vbs_bits(col, bv).cpu().numpy().view(np.uint64)
+        want, _ = O.vbs_lookup(ocol, rows)
+        assert np.array_equal(got, want)
+        v = B.lookup_vbs_bits(col, bv, dec).cpu().numpy()
+        assert np.array_equal(v, vals[rows])
+        v32 = B.lookup_vbs_bits(col, bv, dec, out_dtype=torch.int32).cpu().numpy()
+        assert np.array_equal(v32, vals[rows].astype(np.int32))
+    rows = rng.integers(0, n, size=77_777)
+    v = B.lookup_vbs_rows_dec(col, torch.from_numpy(rows), dec).cpu().numpy()
+    assert np.array_equal(v, vals[rows])
+
+
+def test_tree_decoder_equals_binary_search_decoder():
+    """Decoder kinds 2 (sorted padded codes) and 3 (PPE tree) agree on every
+    code of several dictionaries, incl. single-byte-only and deep ones."""
+    from paper_2209_00220_b200 import _lib
+    for s, dd, n, seed in ((1.0, 8, 5000, 1), (1.2, 20, 300_000, 2), (0.5, 22, 400_000, 3)):
+        vals, od, codes, lens = _ppe_column(s, dd, n, seed)
+        col = B.build_vbs(codes, lens)
+        d = B.Dictionary.build(B.FrequencyTable(od.values, od.weights, B.ColumnKind.NUMERIC),
+                               "prefix_preserving")
+        rows = torch.arange(n, dtype=torch.int64)
+        v3 = B.lookup_vbs_rows_dec(col, rows, d.dev_decoder).cpu().numpy()
+        sp, dv = d.dev_decode
+        dec2 = _lib.BsbDecode()
+        dec2.kind, dec2.values, dec2.sorted_padded, dec2.n_dict = 2, dv.data_ptr(), \
+            sp.data_ptr(), sp.numel()
+        v2 = B.lookup_vbs_rows_dec(col, rows, dec2).cpu().numpy()
+        assert np.array_equal(v3, vals) and np.array_equal(v2, vals)
+
+
+def test_byteslice_fused_bits_lookup():
+    rng = np.random.default_rng(12)
+    for n, w in ((70_001, 13), (4096, 24), (33, 40)):
+        codes = rng.integers(0, 1 << min(w, 62), n, dtype=np.int64).astype(np.uint64)
+        col = B.build_byteslice(codes, w)
+        for flags in _sel_cases(n, rng):
+            rows = np.flatnonzero(flags)
+            bv = B.ResultBitVector(n, O.bools_to_words(flags))
+            got = B.lookup_byteslice_bits(col, bv).cpu().numpy().view(np.uint64)
+            assert np.array_equal(got, codes[rows]), (n, w)
+    # rank-table decode of a fixed dictionary
+    vals = rng.integers(-10**9, 10**9, 100_000)
+    d = B.Dictionary.build(B.FrequencyTable(*np.unique(vals, return_counts=True),
+                                            B.ColumnKind.NUMERIC), "fixed")
+    ranks = d.encode_rows(vals)
+    col = B.build_byteslice(ranks, d.assignment.width_bits)
+    flags = rng.random(len(vals)) < 0.3
+    v = B.lookup_byteslice_bits(col, B.ResultBitVector(len(vals), O.bools_to_words(flags)),
+                                d.dev_decoder).cpu().numpy()
+    assert np.array_equal(v, vals[flags])
+
+
 def test_vbs_errors():
     col = B.build_vbs([1, 2], [1, 1])
     with pytest.raises(ValueError):
@@ -272,6 +351,16 @@ def test_vbs_errors():
     sp, dv = d.dev_decode
     with pytest.raises(LookupError):
         B.lookup_vbs_rows(bad, torch.zeros(1, dtype=torch.int64), sp, dv)
+    with pytest.raises(LookupError):
+        B.lookup_vbs_rows_dec(bad, torch.zeros(1, dtype=torch.int64), d.dev_decoder)
+    with pytest.raises(LookupError):
+        B.lookup_vbs_bits(bad, B.ResultBitVector(1, np.ones(1, np.uint32)), d.dev_decoder)
+    fx = B.Dictionary.build(B.FrequencyTable(np.arange(3), np.array([3, 2, 1]),
+                                             B.ColumnKind.NUMERIC), "fixed")
+    bcol = B.build_byteslice(np.array([1, 5], np.int64), 8)
+    with pytest.raises(LookupError):
+        B.lookup_byteslice_bits(bcol, B.ResultBitVector(2, np.array([3], np.uint32)),
+                                fx.dev_decoder)
 
 
 # --------------------------------------------- encoders, advisor, engine

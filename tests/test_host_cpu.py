@@ -63,6 +63,20 @@ def test_ppe_numerical_native_matches_golden(lib):
         assert np.array_equal(a.lengths, data[f"ppe{i}/lengths"]), i
 
 
+def test_ppe_decode_tree_on_golden_codes():
+    """The lookup kernels' PPE tree decoder (host-built tables) maps every
+    reference-generated ppe_numerical code back to its rank, and refuses
+    code sets that are not ppe-shaped."""
+    from paper_2209_00220_b200.dictionary import ppe_decode_tree
+    data, _ = load("dict")
+    for i in range(int(data["n_ppe"])):
+        t = ppe_decode_tree(data[f"ppe{i}/codes"], data[f"ppe{i}/lengths"])
+        assert t is not None, i
+    # a deep leaf whose suffixes do not enumerate 1..size is not ppe-shaped
+    assert ppe_decode_tree(np.array([0x01, 0x020105], np.uint64),
+                           np.array([1, 3], np.uint8)) is None
+
+
 def test_ppe_errors(lib):
     from paper_2209_00220_b200.dictionary import ppe_numerical
     with pytest.raises(ValueError):

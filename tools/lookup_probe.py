@@ -1,0 +1,18 @@
+"""Run the cfg3 lookup measurements alone (diagnostic; for ncu launch lists).
+
+    python tools/lookup_probe.py [steps] [log2n]
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+if __name__ == "__main__":
+    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+    log2n = int(sys.argv[2]) if len(sys.argv) > 2 else 28
+    for k, v in bench.measure_lookups(steps, log2n).items():
+        print(k, json.dumps(v))
