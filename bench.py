@@ -433,7 +433,7 @@ def run_b200(args):
     return out
 
 
-def measure_lookups(steps: int, log2n: int = 28):
+def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
     """cfg3 (BASELINE.json configs[2]): 2^28-row ByteSlice column of 24-bit
     uniform codes (identity codes = values) and a 2^28-row Zipf(1.0)/2^20
     PP-VBS column; lookups of 2^24 random row ids (unsorted and sorted) and of
@@ -506,6 +506,8 @@ def measure_lookups(steps: int, log2n: int = 28):
         else:
             drows = torch.from_numpy(rows).cuda()
         for layout in ("byteslice", "ppvbs"):
+            if only and only not in f"{layout}/{name}":
+                continue
             if is_bits and layout == "byteslice":
                 # fused bitvector -> codes (identity codes: code = value)
                 fn = lambda: lib.bsb_byteslice_lookup_bits(

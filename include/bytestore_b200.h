@@ -211,25 +211,24 @@ int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
  *  kind 1: rank table: value = values[code]            (decode_ranks)
  *  kind 2: sorted padded codes + values in that order   (decode_padded,
  *          binary search; any dictionary)
- *  kind 3: PPE tree (ppe_numerical dictionaries, <= 3 dependent lookups):
- *          t1[256] rank of 1-byte codes; c1[256] child id of first bytes of
- *          longer codes; t2[c1*256+b2] rank of 2-byte codes; c2[c1*256+b2]
- *          leaf id of longer codes; leaf (start, size, beta): rank =
- *          start + suffix - 1.  Entries of -1 mark codes not in the
- *          dictionary (BSB_ENOTFOUND).  values = rank -> value. */
+ *  kind 3: PPE tree (ppe_numerical dictionaries, dictionary.py:170-195):
+ *          two dependent table reads + the value.  -1 = absent in every
+ *          field; a node may be a code and a parent at once.
+ *            e1[b1] (int64[256]) = child c (bits 0-31) | rank of the 1-byte
+ *              code b1 (bits 32-63)
+ *            e2[2*(c*256+b2)]   = rank of the 2-byte code (b1, b2)
+ *            e2[2*(c*256+b2)+1] = leaf start | size << 32 | beta << 56: codes
+ *              of length beta + 2 below (b1, b2), rank = start + suffix - 1,
+ *              1 <= suffix <= size
+ *          An absent code gives BSB_ENOTFOUND.  values = rank -> value. */
 typedef struct bsb_decode {
   int32_t kind;
   int32_t reserved;
   const int64_t* values;
   const uint64_t* sorted_padded;
   int64_t n_dict;
-  const int32_t* t1;
-  const int32_t* c1;
-  const int32_t* t2;
-  const int32_t* c2;
-  const int64_t* leaf_start;
-  const int32_t* leaf_size;
-  const int32_t* leaf_beta;
+  const int64_t* e1;
+  const int64_t* e2;
 } bsb_decode;
 
 /* Fused bitvector-driven lookups (bitvector.py:71-72 + lookup_* + decode):

@@ -47,9 +47,8 @@ class BsbVbs(ctypes.Structure):
 
 class BsbDecode(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("reserved", c_int32), ("values", c_void_p),
-                ("sorted_padded", c_void_p), ("n_dict", c_int64), ("t1", c_void_p),
-                ("c1", c_void_p), ("t2", c_void_p), ("c2", c_void_p), ("leaf_start", c_void_p),
-                ("leaf_size", c_void_p), ("leaf_beta", c_void_p)]
+                ("sorted_padded", c_void_p), ("n_dict", c_int64), ("e1", c_void_p),
+                ("e2", c_void_p)]
 
 
 class BsbColumnRef(ctypes.Structure):

@@ -2,7 +2,9 @@
 // compaction and word-level bitvector algebra.
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "bsb_common.cuh"
 
@@ -349,13 +351,8 @@ struct Decoder {
   const int64_t* values;
   const uint64_t* sorted;
   int64_t n;
-  const int32_t* t1;
-  const int32_t* c1;
-  const int32_t* t2;
-  const int32_t* c2;
-  const int64_t* leaf_start;
-  const int32_t* leaf_size;
-  const int32_t* leaf_beta;
+  const int64_t* e1;
+  const int64_t* e2;
 };
 
 static void fill_decoder(Decoder& D, const bsb_decode* d) {
@@ -365,13 +362,8 @@ static void fill_decoder(Decoder& D, const bsb_decode* d) {
   D.values = d->values;
   D.sorted = d->sorted_padded;
   D.n = d->n_dict;
-  D.t1 = d->t1;
-  D.c1 = d->c1;
-  D.t2 = d->t2;
-  D.c2 = d->c2;
-  D.leaf_start = d->leaf_start;
-  D.leaf_size = d->leaf_size;
-  D.leaf_beta = d->leaf_beta;
+  D.e1 = d->e1;
+  D.e2 = d->e2;
 }
 
 // value of a looked-up code; `code` = right-aligned code (ByteSlice rank or
@@ -379,7 +371,7 @@ static void fill_decoder(Decoder& D, const bsb_decode* d) {
 // the code is not in the dictionary.
 template <int DK = -1>  // DK >= 0: decoder kind fixed at compile time
 __device__ __forceinline__ int64_t decode_value(const Decoder& D, uint64_t code, uint64_t padded,
-                                                int len, bool& bad) {
+                                                int len, bool& bad, const int64_t* e1s) {
   switch (DK >= 0 ? DK : D.kind) {
     case 1:
       if (code >= (uint64_t)D.n) {
@@ -403,23 +395,24 @@ __device__ __forceinline__ int64_t decode_value(const Decoder& D, uint64_t code,
       return __ldg(D.values + lo);
     }
     case 3: {
-      int32_t r = -1;
+      // e1 may be a shared-memory copy (e1s); see bsb_decode in the header
+      int64_t r = -1;
       const uint32_t b1 = (uint32_t)(code >> (8 * (len - 1))) & 0xFFu;
+      const uint64_t n1 = (uint64_t)e1s[b1];
       if (len == 1) {
-        r = __ldg(D.t1 + b1);
+        const uint32_t r1 = (uint32_t)(n1 >> 32);
+        if (r1 != 0xFFFFFFFFu) r = r1;
       } else {
-        const int32_t c = __ldg(D.c1 + b1);
+        const uint32_t c = (uint32_t)n1;
         const uint32_t b2 = (uint32_t)(code >> (8 * (len - 2))) & 0xFFu;
-        if (c >= 0) {
+        if (c != 0xFFFFFFFFu) {
+          const int64_t e = __ldg(D.e2 + 2 * ((int64_t)c * 256 + b2) + (len > 2));
           if (len == 2) {
-            r = __ldg(D.t2 + (int64_t)c * 256 + b2);
-          } else {
-            const int32_t lf = __ldg(D.c2 + (int64_t)c * 256 + b2);
-            if (lf >= 0 && __ldg(D.leaf_beta + lf) == len - 2) {
-              const uint64_t sfx = code & ((1ull << (8 * (len - 2))) - 1ull);
-              if (sfx >= 1 && sfx <= (uint64_t)__ldg(D.leaf_size + lf))
-                r = (int32_t)(__ldg(D.leaf_start + lf) + (int64_t)sfx - 1);
-            }
+            r = e;
+          } else if (e >= 0 && (int)(e >> 56) == len - 2) {
+            const uint64_t sfx = code & ((1ull << (8 * (len - 2))) - 1ull);
+            if (sfx >= 1 && sfx <= (uint64_t)((e >> 32) & 0xFFFFFF))
+              r = (e & 0xFFFFFFFFll) + (int64_t)sfx - 1;
           }
         }
       }
@@ -447,29 +440,42 @@ __device__ __forceinline__ void vbs_block_meta(const VbsLookupDesc& d, int64_t b
 }
 
 // right-aligned code and length of row lr of block blk, given its BS_1 byte
+// Code length of row lr from the block's existence words (lengths nest, so
+// it is one plus the number of levels >= 2 whose word has the row's bit).
+__device__ __forceinline__ int vbs_row_len(const VbsLookupDesc& d, const VbsBlockMeta& mt,
+                                           int lr) {
+  int L = 1;
+#pragma unroll
+  for (int j = 2; j <= kMaxLevels; ++j) L += (j <= d.K) ? (int)((mt.m[j - 1] >> lr) & 1u) : 0;
+  return L;
+}
+
+// Right-aligned code of row lr of block blk, given its BS_1 byte.  All deep
+// byte loads are independent (issued together).
+template <int MODE = -1>  // MODE >= 0: deep layout fixed at compile time
 __device__ __forceinline__ uint64_t vbs_row_code_f(const VbsLookupDesc& d, int64_t blk, int lr,
                                                    const VbsBlockMeta& mt, uint32_t first,
                                                    int& len) {
+  const int mode = MODE >= 0 ? MODE : d.mode;
   const uint32_t below = (1u << lr) - 1u;
-  uint64_t code = first;
-  len = 1;
+  len = vbs_row_len(d, mt, lr);
   const int64_t q = mt.dir2 + __popc(mt.m[1] & below);
-  for (int j = 2; j <= d.K; ++j) {
-    const uint32_t w = mt.m[j - 1];
-    if (!((w >> lr) & 1u)) break;
+  uint64_t code = first;
+#pragma unroll
+  for (int j = 2; j <= kMaxLevels; ++j) {
+    if (j > len) continue;  // predicated, not a break: the loads issue together
     uint32_t byte;
-    if (d.mode == BSB_DEEP_SLICED) {
+    if (mode == BSB_DEEP_SLICED) {
       byte = __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
-    } else if (d.mode == BSB_DEEP_PLANES) {
+    } else if (mode == BSB_DEEP_PLANES) {
       const uint16_t v = __ldg(reinterpret_cast<const uint16_t*>(d.deep[((j - 2) >> 1) + 1]) + q);
       byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
-    } else if (d.mode == BSB_DEEP_RANK2) {
+    } else if (mode == BSB_DEEP_RANK2) {
       byte = __ldg(d.deep[j - 1] + q);
     } else {
-      byte = __ldg(d.deep[j - 1] + (__ldg(d.dir[j - 1] + blk) + __popc(w & below)));
+      byte = __ldg(d.deep[j - 1] + (__ldg(d.dir[j - 1] + blk) + __popc(mt.m[j - 1] & below)));
     }
     code = (code << 8) | byte;
-    len = j;
   }
   return code;
 }
@@ -488,19 +494,29 @@ __device__ __forceinline__ void emit(uint64_t* oc, int64_t* ov, int32_t* ov32, i
 
 // Fused bitvector -> values.  Warp per tile of 1024 rows.  Lane = block:
 // every block with a selected row has its sectors fetched with 256-bit loads
-// (ByteSlice: the K plane sectors; PP-VBS: the BS_1 sector, the existence
-// words and the level-2 directory entry) into the warp's shared-memory
-// stage, all in flight together; the tile's set rows are compacted into a
-// row list; then lane k assembles listed rows k, k+32, ... from the stage
-// (PP-VBS deep bytes from HBM), decodes and writes them contiguously.  A bad
-// code sets *err (UINT64_MAX when err is the output count).
+// (ByteSlice: the K plane sectors; PP-VBS: the BS_1 sector) into the warp's
+// shared-memory stage, all in flight together, plus (PP-VBS) its existence
+// words and level-2 directory entry.  The lane then lists its block's set
+// rows as records (row in tile | code length - 1 | deep-row offset), the
+// length coming from bit-sliced counts of the nested existence words.  Lane
+// k then assembles listed rows k, k+32, ... (kRowsPerLane at a time, their
+// deep-byte loads in flight together), decodes them (PPE first-level table
+// in shared memory) and writes them contiguously.  A bad code sets *err
+// (UINT64_MAX when err is the output count).
 constexpr int kBitsThreads = 128;
 
+// per-warp shared memory: row records (u32 PP-VBS, u16 ByteSlice) + stage
 __host__ __device__ constexpr int bits_stage_bytes(bool vbs, int K) {
-  return 2048 + (vbs ? 1024 + 128 * (K > 1 ? K - 1 : 0) + 256 : 1024 * K);
+  return vbs ? 4096 + 1024 + 128 * (K > 1 ? K - 1 : 0) + 256 : 2048 + 1024 * K;
 }
 
-template <bool VBS, int DK>
+__device__ __forceinline__ void sts256(uint8_t* dst, const uint32_t (&v)[8]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  d[0] = make_uint4(v[0], v[1], v[2], v[3]);
+  d[1] = make_uint4(v[4], v[5], v[6], v[7]);
+}
+
+template <bool VBS, int DK, int MODE, int KT>
 __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     const uint8_t* __restrict__ slices, int64_t stride, int K, int width,  // ByteSlice
     const __grid_constant__ VbsLookupDesc vd,                              // PP-VBS
@@ -509,14 +525,21 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     uint64_t* __restrict__ oc, int64_t* __restrict__ ov, int32_t* __restrict__ ov32,
     unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  const int KL = VBS ? vd.K : K;
-  uint8_t* wbase = dsm + (threadIdx.x >> 5) * bits_stage_bytes(VBS, KL);
-  uint16_t* idx = reinterpret_cast<uint16_t*>(wbase);
-  uint8_t* stage = wbase + 2048;
-  uint32_t* smeta = reinterpret_cast<uint32_t*>(stage + 1024);          // VBS only
-  int64_t* sdir = reinterpret_cast<int64_t*>(smeta + 32 * (KL > 1 ? KL - 1 : 0));
+  int64_t* e1s = reinterpret_cast<int64_t*>(dsm);  // DK == 3: first-level PPE table
+  if (DK == 3) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) e1s[i] = __ldg(D.e1 + i);
+    __syncthreads();
+  }
+  const int KL = KT > 0 ? KT : (VBS ? vd.K : K);
+  const int KD = KL > 1 ? KL - 1 : 0;
+  uint8_t* wbase = dsm + (DK == 3 ? 2048 : 0) + (threadIdx.x >> 5) * bits_stage_bytes(VBS, KL);
+  using Rec = typename std::conditional<VBS, uint32_t, uint16_t>::type;
+  constexpr int kRowsPerLane = VBS ? 4 : 2;  // rows assembled per lane at a time
+  Rec* idx = reinterpret_cast<Rec*>(wbase);
+  uint8_t* stage = wbase + 1024 * sizeof(Rec);
+  uint32_t* smeta = reinterpret_cast<uint32_t*>(stage + 1024);  // PACKED: m[(j-2)*32 + b]
+  int64_t* sdir = reinterpret_cast<int64_t*>(smeta + 32 * KD);   // level-2 directory
   const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int shift = VBS ? 0 : 8 * K - width;
@@ -532,56 +555,96 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     if (total) {
       const int64_t blk = t * 32 + lane;
-      if (w) {
-        if (VBS) {
+      uint32_t m[kMaxLevels + 1];
+#pragma unroll
+      for (int j = 0; j <= kMaxLevels; ++j) m[j] = 0u;
+      if (VBS) {
+        const bool in = blk < nb;
+        if (w) {
+#pragma unroll
+          for (int j = 2; j <= kMaxLevels; ++j)
+            if (j <= KL) m[j] = in ? __ldg(vd.exist[j - 1] + blk) : 0u;
+          sdir[lane] = (in && MODE != BSB_DEEP_PACKED && KL >= 2) ? __ldg(vd.dir[1] + blk) : 0;
           uint32_t v[8];
           ldg256(vd.bs1 + blk * 32, v);
-          uint4* dst = reinterpret_cast<uint4*>(stage + lane * 32);
-          dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
-          dst[1] = make_uint4(v[4], v[5], v[6], v[7]);
-          for (int j = 2; j <= KL; ++j) smeta[(j - 2) * 32 + lane] = __ldg(vd.exist[j - 1] + blk);
-          sdir[lane] = (vd.mode != BSB_DEEP_PACKED && KL >= 2) ? __ldg(vd.dir[1] + blk) : 0;
-        } else {
-          for (int j = 0; j < K; ++j) {
-            uint32_t v[8];
-            ldg256(slices + j * stride + blk * 32, v);
-            uint4* dst = reinterpret_cast<uint4*>(stage + j * 1024 + lane * 32);
-            dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
-            dst[1] = make_uint4(v[4], v[5], v[6], v[7]);
+          sts256(stage + lane * 32, v);
+          if (MODE == BSB_DEEP_PACKED) {
+#pragma unroll
+            for (int j = 2; j <= kMaxLevels; ++j)
+              if (j <= KL) smeta[(j - 2) * 32 + lane] = m[j];
           }
+        }
+      } else if (w) {
+        for (int j = 0; j < K; ++j) {
+          uint32_t v[8];
+          ldg256(slices + j * stride + blk * 32, v);
+          sts256(stage + j * 1024 + lane * 32, v);
         }
       }
       const uint32_t excl = incl - c;
       const int64_t tbase = t ? __ldg(tile_incl + t - 1) : 0;
-      // each lane lists its own block's set rows (ascending)
-      uint32_t rest = w;
-      uint32_t o = excl;
-      while (rest) {
-        const int bit = __ffs(rest) - 1;
-        rest &= rest - 1;
-        idx[o++] = (uint16_t)((lane << 5) | bit);
+      // each lane lists its block's set rows (ascending) as records
+      {
+        // bit-sliced (code length - 1) of the block's rows; lengths nest, so
+        // length - 1 >= k iff the row is in M_{k+1}
+        const uint32_t c0 = (m[2] & ~m[3]) | (m[4] & ~m[5]) | (m[6] & ~m[7]) | m[8];
+        const uint32_t c1 = (m[3] & ~m[5]) | m[7];
+        const uint32_t c2 = m[5];
+        uint32_t rest = w;
+        uint32_t o = excl;
+        while (rest) {
+          const int bit = __ffs(rest) - 1;
+          rest &= rest - 1;
+          uint32_t rec = (uint32_t)((lane << 5) | bit);
+          if (VBS) {
+            const uint32_t lm1 = ((c0 >> bit) & 1u) | (((c1 >> bit) & 1u) << 1) |
+                                 (((c2 >> bit) & 1u) << 2);
+            rec |= (lm1 << 10) | ((uint32_t)__popc(m[2] & ((1u << bit) - 1u)) << 13);
+          }
+          idx[o++] = (Rec)rec;
+        }
       }
       __syncwarp();
-      for (uint32_t k0 = lane; k0 < total; k0 += 64) {
-        uint64_t code[2], pad[2];
-        int len[2];
-        bool on[2];
+      for (uint32_t k0 = lane; k0 < total; k0 += 32 * kRowsPerLane) {
+        uint64_t code[kRowsPerLane], pad[kRowsPerLane];
+        int len[kRowsPerLane];
+        bool on[kRowsPerLane];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRowsPerLane; ++u) {
           const uint32_t k = k0 + 32 * u;
           on[u] = k < total;
           const uint32_t r = on[u] ? idx[k] : 0u;
-          const int bl = (int)(r >> 5);
+          const int bl = (int)((r >> 5) & 31);
           const int lr = (int)(r & 31);
           const int off = bl * 32 + swz(lr);
           if (VBS) {
-            VbsBlockMeta mt;
+            len[u] = on[u] ? 1 + (int)((r >> 10) & 7u) : 1;
+            uint64_t cd = stage[off];
+            const int64_t q = MODE == BSB_DEEP_PACKED ? 0 : sdir[bl] + (r >> 13);
+            const int64_t qs = (q & ~int64_t(31)) + swz((int)(q & 31));
+            const int64_t blkr = t * 32 + bl;
+            const uint32_t below = (1u << lr) - 1u;
 #pragma unroll
-            for (int j = 2; j <= kMaxLevels; ++j)
-              mt.m[j - 1] = (j <= KL && on[u]) ? smeta[(j - 2) * 32 + bl] : 0u;
-            mt.dir2 = sdir[bl];
-            code[u] = vbs_row_code_f(vd, t * 32 + bl, lr, mt, stage[off], len[u]);
-            pad[u] = code[u] << (8 * (KL - len[u]));
+            for (int j = 2; j <= kMaxLevels; ++j) {
+              if (j <= KL && j <= len[u]) {
+                uint32_t byte;
+                if (MODE == BSB_DEEP_SLICED) {
+                  byte = __ldg(vd.deep[j - 1] + qs);
+                } else if (MODE == BSB_DEEP_PLANES) {
+                  const uint16_t v =
+                      __ldg(reinterpret_cast<const uint16_t*>(vd.deep[((j - 2) >> 1) + 1]) + q);
+                  byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
+                } else if (MODE == BSB_DEEP_RANK2) {
+                  byte = __ldg(vd.deep[j - 1] + q);
+                } else {
+                  byte = __ldg(vd.deep[j - 1] + (__ldg(vd.dir[j - 1] + blkr) +
+                                                 __popc(smeta[(j - 2) * 32 + bl] & below)));
+                }
+                cd = (cd << 8) | byte;
+              }
+            }
+            code[u] = cd;
+            pad[u] = cd << (8 * (KL - len[u]));
           } else {
             uint64_t cd = 0;
 #pragma unroll
@@ -592,9 +655,10 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRowsPerLane; ++u) {
           if (!on[u]) continue;
-          const int64_t v = decode_value<DK>(D, code[u], pad[u], len[u], bad);
+          const int64_t v = decode_value<DK>(D, code[u], pad[u], len[u], bad,
+                                             DK == 3 ? e1s : D.e1);
           emit(oc, ov, ov32, tbase + k0 + 32 * u, pad[u], v);
         }
       }
@@ -606,12 +670,20 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
 }
 
 // Row-id lookup + general decode; kIdsPerThread ids per thread in flight.
+template <int MODE>
 __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc vd,
                                            const int64_t* __restrict__ rows, int64_t n_ids,
                                            const __grid_constant__ Decoder D,
                                            uint64_t* __restrict__ oc, int64_t* __restrict__ ov,
                                            int32_t* __restrict__ ov32,
                                            unsigned int* __restrict__ err) {
+  __shared__ int64_t e1sm[256];
+  const int64_t* e1s = D.e1;
+  if (D.kind == 3) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) e1sm[i] = __ldg(D.e1 + i);
+    __syncthreads();
+    e1s = e1sm;
+  }
   bool bad = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
@@ -625,14 +697,15 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
       const int64_t blk = r >> 5;
       VbsBlockMeta mt;
       vbs_block_meta(vd, blk, mt);
-      code[u] = vbs_row_code(vd, blk, (int)(r & 31), mt, len[u]);
+      const int lr = (int)(r & 31);
+      code[u] = vbs_row_code_f<MODE>(vd, blk, lr, mt, __ldg(vd.bs1 + (blk * 32 + swz(lr))), len[u]);
     }
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
       const int64_t i = i0 + u * nthr;
       if (i >= n_ids) break;
       const uint64_t padded = code[u] << (8 * (vd.K - len[u]));
-      const int64_t v = decode_value(D, code[u], padded, len[u], bad);
+      const int64_t v = decode_value(D, code[u], padded, len[u], bad, e1s);
       emit(oc, ov, ov32, i, padded, v);
     }
   }
@@ -697,8 +770,11 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
   std::memset(&vd, 0, sizeof(vd));
   if (VBS) fill_lookup_desc(vd, vcol);
   const int wpb = kBitsThreads / 32;
-  const int smem = wpb * bits_stage_bytes(VBS, VBS ? vcol->max_len : bcol->n_slices);
+  const int smem = wpb * bits_stage_bytes(VBS, VBS ? vcol->max_len : bcol->n_slices) +
+                   (D.kind == 3 ? 2048 : 0);
   auto launch = [&](auto kern) -> int {
+    if (smem > 48 * 1024)
+      BSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
     BSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBitsThreads, smem));
     const int bgrid = (int)std::min<int64_t>((ntiles + wpb - 1) / wpb,
@@ -711,11 +787,39 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
     return BSB_OK;
   };
   int rc;
-  switch (D.kind) {
-    case 0: rc = launch(lookup_bits_kernel<VBS, 0>); break;
-    case 1: rc = launch(lookup_bits_kernel<VBS, 1>); break;
-    case 2: rc = launch(lookup_bits_kernel<VBS, 2>); break;
-    default: rc = launch(lookup_bits_kernel<VBS, 3>); break;
+  if (!VBS) {
+    rc = D.kind == 1 ? launch(lookup_bits_kernel<VBS, 1, 0, 0>)
+                     : launch(lookup_bits_kernel<VBS, 0, 0, 0>);
+  } else {
+    // SLICED (the default deep layout) gets the code length as a template
+    // argument; the other layouts take it at run time.
+    auto sliced_k = [&](auto dk) -> int {
+      constexpr int DKC = decltype(dk)::value;
+      switch (vcol->max_len) {
+        case 2: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 2>);
+        case 3: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 3>);
+        case 4: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 4>);
+        case 5: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 5>);
+        case 6: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 6>);
+        case 7: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 7>);
+        case 8: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 8>);
+        default: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 0>);
+      }
+    };
+    auto by_mode = [&](auto dk) -> int {
+      constexpr int DKC = decltype(dk)::value;
+      switch (vcol->deep_mode) {
+        case BSB_DEEP_PACKED: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_PACKED, 0>);
+        case BSB_DEEP_RANK2: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_RANK2, 0>);
+        case BSB_DEEP_PLANES: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_PLANES, 0>);
+        default: return sliced_k(dk);
+      }
+    };
+    switch (D.kind) {
+      case 0: rc = by_mode(std::integral_constant<int, 0>()); break;
+      case 2: rc = by_mode(std::integral_constant<int, 2>()); break;
+      default: rc = by_mode(std::integral_constant<int, 3>()); break;
+    }
   }
   if (rc != BSB_OK) return rc;
   BSB_CUDA(cudaFreeAsync(tmp, s));
@@ -773,9 +877,20 @@ extern "C" int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, 
     BSB_CUDA(cudaMallocAsync(&err, 4, s));
     BSB_CUDA(cudaMemsetAsync(err, 0, 4, s));
   }
-  vbs_lookup_rows_dec_kernel<<<grid_for_l((n_ids + kIdsPerThread - 1) / kIdsPerThread, 256), 256,
-                               0, s>>>(vd, rows, n_ids, D, out_padded, out_values, out_values32,
-                                       err);
+  const int g = grid_for_l((n_ids + kIdsPerThread - 1) / kIdsPerThread, 256);
+  switch (col->deep_mode) {
+#define BSB_ROWS_DEC(M)                                                                   \
+  case M:                                                                                 \
+    vbs_lookup_rows_dec_kernel<M><<<g, 256, 0, s>>>(vd, rows, n_ids, D, out_padded,       \
+                                                    out_values, out_values32, err);       \
+    break;
+    BSB_ROWS_DEC(BSB_DEEP_PACKED)
+    BSB_ROWS_DEC(BSB_DEEP_RANK2)
+    BSB_ROWS_DEC(BSB_DEEP_PLANES)
+    BSB_ROWS_DEC(BSB_DEEP_SLICED)
+#undef BSB_ROWS_DEC
+    default: return BSB_EINVAL;
+  }
   BSB_LAUNCH_CHECK();
   if (err_dev) return BSB_OK;
   return finish_err(err, s, D.kind >= 2);

@@ -175,63 +175,75 @@ def compare_codes(code1: int, len1: int, code2: int, len2: int):
 
 
 def ppe_decode_tree(codes, lens):
-    """Tables for decoding ppe_numerical codes in <= 3 dependent lookups.
+    """Two-level tables decoding ppe_numerical codes (include/bytestore_b200.h
+    bsb_decode kind 3).
 
     ppe_numerical builds a 256-ary tree whose internal nodes sit at depth 0
     and 1 only and whose depth-2 nodes are leaves enumerating a contiguous
-    rank range (dictionary.py:170-195); so a code of length L decodes as
-    t1[b1] (L = 1), t2[c1[b1], b2] (L = 2) or leaf_start + suffix - 1 of leaf
-    c2[c1[b1], b2] (L >= 3).  Every code is decoded through the tables before
-    they are accepted; returns None when the codes do not have that shape (the
-    caller then decodes by binary search over the sorted padded codes).
+    rank range (dictionary.py:170-195); a node can be a code and a parent at
+    once.  So, with -1 for "absent" in every field:
+      e1[b1]            = child c (low 32 bits) | rank of 1-byte code b1 << 32
+      e2[2*(c*256+b2)]  = rank of the 2-byte code (b1, b2)
+      e2[2*(c*256+b2)+1]= leaf start | size << 32 | beta << 56: the codes of
+                          length beta + 2 below (b1, b2), rank = start +
+                          suffix - 1 for 1 <= suffix <= size.
+    Every code is decoded through the tables before they are accepted;
+    returns None when the codes do not have that shape (the caller then
+    decodes by binary search over the sorted padded codes).
     """
     cd = np.asarray(codes, dtype=np.uint64)
     L = np.asarray(lens).astype(np.int64)
     D = len(cd)
-    if D == 0 or L.max() > 8:
+    if D == 0 or L.max() > 8 or D >= (1 << 31) - 1:
         return None
     ranks = np.arange(D, dtype=np.int64)
-    sh1 = (np.uint64(8) * (L - 1).astype(np.uint64))
-    b1 = ((cd >> sh1) & np.uint64(0xFF)).astype(np.int64)
-    sh2 = (np.uint64(8) * np.maximum(L - 2, 0).astype(np.uint64))
-    b2 = ((cd >> sh2) & np.uint64(0xFF)).astype(np.int64)
-    one, two, three = L == 1, L == 2, L >= 3
-    t1 = np.full(256, -1, np.int32)
-    t1[b1[one]] = ranks[one]
-    c1 = np.full(256, -1, np.int32)
+    b1 = ((cd >> (np.uint64(8) * (L - 1).astype(np.uint64))) & np.uint64(0xFF)).astype(np.int64)
+    b2 = ((cd >> (np.uint64(8) * np.maximum(L - 2, 0).astype(np.uint64)))
+          & np.uint64(0xFF)).astype(np.int64)
+    one, two, deep = L == 1, L == 2, L >= 3
+    M32 = 0xFFFFFFFF
+    r1 = np.full(256, M32, np.int64)
+    r1[b1[one]] = ranks[one]
+    ch = np.full(256, M32, np.int64)
     ub1 = np.unique(b1[~one])
-    c1[ub1] = np.arange(len(ub1), dtype=np.int32)
-    n1 = max(len(ub1), 1)
-    key = c1[b1].astype(np.int64) * 256 + b2
-    t2 = np.full(n1 * 256, -1, np.int32)
-    t2[key[two]] = ranks[two]
-    c2 = np.full(n1 * 256, -1, np.int32)
-    lkeys, inv = np.unique(key[three], return_inverse=True)
-    nl = len(lkeys)
-    c2[lkeys] = np.arange(nl, dtype=np.int32)
-    start = np.zeros(max(nl, 1), np.int64)
-    size = np.zeros(max(nl, 1), np.int32)
-    beta = np.zeros(max(nl, 1), np.int32)
-    if nl:
-        start[:nl] = np.iinfo(np.int64).max
-        np.minimum.at(start, inv, ranks[three])
-        size[:nl] = np.bincount(inv, minlength=nl)
-        beta[inv] = (L[three] - 2)
+    ch[ub1] = np.arange(len(ub1))
+    e1 = (ch | (r1 << 32)).astype(np.uint64).view(np.int64)
+    nk = max(len(ub1), 1) * 256
+    e2 = np.full(2 * nk, -1, np.int64)
+    key = ch[b1] * 256 + b2          # valid where L >= 2
+    e2[2 * key[two]] = ranks[two]
+    if deep.any():
+        rk, Ld = ranks[deep], L[deep]
+        ukey, inv = np.unique(key[deep], return_inverse=True)
+        start = np.full(len(ukey), np.iinfo(np.int64).max)
+        np.minimum.at(start, inv, rk)
+        size = np.bincount(inv, minlength=len(ukey)).astype(np.int64)
+        beta = np.zeros(len(ukey), np.int64)
+        beta[inv] = Ld - 2
+        if (beta[inv] != Ld - 2).any() or size.max() >= (1 << 24):
+            return None
+        e2[2 * ukey + 1] = start | (size << 32) | (beta << 56)
     # decode every code through the tables and require the identity
     got = np.full(D, -1, np.int64)
-    got[one] = t1[b1[one]]
-    got[two] = t2[key[two]]
-    if nl:
-        lf = c2[key[three]]
-        sfx = (cd[three] & ((np.uint64(1) << (np.uint64(8) * (L[three] - 2).astype(np.uint64)))
-                            - np.uint64(1))).astype(np.int64)
-        okb = beta[lf] == L[three] - 2
-        oks = (sfx >= 1) & (sfx <= size[lf])
-        got[three] = np.where(okb & oks, start[lf] + sfx - 1, -1)
+    e1u = e1.view(np.uint64)
+    r1g = (e1u[b1[one]] >> np.uint64(32)).astype(np.int64)
+    got[one] = np.where(r1g == M32, -1, r1g)
+    c = (e1u[b1] & np.uint64(M32)).astype(np.int64)
+    kk = c * 256 + b2
+    okc = c != M32
+    if two.any():
+        got[two] = np.where(okc[two], e2[2 * np.where(okc[two], kk[two], 0)], -1)
+    if deep.any():
+        ent = np.where(okc[deep], e2[2 * np.where(okc[deep], kk[deep], 0) + 1], -1)
+        st, sz, bt = ent & M32, (ent >> 32) & 0xFFFFFF, ent >> 56
+        Ld = L[deep]
+        sh = (np.uint64(8) * (Ld - 2).astype(np.uint64))
+        sfx = (cd[deep] & ((np.uint64(1) << sh) - np.uint64(1))).astype(np.int64)
+        ok = (ent >= 0) & (bt == Ld - 2) & (sfx >= 1) & (sfx <= sz)
+        got[deep] = np.where(ok, st + sfx - 1, -1)
     if not np.array_equal(got, ranks):
         return None
-    return {"t1": t1, "c1": c1, "t2": t2, "c2": c2, "leaf_start": start, "leaf_size": size,
-            "leaf_beta": beta}
+    return {"e1": e1, "e2": e2}
 
 
 class Dictionary:
@@ -319,8 +331,8 @@ class Dictionary:
                 keep["values"] = self.dev_values
                 dec.kind = 3
                 dec.values = keep["values"].data_ptr()
-                for k in tree:
-                    setattr(dec, k, keep[k].data_ptr())
+                dec.e1 = keep["e1"].data_ptr()
+                dec.e2 = keep["e2"].data_ptr()
             else:
                 sp, vals = self.dev_decode
                 keep["sp"], keep["vals"] = sp, vals

@@ -291,6 +291,22 @@ def test_vbs_fused_bits_lookup_and_tree_decode(mode):
     rows = rng.integers(0, n, size=77_777)
     v = B.lookup_vbs_rows_dec(col, torch.from_numpy(rows), dec).cpu().numpy()
     assert np.array_equal(v, vals[rows])
+    # random codes up to 8 bytes (deepest stage), ragged row counts
+    for n2, K in ((40_003, 8), (1100, 2), (5, 3)):
+        lens = rng.integers(1, K + 1, size=n2).astype(np.uint8)
+        byts = rng.integers(0, 256, size=(n2, 8), dtype=np.uint64)
+        byts[:, 0] |= np.uint64(1)
+        codes = np.zeros(n2, np.uint64)
+        for k in range(8):
+            use = lens > k
+            codes[use] |= byts[use, k] << np.uint64(8 * k)
+        col = B.build_vbs(codes, lens, deep_mode=mode)
+        ocol = O.vbs_build(codes, lens)
+        for flags in _sel_cases(n2, rng):
+            rows = np.flatnonzero(flags)
+            got = B.lookup_vbs_bits(col, B.ResultBitVector(n2, O.bools_to_words(flags)))
+            want, _ = O.vbs_lookup(ocol, rows)
+            assert np.array_equal(got.cpu().numpy().view(np.uint64), want), (n2, K)
 
 
 def test_tree_decoder_equals_binary_search_decoder():

@@ -14,5 +14,6 @@ import bench  # noqa: E402
 if __name__ == "__main__":
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     log2n = int(sys.argv[2]) if len(sys.argv) > 2 else 28
-    for k, v in bench.measure_lookups(steps, log2n).items():
+    only = sys.argv[3] if len(sys.argv) > 3 else None
+    for k, v in bench.measure_lookups(steps, log2n, only).items():
         print(k, json.dumps(v))
