@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-lookup", action="store_true")
     ap.add_argument("--lookup-steps", type=int, default=10)
+    ap.add_argument("--no-extra", action="store_true", help="skip cfg1/cfg4/cfg5")
     ap.add_argument("--deep-mode", default="auto",
                     help="PP-VBS deep layout: auto|packed|rank2|planes|sliced")
     ap.add_argument("--profile", action="store_true",
@@ -394,10 +395,16 @@ def run_b200(args):
         if not args.profile and not args.no_lookup:
             torch.cuda.empty_cache()
             lookups = measure_lookups(max(3, args.lookup_steps), args.rows_log2)
+        extra = None
+        if not args.profile and not args.no_extra:
+            extra = measure_extra_configs(data)
         cpu = None
         if world == 1 and not args.profile and not args.no_cpu_baseline:
             cpu = cpu_baseline(n, 1 << 22, os.cpu_count() or 1)
         dom_e = by_layout[dom]
+        kname = ("vbs_sliced_kernel<BETWEEN> (PP-VBS, SLICED deep layout)"
+                 if dom == "ppvbs" and col_v.deep_mode == _lib.DEEP_SLICED else
+                 f"scan_kernel<{dom}, BETWEEN>")
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "Gcodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -410,15 +417,19 @@ def run_b200(args):
                        "l2": f"inputs larger than L2 (PP-VBS {col_bytes(col_v) / 1e6:.0f} MB, "
                              f"ByteSlice {col_bytes(col_b) / 1e6:.0f} MB per column)",
                        "parallelism": f"row shards x{world}" if world > 1 else "single GPU"},
-            "roofline": {"bound": "hbm", "kernel": f"scan_kernel<{dom}, BETWEEN>",
+            "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": round(dom_e["gbs"], 1), "peak": peak, "unit": "GB/s",
                          "frac": round(dom_e["frac"], 4), "peak_source": peak_src,
                          "traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic.json (dram read+write per "
+                                           "launch, mean of the 4 windows)",
+                         "alg_bytes_per_launch": int(dom_e["alg_bytes"] / 4),
                          "alg_bytes_per_step": int(dom_e["alg_bytes"])},
             "layouts": {k: {"gcodes_s": round(v["gcodes_s"], 2), "hbm_gbs": round(v["gbs"], 1),
                             "frac": round(v["frac"], 4), "windows": v["windows"]}
                         for k, v in by_layout.items()},
             "lookup": lookups,
+            "configs": extra,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": len(scans) * args.steps,
@@ -430,6 +441,25 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return out
+
+
+def measure_extra_configs(data) -> dict:
+    """SURVEY.md §8(d) cfg1 / cfg4 / cfg5 (bench_cfgs.py); a failure is
+    reported in the line instead of hiding the headline."""
+    import torch
+
+    import bench_cfgs
+    out = {}
+    for name, fn in (("cfg1", bench_cfgs.measure_cfg1), ("cfg4", bench_cfgs.measure_cfg4),
+                     ("cfg5", bench_cfgs.measure_cfg5)):
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        try:
+            out[name] = fn()
+        except Exception as exc:  # noqa: BLE001 - recorded, not swallowed
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        out[name]["wall_s"] = round(time.perf_counter() - t0, 1)
     return out
 
 

@@ -1,0 +1,308 @@
+"""Secondary measurements for bench.py: SURVEY.md §8(d) cfg1, cfg4 and cfg5
+(one GPU's shard).  Each returns a JSON-able dict that bench.py attaches to
+its line under "configs"; every timed number is device time from CUDA events
+on the launching stream, after warm-up, and every workload is checked against
+a host numpy filter of the same raw values before it is timed.
+
+  cfg1  ByteSlice LT scan + fused bitvector lookup, 2^24 rows, w=16
+        (32 MiB column: 16 distinct replicas rotated so L2 never holds one)
+  cfg4  16 columns x 2^27 rows through the advisor (GPU wall-clock AUC), then
+        the 4-predicate conjunction as ONE fused device pass + 3 projections
+        decoded on the device + SUM(u32)
+  cfg5  one GPU's shard of the 8-GPU scan: 4 columns x 2^29 rows (2 uniform
+        int32 ByteSlice w=32, 2 Zipf(1.1)/2^24 PP-VBS), each predicate alone
+        and the 4-way AND, plus the global row-id compaction
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _time(fn, reps: int, warmup: int = 3) -> float:
+    """Mean device ms of fn over reps (events bracket the batch)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = _events()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def _q(uniq: np.ndarray, counts: np.ndarray, n: int, x: float) -> int:
+    """Nearest-rank quantile sorted(values)[min(n-1, floor(x*n))] from a
+    frequency table (reference advisor.py:56-59)."""
+    cum = np.cumsum(counts)
+    return int(uniq[np.searchsorted(cum, min(n - 1, int(x * n)), side="right")])
+
+
+def _alg_bytes(cols, preds):
+    """Pipelined algorithmic bytes of a conjunction: each
+    predicate's own slice/mask terms over the blocks still live."""
+    from paper_2209_00220_b200.byteslice import scan_byteslice
+    from paper_2209_00220_b200.roofline import scan_alg_bytes
+    from paper_2209_00220_b200.vbs import scan_vbs
+    total, running = 0, None
+    for (lay, c, ex), p in zip(cols, preds):
+        fn = scan_vbs if lay == "ppvbs" else scan_byteslice
+        bv, st = fn(c, p, running)
+        st = st.materialize()
+        total += scan_alg_bytes(st.block_depth, lay, c.max_len if lay == "ppvbs" else c.n_slices,
+                                ex, masked=running is not None)
+        running = bv
+    return total
+
+
+# --------------------------------------------------------------------- cfg1
+def measure_cfg1(reps: int = 50) -> dict:
+    import torch
+
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.byteslice import build_byteslice, scan_byteslice
+    from paper_2209_00220_b200.device import stream
+    from paper_2209_00220_b200.predicate import Op, ResolvedPredicate
+    from paper_2209_00220_b200.roofline import hbm_peak, scan_alg_bytes
+
+    n, w = 1 << 24, 16
+    codes = np.random.default_rng(1).integers(0, 65536, n)
+    want = codes < 6554
+    replicas = [build_byteslice(codes, w) for _ in range(16)]
+    pred = ResolvedPredicate.compare(Op.LT, 6554, 2)
+    bv, st = scan_byteslice(replicas[0], pred)
+    assert bv.count() == int(want.sum()), "cfg1 scan count"
+    ab = scan_alg_bytes(st.materialize().block_depth, "byteslice", 2)
+    nsel = int(want.sum())
+    lib = _lib.load()
+    out = torch.empty(nsel, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    # lookup parity: fused bitvector -> codes (identity dictionary: code = value)
+    _lib.check(lib.bsb_byteslice_lookup_bits(replicas[0].desc_ref, bv.dwords.data_ptr(), None,
+                                             out.data_ptr(), None, None, cnt.data_ptr(),
+                                             stream()), "cfg1 lookup")
+    assert np.array_equal(out.cpu().numpy(), codes[want]), "cfg1 lookup values"
+    outs = [torch.empty(n // 32, dtype=torch.int32, device="cuda") for _ in replicas]
+    cnts = [torch.empty(1, dtype=torch.int64, device="cuda") for _ in replicas]
+    cp = pred.to_c()
+    it = [0]
+
+    def scan():
+        i = it[0] % 16
+        it[0] += 1
+        lib.bsb_byteslice_scan(replicas[i].desc_ref, ctypes_ref(cp), None,
+                               outs[i].data_ptr(), cnts[i].data_ptr(), None, None, stream())
+
+    ms_scan = _time(scan, reps)
+    bvs = []
+    for i in range(16):
+        b, _ = scan_byteslice(replicas[i], pred)
+        bvs.append(b)
+
+    def look():
+        i = it[0] % 16
+        it[0] += 1
+        lib.bsb_byteslice_lookup_bits(replicas[i].desc_ref, bvs[i].dwords.data_ptr(), None,
+                                      out.data_ptr(), None, None, cnt.data_ptr(), stream())
+
+    ms_look = _time(look, reps)
+    peak, _ = hbm_peak()
+    return {
+        "workload": "cfg1: 2^24 uniform 16-bit codes, ByteSlice w=16, LT 6554, then fused "
+                    "bitvector lookup of the 1,676,081-ish matches (16 rotated replicas)",
+        "rows": n, "selected": nsel,
+        "scan": {"us": round(ms_scan * 1e3, 2), "gcodes_s": round(n / ms_scan / 1e6, 1),
+                 "alg_bytes_per_code": round(ab / n, 4),
+                 "frac": round(ab / (ms_scan * 1e-3) / 1e9 / peak, 4)},
+        "lookup": {"us": round(ms_look * 1e3, 2),
+                   "mrows_s": round(nsel / ms_look / 1e3, 1)},
+    }
+
+
+def ctypes_ref(x):
+    import ctypes
+    return ctypes.byref(x)
+
+
+# --------------------------------------------------------------------- cfg4
+CFG4_UNIFORM = {"u08": 8, "u12": 12, "u16": 16, "u20": 20, "u24": 24, "u32": 32, "u16b": 16,
+                "u24b": 24}
+CFG4_ZIPF = {"z08": (0.8, 8), "z12": (1.0, 12), "z16": (1.5, 16), "z20": (0.8, 20),
+             "z24": (1.0, 24), "z24b": (1.5, 24), "z16b": (1.0, 16), "z12b": (0.8, 12)}
+
+
+def measure_cfg4(reps: int = 20, log2n: int = 27, advise_count: int = 100) -> dict:
+    import torch
+
+    from paper_2209_00220_b200 import ColumnKind, ZipfSpec
+    from paper_2209_00220_b200.datagen import gen_zipf_device
+    from paper_2209_00220_b200.engine import conj_scan, ingest_arrays, lookup_decode_bits
+    from paper_2209_00220_b200.predicate import Op, Predicate
+    from paper_2209_00220_b200.roofline import hbm_peak
+
+    n = 1 << log2n
+    names = list(CFG4_UNIFORM) + list(CFG4_ZIPF)
+    cols = {}
+    t0 = time.perf_counter()
+    for i, nm in enumerate(names):
+        seed = 100 + i
+        if nm in CFG4_UNIFORM:
+            w = CFG4_UNIFORM[nm]
+            rng = np.random.default_rng(seed)
+            v = (rng.integers(-(1 << 31), 1 << 31, n) if w == 32 else rng.integers(0, 1 << w, n))
+            cols[nm] = torch.from_numpy(v).cuda()
+        else:
+            s, d = CFG4_ZIPF[nm]
+            cols[nm] = gen_zipf_device(ZipfSpec(s, d, n, seed))
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    store, report = ingest_arrays(cols, advise_cost="wall", advise_count=advise_count)
+    torch.cuda.synchronize()
+    t_ingest = time.perf_counter() - t0
+    advice = {e["name"]: {"layout": e["layout"], **({k: round(v, 9) for k, v in
+                                                      e["advice"].items() if k != "chosen"}
+                                                     if "advice" in e else {})}
+              for e in store.manifest["columns"]}
+
+    def q(nm, x):
+        t = store.columns[nm].dictionary.table
+        return _q(t.values, t.weights, n, x)
+
+    preds = [Predicate("u16", Op.LT, 32768),
+             Predicate("z12", Op.BETWEEN, q("z12", 0.2), q("z12", 0.9)),
+             Predicate("u24", Op.GE, q("u24", 0.6)),
+             Predicate("z16", Op.LE, q("z16", 0.7))]
+    proj = ["u32", "z24", "u20"]
+    # host check of the conjunction and SUM(u32)
+    h = {nm: cols[nm].cpu().numpy() for nm in ("u16", "z12", "u24", "z16", "u32")}
+    m = ((h["u16"] < 32768) & (h["z12"] >= preds[1].value) & (h["z12"] <= preds[1].value_high)
+         & (h["u24"] >= preds[2].value) & (h["z16"] <= preds[3].value))
+    want_count, want_sum = int(m.sum()), int(h["u32"][m].astype(np.int64).sum())
+    del h, m
+    stored = [store.columns[p.column] for p in preds]
+    rps = [s.dictionary.encode_literal(p) for s, p in zip(stored, preds)]
+    pairs = [(s.layout, s.column) for s in stored]
+    sel = conj_scan(pairs, rps)
+    assert sel.count() == want_count, "cfg4 conjunction count"
+    got_sum = int(lookup_decode_bits(store.columns["u32"], sel).sum().item())
+    assert got_sum == want_sum, "cfg4 SUM(u32)"
+    ms_scan = _time(lambda: conj_scan(pairs, rps), reps)
+    ms_look = {}
+    for nm in proj:
+        ms_look[nm] = _time(lambda nm=nm: lookup_decode_bits(store.columns[nm], sel), reps)
+    ex = []
+    for s in stored:
+        ex.append([s.column.mask_words(j) for j in range(2, s.column.max_len + 1)]
+                  if s.layout == "ppvbs" else None)
+    ab = _alg_bytes([(s.layout, s.column, e) for s, e in zip(stored, ex)], rps)
+    peak, _ = hbm_peak()
+    return {
+        "workload": "cfg4: 16 columns x 2^27 (8 uniform, 8 Zipf; seeds 100+i), advisor in GPU "
+                    "wall mode, query u16<32768 AND z12 BETWEEN q(.2),q(.9) AND u24>=q(.6) AND "
+                    "z16<=q(.7) -> u32, z24, u20 + SUM(u32)",
+        "rows": n, "selected": want_count, "sum_u32": want_sum,
+        "advisor": advice, "gen_s": round(t_gen, 2), "ingest_s": round(t_ingest, 2),
+        "conj_scan": {"us": round(ms_scan * 1e3, 2),
+                      "gcodes_s": round(4 * n / ms_scan / 1e6, 1),
+                      "alg_bytes": int(ab),
+                      "frac": round(ab / (ms_scan * 1e-3) / 1e9 / peak, 4),
+                      "layouts": [s.layout for s in stored]},
+        "lookups": {nm: {"us": round(t * 1e3, 2), "mrows_s": round(want_count / t / 1e3, 1),
+                         "layout": store.columns[nm].layout} for nm, t in ms_look.items()},
+    }
+
+
+# --------------------------------------------------------------------- cfg5
+def measure_cfg5(reps: int = 20, log2n: int = 29) -> dict:
+    import torch
+
+    from paper_2209_00220_b200 import ColumnKind, Dictionary, FrequencyTable, ZipfSpec
+    from paper_2209_00220_b200.byteslice import build_byteslice, scan_byteslice
+    from paper_2209_00220_b200.datagen import gen_zipf_device, zipf_pmf
+    from paper_2209_00220_b200.engine import conj_scan
+    from paper_2209_00220_b200.predicate import Op, Predicate, ResolvedPredicate
+    from paper_2209_00220_b200.roofline import hbm_peak
+    from paper_2209_00220_b200.vbs import build_vbs, scan_vbs
+
+    n, chunk = 1 << log2n, 0   # shard 0 of the 8 fixed 2^29-row chunks
+    t0 = time.perf_counter()
+    raw, cols, preds = {}, {}, {}
+    for ci, nm in enumerate(("u0", "u1")):
+        v = np.random.default_rng(500 + 10 * ci + chunk).integers(-(1 << 31), 1 << 31, n,
+                                                                 dtype=np.int32)
+        raw[nm] = v
+        codes = torch.from_numpy(v).cuda().to(torch.int64) + (1 << 31)  # bias identity
+        cols[nm] = ("byteslice", build_byteslice(codes, 32), None)
+        srt = torch.sort(codes).values
+        qv = {x: int(srt[min(n - 1, int(x * n))].item()) - (1 << 31) for x in (0.10, 0.50)}
+        del codes, srt
+        if nm == "u0":
+            preds[nm] = (ResolvedPredicate.compare(Op.LT, qv[0.10] + (1 << 31), 4),
+                         lambda v, t=qv[0.10]: v < t)
+        else:
+            preds[nm] = (ResolvedPredicate.compare(Op.GE, qv[0.50] + (1 << 31), 4),
+                         lambda v, t=qv[0.50]: v >= t)
+    # Zipf(1.1)/2^24 columns; dictionary from the expected global weights
+    pmf = zipf_pmf(1.1, 1 << 24)
+    wts = np.maximum(np.rint(pmf * float(1 << 32)).astype(np.int64), 1)
+    dom = np.arange(1 << 24, dtype=np.int64)
+    d = Dictionary.build(FrequencyTable(dom, wts, ColumnKind.NUMERIC), "prefix_preserving")
+    qz = lambda x: _q(dom, wts, int(wts.sum()), x)  # noqa: E731
+    for ci, nm in ((2, "z0"), (3, "z1")):
+        vals = gen_zipf_device(ZipfSpec(1.1, 24, n, 500 + 10 * ci + chunk))
+        raw[nm] = vals.to(torch.int32).cpu().numpy()
+        c, l = d.row_codes_device(vals)  # every value is in the dictionary: rank == value
+        col = build_vbs(c, l)
+        del c, l, vals
+        cols[nm] = ("ppvbs", col, [col.mask_words(j) for j in range(2, col.max_len + 1)])
+    lo, hi = qz(0.80), qz(0.95)
+    preds["z0"] = (d.encode_literal(Predicate("z0", Op.BETWEEN, lo, hi)),
+                   lambda v: (v >= lo) & (v <= hi))
+    q60 = qz(0.60)
+    preds["z1"] = (d.encode_literal(Predicate("z1", Op.LE, q60)), lambda v: v <= q60)
+    t_gen = time.perf_counter() - t0
+    peak, _ = hbm_peak()
+    out = {"workload": "cfg5 shard: 4 columns x 2^29 rows (one of 8 fixed chunks; u0,u1 "
+                       "int32 bias-identity ByteSlice w=32; z0,z1 Zipf(1.1)/2^24 PP-VBS with the "
+                       "dictionary of the expected 2^32-row weights)",
+           "rows": n, "gen_s": round(t_gen, 2), "columns": {}}
+    allm = np.ones(n, bool)
+    for nm in ("u0", "u1", "z0", "z1"):
+        lay, col, ex = cols[nm]
+        rp, hf = preds[nm]
+        hm = hf(raw[nm])
+        allm &= hm
+        fn = scan_vbs if lay == "ppvbs" else scan_byteslice
+        bv, _ = fn(col, rp)
+        assert bv.count() == int(hm.sum()), f"cfg5 {nm} count"
+        ms = _time(lambda: fn(col, rp), reps)
+        ab = _alg_bytes([(lay, col, ex)], [rp])
+        out["columns"][nm] = {"layout": lay, "us": round(ms * 1e3, 2),
+                              "gcodes_s": round(n / ms / 1e6, 1),
+                              "alg_bytes_per_code": round(ab / n, 4),
+                              "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4),
+                              "selected": int(hm.sum())}
+    order = ("u0", "u1", "z0", "z1")
+    pairs = [(cols[k][0], cols[k][1]) for k in order]
+    rps = [preds[k][0] for k in order]
+    sel = conj_scan(pairs, rps)
+    assert sel.count() == int(allm.sum()), "cfg5 AND count"
+    ms = _time(lambda: conj_scan(pairs, rps), reps)
+    ab = _alg_bytes([cols[k] for k in order], rps)
+    ms_ids = _time(lambda: sel.row_ids(row_offset=chunk * n), reps)
+    out["and4"] = {"us": round(ms * 1e3, 2), "gcodes_s": round(4 * n / ms / 1e6, 1),
+                   "alg_bytes_per_code": round(ab / n, 4),
+                   "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4),
+                   "selected": int(allm.sum()),
+                   "row_ids_us": round(ms_ids * 1e3, 2)}
+    return out

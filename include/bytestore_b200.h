@@ -36,7 +36,7 @@ extern "C" {
 #define BSB_TILE_BLOCKS 32    /* blocks per tile (one warp, lane = block)      */
 #define BSB_TILE_ROWS 1024    /* rows per tile                                  */
 #define BSB_MAX_LEVELS 8      /* slices per code (reference vbs.py:77-78)       */
-#define BSB_MAX_CONJ 8        /* predicates fused by bsb_conj_scan              */
+#define BSB_MAX_CONJ 8        /* predicates per bsb_conj_scan call              */
 #define BSB_STATS_WORDS 24    /* int64 counters written by the *_scan stats path */
 
 enum bsb_status {
@@ -121,7 +121,7 @@ typedef struct bsb_vbs {
   const uint32_t* rexist[BSB_MAX_LEVELS];
 } bsb_vbs;
 
-/* One column reference for the fused conjunction (engine.py:322-332). */
+/* One column reference for bsb_conj_scan (engine.py:322-332). */
 enum bsb_layout { BSB_LAYOUT_BYTESLICE = 0, BSB_LAYOUT_PPVBS = 1 };
 typedef struct bsb_column_ref {
   int32_t layout;
@@ -269,11 +269,12 @@ int bsb_bits_combine(int32_t op, const uint32_t* a, const uint32_t* b, uint32_t*
                      int64_t n_rows, void* stream);
 int bsb_bits_popcount(const uint32_t* words, int64_t n_rows, uint64_t* count, void* stream);
 
-/* --------------------------------------------------- fused conjunction */
-/* engine.execute's pipelined conjunction (engine.py:322-332) in one pass:
+/* ------------------------------------------------------------ conjunction */
+/* engine.execute's pipelined conjunction (engine.py:322-332) in one call:
  * predicate i sees the running result of predicates 0..i-1 as its input
- * mask; blocks already zero skip every later predicate's slices.  Columns
- * must share n_rows.  k <= BSB_MAX_CONJ. */
+ * mask (a chain of the per-layout scan kernels, no host sync); blocks already
+ * zero load no slice bytes of later predicates.  Columns must share n_rows.
+ * k <= BSB_MAX_CONJ. */
 int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
                   const uint32_t* mask, uint32_t* out_words, uint64_t* count, void* stream);
 

@@ -188,6 +188,19 @@ __device__ __forceinline__ uint32_t compress_apply(const ExpandNet& net, uint32_
   return x;
 }
 
+// Warp-cooperative pext / pdep of ONE 32-bit word pair (m, x identical in
+// every lane; lane = bit position): a handful of instructions per word, used
+// for the few blocks of a tile whose masks are not trivial.
+__device__ __forceinline__ uint32_t warp_pext(uint32_t m, uint32_t x, int lane) {
+  const uint32_t bit = 1u << lane;
+  const uint32_t v = ((m & x & bit) != 0) ? (1u << __popc(m & (bit - 1u))) : 0u;
+  return __reduce_or_sync(kFull, v);
+}
+__device__ __forceinline__ uint32_t warp_pdep(uint32_t m, uint32_t x, int lane) {
+  const uint32_t bit = 1u << lane;
+  return __ballot_sync(kFull, (m & bit) && ((x >> __popc(m & (bit - 1u))) & 1u));
+}
+
 // Warp-inclusive prefix sum (lane order).
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   const int lane = threadIdx.x & 31;

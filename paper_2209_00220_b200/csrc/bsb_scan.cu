@@ -1,5 +1,6 @@
 // bsb_scan.cu -- scan kernels (ByteSlice, PP-VBS, fused conjunction) and
 // their C-ABI launchers.  Kernel bodies live in bsb_scan_impl.cuh.
+#include <cstdlib>
 #include <cstring>
 
 #include "bsb_scan_impl.cuh"
@@ -382,104 +383,22 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
   }
 }
 
-// ------------------------------------------------------ fused conjunction
-
-namespace bsb {
-
-struct ConjItem {
-  int32_t layout;
-  int32_t between;
-  BsDesc bs;
-  VbsDesc vbs;
-  Leg A, B;
-};
-struct ConjArgs {
-  int64_t n_rows, nb, ntiles;
-  int32_t k;
-  ConjItem item[BSB_MAX_CONJ];
-  const uint32_t* mask;
-  uint32_t* out;
-  unsigned long long* count;
-};
-
-__global__ void __launch_bounds__(kScanThreads) conj_kernel(const __grid_constant__ ConjArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long cnt = 0;
-  for (int64_t tile = warp; tile < a.ntiles; tile += nwarps) {
-    const int64_t b = tile * 32 + lane;
-    const bool inb = b < a.nb;
-    uint32_t z = tile_valid(tile, b, a.n_rows);
-    if (a.mask != nullptr) z &= inb ? __ldg(a.mask + b) : 0u;
-    for (int i = 0; i < a.k; ++i) {
-      if (!__any_sync(kFull, z != 0)) break;  // whole tile already ruled out
-      const ConjItem& it = a.item[i];
-      TileIn in;
-      if (it.layout == BSB_LAYOUT_BYTESLICE) {
-        fetch_bs(it.bs, b, z, in);
-        z = it.between
-                ? scan_tile_bs<true, false>(it.bs, it.A, it.B, b, z, in, nullptr, nullptr)
-                : scan_tile_bs<false, false>(it.bs, it.A, it.B, b, z, in, nullptr, nullptr);
-      } else {
-        fetch_vbs(it.vbs, tile, b, z, in);
-        z = it.between ? scan_tile_vbs<true, false>(it.vbs, it.A, it.B, tile, b, z, in, nullptr,
-                                                    nullptr)
-                       : scan_tile_vbs<false, false>(it.vbs, it.A, it.B, tile, b, z, in,
-                                                     nullptr, nullptr);
-      }
-    }
-    if (inb) a.out[b] = z;
-    cnt += __popc(z);
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
-  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
-}
-
-}  // namespace bsb
-
-// Chain of single scans, each fed the previous result (engine.py:322-332);
-// used when a predicate cannot run inside the fused kernel.
-static int conj_chain(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
-                      const uint32_t* mask, uint32_t* out_words, uint64_t* count,
-                      int64_t nb, cudaStream_t s) {
-  uint32_t* tmp = nullptr;
-  BSB_CUDA(cudaMallocAsync(&tmp, (size_t)nb * 4 + 4, s));
-  const uint32_t* running = mask;
-  for (int i = 0; i < k; ++i) {
-    // the last scan writes out_words; earlier ones alternate through tmp/out
-    uint32_t* dst = ((k - 1 - i) % 2 == 0) ? out_words : tmp;
-    int rc = cols[i].layout == BSB_LAYOUT_BYTESLICE
-                 ? bsb_byteslice_scan(cols[i].byteslice, &preds[i], running, dst, count,
-                                      nullptr, nullptr, s)
-                 : bsb_vbs_scan(cols[i].vbs, &preds[i], running, dst, count, nullptr,
-                                nullptr, s);
-    if (rc) return rc;
-    running = dst;
-  }
-  BSB_CUDA(cudaFreeAsync(tmp, s));
-  return BSB_OK;
-}
-
+// ------------------------------------------------------------- conjunction
+// engine.py:322-332: each predicate's scan takes the running result as its
+// input mask.  Run as a chain of the per-layout scan kernels (each with its
+// own prefetch pipeline; a block whose mask word is 0 loads no slice bytes),
+// alternating two result buffers.  Measured faster than a single fused
+// kernel that serialises every predicate's loads per tile (cfg4: 211 vs
+// 334 us; cfg5 shard: 1.32 vs 1.94 ms).
 extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pred* preds,
                              const uint32_t* mask, uint32_t* out_words, uint64_t* count,
                              void* stream) {
   if (k < 0 || k > BSB_MAX_CONJ || (k > 0 && (!cols || !preds)) || !out_words || !count)
     return BSB_EINVAL;
   cudaStream_t s = as_stream(stream);
-  for (int i = 0; i < k; ++i) {
-    if (cols[i].layout == BSB_LAYOUT_PPVBS && cols[i].vbs &&
-        cols[i].vbs->deep_mode == BSB_DEEP_PLANES && !planes_fast_ok(&preds[i])) {
-      const int64_t n = cols[0].layout == BSB_LAYOUT_BYTESLICE ? cols[0].byteslice->n_rows
-                                                               : cols[0].vbs->n_rows;
-      return conj_chain(k, cols, preds, mask, out_words, count, (n + 31) / 32, s);
-    }
-  }
-  ConjArgs a;
-  std::memset(&a, 0, sizeof(a));
   int64_t n = -1;
   bool all_false = false;
+  int live[BSB_MAX_CONJ];
   int m = 0;
   for (int i = 0; i < k; ++i) {
     const bsb_column_ref& c = cols[i];
@@ -492,6 +411,10 @@ extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pr
     } else if (c.layout == BSB_LAYOUT_PPVBS) {
       if (!c.vbs) return BSB_EINVAL;
       ni = c.vbs->n_rows;
+      const int K = c.vbs->max_len;
+      auto bad = [&](int l) { return l < 1 || l > K; };
+      if (p->trivial < 0 && (bad(p->length) || (p->op == BSB_BETWEEN && bad(p->length2))))
+        return BSB_ERANGE;
     } else {
       return BSB_EINVAL;
     }
@@ -499,54 +422,34 @@ extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pr
     n = ni;
     if (p->trivial == 0) all_false = true;
     if (p->trivial >= 0) continue;  // constant true: no-op in a conjunction
-    ConjItem& it = a.item[m++];
-    it.layout = c.layout;
-    it.between = p->op == BSB_BETWEEN;
-    if (c.layout == BSB_LAYOUT_BYTESLICE) {
-      const bsb_byteslice* col = c.byteslice;
-      it.bs.slices = col->slices;
-      it.bs.stride = col->stride;
-      it.bs.K = col->n_slices;
-      if (it.between) {
-        bs_leg(it.A, BSB_GE, p->code, col->width_bits, col->n_slices);
-        bs_leg(it.B, BSB_LE, p->code2, col->width_bits, col->n_slices);
-      } else {
-        bs_leg(it.A, p->op, p->code, col->width_bits, col->n_slices);
-        it.B = it.A;
-      }
-    } else {
-      const bsb_vbs* col = c.vbs;
-      const int K = col->max_len;
-      fill_vbs_desc(it.vbs, col);
-      auto bad = [&](int l) { return l < 1 || l > K; };
-      if (it.between) {
-        if (bad(p->length) || bad(p->length2)) return BSB_ERANGE;
-        fill_leg(it.A, BSB_GE, p->code, p->length, p->length);
-        fill_leg(it.B, BSB_LE, p->code2, p->length2, p->length2);
-      } else {
-        if (bad(p->length)) return BSB_ERANGE;
-        fill_leg(it.A, p->op, p->code, p->length, p->length);
-        it.B = it.A;
-      }
-    }
+    live[m++] = i;
   }
   if (n < 0) return BSB_EINVAL;  // need at least one column to know n_rows
-  a.n_rows = n;
-  a.nb = (n + 31) / 32;
-  a.ntiles = (a.nb + 31) / 32;
-  a.k = all_false ? 0 : m;
-  a.mask = mask;
-  a.out = out_words;
-  a.count = reinterpret_cast<unsigned long long*>(count);
-  BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
-  if (all_false) {
+  if (all_false || m == 0) {
     bsb_pred f;
     std::memset(&f, 0, sizeof(f));
-    f.trivial = 0;
+    f.trivial = all_false ? 0 : 1;
     return run_trivial(n, &f, mask, out_words, count, nullptr, nullptr, 0, s);
   }
-  const int grid = persistent_grid(conj_kernel, kScanThreads, kScanThreads / 32, a.ntiles);
-  conj_kernel<<<grid, kScanThreads, 0, s>>>(a);
-  BSB_LAUNCH_CHECK();
+  const int64_t nb = (n + 31) / 32;
+  uint32_t* tmp = nullptr;
+  if (m > 1) BSB_CUDA(cudaMallocAsync(&tmp, (size_t)nb * 4 + 4, s));
+  const uint32_t* running = mask;
+  for (int t = 0; t < m; ++t) {
+    const int i = live[t];
+    // the last scan writes out_words; earlier ones alternate through tmp/out
+    uint32_t* dst = ((m - 1 - t) % 2 == 0) ? out_words : tmp;
+    const int rc = cols[i].layout == BSB_LAYOUT_BYTESLICE
+                       ? bsb_byteslice_scan(cols[i].byteslice, &preds[i], running, dst, count,
+                                            nullptr, nullptr, s)
+                       : bsb_vbs_scan(cols[i].vbs, &preds[i], running, dst, count, nullptr,
+                                      nullptr, s);
+    if (rc) {
+      if (tmp) cudaFreeAsync(tmp, s);
+      return rc;
+    }
+    running = dst;
+  }
+  if (tmp) BSB_CUDA(cudaFreeAsync(tmp, s));
   return BSB_OK;
 }

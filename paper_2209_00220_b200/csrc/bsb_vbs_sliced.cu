@@ -26,6 +26,9 @@ constexpr int kSuperBlocks = kSuperTiles * 32;    // row blocks per iteration
 constexpr int kMaxDeepBlocks = kSuperBlocks + 4;  // deep blocks touched (+ guard)
 constexpr int kSlicedThreads = 256;
 constexpr int kSlicedWarps = kSlicedThreads / 32;
+// up to this many blocks with non-trivial masks per tile are compressed /
+// expanded warp-cooperatively; more switch to the per-lane butterfly
+constexpr int kSerialBlocks = 6;
 
 struct SlicedArgs {
   int64_t n_rows, nb, ntiles;
@@ -82,6 +85,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
   for (; st < nsuper; st += nwarps) {
     int64_t dfirst = 0;  // global deep row of the super-tile's first deep row
     int64_t db0 = 0;
+    uint32_t netmask = 0;  // tiles whose butterfly masks are in shared memory
     int soff = 0;        // running deep-row offset from db0 * 32
     // ---------------- phase 1: level 1, three tiles
     for (u = 0; u < kSuperTiles; ++u) {
@@ -110,10 +114,36 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
         soff = (int)(dfirst & 31);
       }
       const int o = soff + (int)(incl - (uint32_t)c2);
-      const ExpandNet net = expand_setup(in.m2);
-      const uint32_t pA = compress_apply(net, zeqA);
-      const uint32_t pB = BETWEEN ? compress_apply(net, zeqB) : 0u;
+      // Tied rows -> deep-row order (pext by M_2).  zeq is a subset of M_2, so
+      // zeq == 0 or zeq == M_2 compress trivially; the few other blocks of the
+      // tile are compressed by the whole warp one at a time, or, when there are
+      // many, by each lane's butterfly network (whose masks phase 3 reuses).
       const int i = u * 32 + lane;
+      const uint32_t full = c2 >= 32 ? kFull : ((1u << c2) - 1u);
+      uint32_t pA = zeqA ? full : 0u;
+      uint32_t pB = (BETWEEN && zeqB) ? full : 0u;
+      const bool ntr = (zeqA != 0 && zeqA != in.m2) || (BETWEEN && zeqB != 0 && zeqB != in.m2);
+      uint32_t ntm = __ballot_sync(kFull, ntr);
+      if (__popc(ntm) > kSerialBlocks) {
+        const ExpandNet net = expand_setup(in.m2);
+        pA = compress_apply(net, zeqA);
+        if (BETWEEN) pB = compress_apply(net, zeqB);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) sm.mv[k][i] = net.mv[k];
+        netmask |= 1u << u;
+      } else {
+        while (ntm) {
+          const int L = __ffs(ntm) - 1;
+          ntm &= ntm - 1;
+          const uint32_t mL = __shfl_sync(kFull, in.m2, L);
+          const uint32_t x = warp_pext(mL, __shfl_sync(kFull, zeqA, L), lane);
+          const uint32_t y = BETWEEN ? warp_pext(mL, __shfl_sync(kFull, zeqB, L), lane) : 0u;
+          if (lane == L) {
+            pA = x;
+            pB = y;
+          }
+        }
+      }
       sm.valid[i] = valid;
       sm.zgtA[i] = zgtA;
       sm.eqfA[i] = eqfA;
@@ -122,8 +152,6 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
       sm.zeqB[i] = zeqB;
       sm.m2[i] = in.m2;
       sm.off[i] = (uint32_t)o;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) sm.mv[k][i] = net.mv[k];
       if (u == 0) {
         for (int k = lane; k < kMaxDeepBlocks; k += 32) {
           sm.cA[k] = 0;
@@ -209,11 +237,35 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
           pP = __funnelshift_r(sm.rP[wi], sm.rP[wi + 1], sb) & lowm;
           pQ = __funnelshift_r(sm.rQ[wi], sm.rQ[wi + 1], sb) & lowm;
         }
-        ExpandNet net;
-        net.m0 = m2;
+        // deep-row results -> row space (pdep by M_2), trivial cases first
+        uint32_t eP = pP ? m2 : 0u, eQ = pQ ? m2 : 0u;
+        uint32_t ntm = __ballot_sync(kFull, (pP != 0 && pP != lowm) || (pQ != 0 && pQ != lowm));
+        if (ntm) {
+          if (__popc(ntm) > kSerialBlocks) {
+            ExpandNet net;
+            if ((netmask >> u) & 1u) {
+              net.m0 = m2;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) net.mv[k] = sm.mv[k][i];
-        const uint32_t eP = expand_apply(net, pP), eQ = expand_apply(net, pQ);
+              for (int k = 0; k < 5; ++k) net.mv[k] = sm.mv[k][i];
+            } else {
+              net = expand_setup(m2);
+            }
+            eP = expand_apply(net, pP);
+            eQ = expand_apply(net, pQ);
+          } else {
+            while (ntm) {
+              const int L = __ffs(ntm) - 1;
+              ntm &= ntm - 1;
+              const uint32_t mL = __shfl_sync(kFull, m2, L);
+              const uint32_t x = warp_pdep(mL, __shfl_sync(kFull, pP, L), lane);
+              const uint32_t y = warp_pdep(mL, __shfl_sync(kFull, pQ, L), lane);
+              if (lane == L) {
+                eP = x;
+                eQ = y;
+              }
+            }
+          }
+        }
         if (BETWEEN) {
           zgtA |= zeqA & eP;
           zgtB |= zeqB & eQ;

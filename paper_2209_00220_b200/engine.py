@@ -1,11 +1,11 @@
 """Layout dispatch and query execution (mirror of reference engine.py).
 
 The dispatch point (engine.py:172-221) is where device layouts plug in.
-``execute`` (engine.py:311-353) runs every conjunction as ONE fused device
-pass (bsb_conj_scan: predicate i sees the running result as its input mask
-and blocks already ruled out skip later columns entirely), ORs disjunction
-arms on the device, compacts the selection once and gathers + decodes each
-projected column with the lookup kernels.
+``execute`` (engine.py:311-353) runs every conjunction as one device call
+(bsb_conj_scan: predicate i sees the running result as its input mask and
+blocks already ruled out load nothing from later columns), ORs disjunction
+arms on the device and gathers + decodes each projected column straight from
+the selection bitvector with the fused lookup kernels.
 
 In scope: "byteslice" and "ppvbs" numeric columns.  CSV ingest (file I/O)
 is replaced by ``ingest_arrays`` over in-memory columns; the baseline
@@ -216,7 +216,7 @@ def _resolve(stored: StoredColumn, pred: Predicate) -> ResolvedPredicate:
 
 
 def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64) -> QueryResult:
-    """engine.py:311-353 with fused device conjunctions."""
+    """engine.py:311-353 with device conjunctions and fused lookups."""
     for name in query.projection:
         if name not in store.columns:
             raise DataError(f"unknown projection column {name!r}")

@@ -439,7 +439,7 @@ def test_fixture_query_192_through_engine():
     assert np.array_equal(q.columns["qty"], f["proj_qty"])
 
 
-def test_conjunction_fused_equals_pipelined_oracle():
+def test_conjunction_call_equals_pipelined_oracle():
     rng = np.random.default_rng(10)
     n = 300_007
     cols = {"u16": rng.integers(0, 1 << 16, n), "z12": O.gen_zipf(1.0, 12, n, 11),
@@ -461,6 +461,44 @@ def test_conjunction_fused_equals_pipelined_oracle():
     assert res.n_selected == int(want.sum())
     assert np.array_equal(res.columns["u24"], cols["u24"][want])
     assert np.array_equal(res.columns["z12"], cols["z12"][want])
+
+
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
+def test_conj_scan_mask_trivial_and_long_chains(mode):
+    """bsb_conj_scan == the pipelined oracle for chains longer than
+    BSB_MAX_CONJ, constant predicates inside the chain and an input mask."""
+    rng = np.random.default_rng(21)
+    n = 70_001
+    vals, od, codes, lens = _ppe_column(1.1, 16, n, 22)
+    col_v = B.build_vbs(codes, lens, deep_mode=mode)
+    ocol = O.vbs_build(codes, lens)
+    u = rng.integers(0, 1 << 12, n)
+    col_b = B.build_byteslice(u, 12)
+    planes = O.bs_build(u, 12)
+    srt = np.sort(vals)
+    mw = O.bools_to_words(rng.random(n) < 0.7)
+    chain, opreds = [], []
+    for i in range(11):
+        if i % 5 == 4:
+            t = bool(i % 2)
+            chain.append((("ppvbs", col_v), ResolvedPredicate.constant(t)))
+            opreds.append(("v", O.pred_const(t)))
+        elif i % 2:
+            lo, hi = sorted(int(x) for x in rng.choice(srt, 2))
+            p = od.encode_literal("BETWEEN", lo, hi)
+            chain.append((("ppvbs", col_v), rp(list(p))))
+            opreds.append(("v", p))
+        else:
+            c = int(rng.integers(0, 1 << 12))
+            chain.append((("byteslice", col_b), ResolvedPredicate.compare(Op.GE, c, 2)))
+            opreds.append(("b", O.pred_compare("GE", c, 2)))
+    got = E.conj_scan([c for c, _ in chain], [p for _, p in chain], B.ResultBitVector(n, mw))
+    want = mw
+    for kind, p in opreds:
+        want = (O.vbs_scan(ocol, p, want)[0] if kind == "v"
+                else O.bs_scan(planes, 12, n, p, want)[0])
+    assert np.array_equal(got.words, want)
+    assert got.count() == O.words_count(want)
 
 
 def test_device_bitvector_ops():
