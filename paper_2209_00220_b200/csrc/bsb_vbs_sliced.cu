@@ -32,6 +32,8 @@ constexpr int kSerialBlocks = 6;
 
 struct SlicedArgs {
   int64_t n_rows, nb, ntiles;
+  int64_t full_tiles;  // tiles whose 1024 rows are all < n_rows
+  int serial_blocks;   // warp-cooperative pext/pdep up to this many blocks
   VbsDesc d;
   Leg A, B;
   const uint32_t* mask;
@@ -65,54 +67,59 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
   const int64_t nsuper = (a.ntiles + kSuperTiles - 1) / kSuperTiles;
   unsigned long long cnt = 0;
 
+  // valid rows of block b of tile t (input mask applied); 0 past the column
   auto tile_valid_word = [&](int64_t tile, int64_t b) -> uint32_t {
-    if (tile >= a.ntiles) return 0u;
-    uint32_t v = ((tile + 1) * kTileRows <= a.n_rows) ? kFull : tail_valid(b, a.n_rows);
+    uint32_t v = tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
     if (MASKED) v &= b < a.nb ? __ldg(a.mask + b) : 0u;
     return v;
+  };
+  // level-1 sector + level-2 existence word of block b (zeros when invalid)
+  auto fetch = [&](int64_t b, uint32_t valid, TileIn& t) {
+    if (valid) {
+      ldg256(d.bs1 + b * 32, t.w);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t.w[i] = 0;
+    }
+    t.m2 = (K >= 2 && b < a.nb) ? __ldg(d.exist[1] + b) : 0u;
   };
 
   // prefetch pipeline over the flattened tile sequence of this warp
   int64_t st = warp;
-  int u = 0;
   TileIn inN;
   uint32_t vN = 0;
   if (st < nsuper) {
-    const int64_t t0 = st * kSuperTiles;
-    vN = tile_valid_word(t0, t0 * 32 + lane);
-    fetch_vbs(d, t0 < a.ntiles ? t0 : 0, t0 * 32 + lane, vN, inN);
+    const int64_t b0 = st * kSuperTiles * 32 + lane;
+    vN = tile_valid_word(st * kSuperTiles, b0);
+    fetch(b0, vN, inN);
   }
   for (; st < nsuper; st += nwarps) {
-    int64_t dfirst = 0;  // global deep row of the super-tile's first deep row
-    int64_t db0 = 0;
+    // global deep row of the super-tile's first deep row
+    const int64_t dfirst = K >= 2 ? __ldg(d.dir[1] + st * kSuperTiles * 32) : 0;
+    const int64_t db0 = dfirst >> 5;
     uint32_t netmask = 0;  // tiles whose butterfly masks are in shared memory
-    int soff = 0;        // running deep-row offset from db0 * 32
+    int soff = (int)(dfirst & 31);  // running deep-row offset from db0 * 32
+    for (int k = lane; k < kMaxDeepBlocks; k += 32) {
+      sm.cA[k] = 0;
+      sm.cB[k] = 0;
+    }
     // ---------------- phase 1: level 1, three tiles
-    for (u = 0; u < kSuperTiles; ++u) {
+#pragma unroll
+    for (int u = 0; u < kSuperTiles; ++u) {
       const int64_t tile = st * kSuperTiles + u;
-      const int64_t b = tile * 32 + lane;
       const uint32_t valid = vN;
       const TileIn in = inN;
       // prefetch the next tile in this warp's sequence
-      int64_t ntile = (u + 1 < kSuperTiles) ? tile + 1 : (st + nwarps) * kSuperTiles;
-      if (ntile < a.ntiles) {
-        vN = tile_valid_word(ntile, ntile * 32 + lane);
-        fetch_vbs(d, ntile, ntile * 32 + lane, vN, inN);
-      } else {
-        vN = 0;
-        inN.m2 = 0;  // past the column: no deep rows
-      }
+      const int64_t ntile = (u + 1 < kSuperTiles) ? tile + 1 : (st + nwarps) * kSuperTiles;
+      const int64_t nb_ = ntile * 32 + lane;
+      vN = tile_valid_word(ntile, nb_);
+      fetch(nb_, vN, inN);
       uint32_t zeqA = valid, zgtA = 0, eqfA = 0, zeqB = valid, zgtB = 0, eqfB = 0;
       int depth = 0;
       vbs_level1<BETWEEN, false>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB,
                                  nullptr, depth);
       const int c2 = __popc(in.m2);
       const uint32_t incl = warp_incl_scan((uint32_t)c2);
-      if (u == 0) {
-        dfirst = __shfl_sync(kFull, in.base, 0);
-        db0 = dfirst >> 5;
-        soff = (int)(dfirst & 31);
-      }
       const int o = soff + (int)(incl - (uint32_t)c2);
       // Tied rows -> deep-row order (pext by M_2).  zeq is a subset of M_2, so
       // zeq == 0 or zeq == M_2 compress trivially; the few other blocks of the
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
       uint32_t pB = (BETWEEN && zeqB) ? full : 0u;
       const bool ntr = (zeqA != 0 && zeqA != in.m2) || (BETWEEN && zeqB != 0 && zeqB != in.m2);
       uint32_t ntm = __ballot_sync(kFull, ntr);
-      if (__popc(ntm) > kSerialBlocks) {
+      if (__popc(ntm) > a.serial_blocks) {
         const ExpandNet net = expand_setup(in.m2);
         pA = compress_apply(net, zeqA);
         if (BETWEEN) pB = compress_apply(net, zeqB);
@@ -152,12 +159,6 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
       sm.zeqB[i] = zeqB;
       sm.m2[i] = in.m2;
       sm.off[i] = (uint32_t)o;
-      if (u == 0) {
-        for (int k = lane; k < kMaxDeepBlocks; k += 32) {
-          sm.cA[k] = 0;
-          sm.cB[k] = 0;
-        }
-      }
       __syncwarp();
       const int wi = o >> 5, sb = o & 31;
       const bool spill = sb != 0 && sb + c2 > 32;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
     __syncwarp();
     // ---------------- phase 3: back to row space
 #pragma unroll 1
-    for (u = 0; u < kSuperTiles; ++u) {
+    for (int u = 0; u < kSuperTiles; ++u) {
       const int64_t tile = st * kSuperTiles + u;
       if (tile >= a.ntiles) break;
       const int64_t b = tile * 32 + lane;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
         uint32_t eP = pP ? m2 : 0u, eQ = pQ ? m2 : 0u;
         uint32_t ntm = __ballot_sync(kFull, (pP != 0 && pP != lowm) || (pQ != 0 && pQ != lowm));
         if (ntm) {
-          if (__popc(ntm) > kSerialBlocks) {
+          if (__popc(ntm) > a.serial_blocks) {
             ExpandNet net;
             if ((netmask >> u) & 1u) {
               net.m0 = m2;
@@ -329,6 +330,13 @@ int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B
   a.n_rows = n_rows;
   a.nb = (n_rows + 31) / 32;
   a.ntiles = (a.nb + 31) / 32;
+  a.full_tiles = n_rows / kTileRows;
+  static int serial = -1;
+  if (serial < 0) {
+    const char* e = std::getenv("BSB_SLICED_SERIAL");
+    serial = e ? std::atoi(e) : kSerialBlocks;
+  }
+  a.serial_blocks = serial;
   a.d = d;
   a.A = A;
   a.B = B;
