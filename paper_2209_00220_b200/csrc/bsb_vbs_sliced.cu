@@ -45,7 +45,6 @@ struct SlicedSmem {
   // per row block: level-1 state + butterfly stage masks
   uint32_t valid[kSuperBlocks], zgtA[kSuperBlocks], eqfA[kSuperBlocks], zeqA[kSuperBlocks];
   uint32_t zgtB[kSuperBlocks], zeqB[kSuperBlocks], m2[kSuperBlocks], off[kSuperBlocks];
-  uint32_t mv[5][kSuperBlocks];
   // per deep block: candidates in, results out
   uint32_t cA[kMaxDeepBlocks], cB[kMaxDeepBlocks], rP[kMaxDeepBlocks], rQ[kMaxDeepBlocks];
 };
@@ -97,7 +96,6 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
     // global deep row of the super-tile's first deep row
     const int64_t dfirst = K >= 2 ? __ldg(d.dir[1] + st * kSuperTiles * 32) : 0;
     const int64_t db0 = dfirst >> 5;
-    uint32_t netmask = 0;  // tiles whose butterfly masks are in shared memory
     int soff = (int)(dfirst & 31);  // running deep-row offset from db0 * 32
     for (int k = lane; k < kMaxDeepBlocks; k += 32) {
       sm.cA[k] = 0;
@@ -135,9 +133,6 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
         const ExpandNet net = expand_setup(in.m2);
         pA = compress_apply(net, zeqA);
         if (BETWEEN) pB = compress_apply(net, zeqB);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) sm.mv[k][i] = net.mv[k];
-        netmask |= 1u << u;
       } else {
         while (ntm) {
           const int L = __ffs(ntm) - 1;
@@ -243,14 +238,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
         uint32_t ntm = __ballot_sync(kFull, (pP != 0 && pP != lowm) || (pQ != 0 && pQ != lowm));
         if (ntm) {
           if (__popc(ntm) > a.serial_blocks) {
-            ExpandNet net;
-            if ((netmask >> u) & 1u) {
-              net.m0 = m2;
-#pragma unroll
-              for (int k = 0; k < 5; ++k) net.mv[k] = sm.mv[k][i];
-            } else {
-              net = expand_setup(m2);
-            }
+            const ExpandNet net = expand_setup(m2);
             eP = expand_apply(net, pP);
             eQ = expand_apply(net, pQ);
           } else {
@@ -315,9 +303,10 @@ static int launch_sliced(const SlicedArgs& a, cudaStream_t s) {
   static int minb = -1;
   if (minb < 0) {
     const char* e = std::getenv("BSB_SLICED_MINB");
-    minb = (e && std::atoi(e) == 3) ? 3 : 4;
+    minb = e ? std::atoi(e) : 4;
   }
   if (minb == 3) return launch_sliced_k<BETWEEN, MASKED, 3>(a, s);
+  if (minb == 5) return launch_sliced_k<BETWEEN, MASKED, 5>(a, s);
   return launch_sliced_k<BETWEEN, MASKED, 4>(a, s);
 }
 
