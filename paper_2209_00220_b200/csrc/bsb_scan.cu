@@ -323,7 +323,8 @@ namespace bsb {
 int vbs_rows_scan(const VbsDesc& d, int64_t n_rows, const bsb_pred* p, const uint32_t* mask,
                   uint32_t* out, uint64_t* count, int64_t* stats, int8_t* depth,
                   cudaStream_t s);
-int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B, bool between,
+int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const Leg& A,
+                    const Leg& B, bool between,
                     const uint32_t* mask, uint32_t* out, unsigned long long* count,
                     cudaStream_t s);
 }
@@ -377,8 +378,8 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
       return K <= 5 ? scan_dispatch<1 + BSB_DEEP_PLANES>(a, pred, K, s)
                     : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
     case BSB_DEEP_SLICED:
-      return vbs_sliced_scan(a.vbs, a.n_rows, a.A, a.B, pred->op == BSB_BETWEEN, mask,
-                             out_words, a.count, s);
+      return vbs_sliced_scan(a.vbs, a.n_rows, K >= 2 ? col->deep_len[1] : 0, a.A, a.B,
+                             pred->op == BSB_BETWEEN, mask, out_words, a.count, s);
     default: return BSB_EINVAL;
   }
 }

@@ -21,9 +21,14 @@
 
 namespace bsb {
 
-constexpr int kSuperTiles = 3;                    // tiles per warp iteration
-constexpr int kSuperBlocks = kSuperTiles * 32;    // row blocks per iteration
-constexpr int kMaxDeepBlocks = kSuperBlocks + 4;  // deep blocks touched (+ guard)
+// Tiles per warp iteration (ST) is a template argument chosen per column so
+// that a super-tile's deep rows fill about one warp of deep blocks.
+template <int ST>
+struct SuperTile {
+  static constexpr int kTiles = ST;
+  static constexpr int kBlocks = ST * 32;           // row blocks per iteration
+  static constexpr int kMaxDeepBlocks = ST * 32 + 4;  // deep blocks touched (+ guard)
+};
 constexpr int kSlicedThreads = 256;
 constexpr int kSlicedWarps = kSlicedThreads / 32;
 // up to this many blocks with non-trivial masks per tile are compressed /
@@ -41,19 +46,23 @@ struct SlicedArgs {
   unsigned long long* count;
 };
 
+template <int ST>
 struct SlicedSmem {
-  // per row block: level-1 state + butterfly stage masks
-  uint32_t valid[kSuperBlocks], zgtA[kSuperBlocks], eqfA[kSuperBlocks], zeqA[kSuperBlocks];
-  uint32_t zgtB[kSuperBlocks], zeqB[kSuperBlocks], m2[kSuperBlocks], off[kSuperBlocks];
+  static constexpr int NB = SuperTile<ST>::kBlocks, ND = SuperTile<ST>::kMaxDeepBlocks;
+  // per row block: level-1 state
+  uint32_t valid[NB], zgtA[NB], eqfA[NB], zeqA[NB];
+  uint32_t zgtB[NB], zeqB[NB], m2[NB], off[NB];
   // per deep block: candidates in, results out
-  uint32_t cA[kMaxDeepBlocks], cB[kMaxDeepBlocks], rP[kMaxDeepBlocks], rQ[kMaxDeepBlocks];
+  uint32_t cA[ND], cB[ND], rP[ND], rQ[ND];
 };
 
-template <bool BETWEEN, bool MASKED, int MINB>
+template <bool BETWEEN, bool MASKED, int MINB, int ST>
 __global__ void __launch_bounds__(kSlicedThreads, MINB)
     vbs_sliced_kernel(const __grid_constant__ SlicedArgs a) {
+  constexpr int kSuperTiles = SuperTile<ST>::kTiles;
+  constexpr int kMaxDeepBlocks = SuperTile<ST>::kMaxDeepBlocks;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SlicedSmem& sm = reinterpret_cast<SlicedSmem*>(smem_raw)[threadIdx.x >> 5];
+  SlicedSmem<ST>& sm = reinterpret_cast<SlicedSmem<ST>*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -275,10 +284,11 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool MASKED, int MINB>
+template <bool BETWEEN, bool MASKED, int MINB, int ST>
 static int launch_sliced_k(const SlicedArgs& a, cudaStream_t s) {
-  auto kern = vbs_sliced_kernel<BETWEEN, MASKED, MINB>;
-  const size_t smem = sizeof(SlicedSmem) * kSlicedWarps;
+  constexpr int kSuperTiles = ST;
+  auto kern = vbs_sliced_kernel<BETWEEN, MASKED, MINB, ST>;
+  const size_t smem = sizeof(SlicedSmem<ST>) * kSlicedWarps;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -299,19 +309,33 @@ static int launch_sliced_k(const SlicedArgs& a, cudaStream_t s) {
 // Occupancy variant: 4 resident CTAs (64 registers) by default;
 // BSB_SLICED_MINB=3 selects the 80-register build (tuning experiments).
 template <bool BETWEEN, bool MASKED>
-static int launch_sliced(const SlicedArgs& a, cudaStream_t s) {
-  static int minb = -1;
+static int launch_sliced(const SlicedArgs& a, int64_t deep_rows, cudaStream_t s) {
+  static int minb = -1, st_env = -1;
   if (minb < 0) {
     const char* e = std::getenv("BSB_SLICED_MINB");
-    minb = e ? std::atoi(e) : 4;
+    minb = (e && std::atoi(e) == 3) ? 3 : 4;
+    const char* t = std::getenv("BSB_SLICED_TILES");
+    st_env = t ? std::atoi(t) : 0;
   }
-  if (minb == 3) return launch_sliced_k<BETWEEN, MASKED, 3>(a, s);
-  if (minb == 5) return launch_sliced_k<BETWEEN, MASKED, 5>(a, s);
-  return launch_sliced_k<BETWEEN, MASKED, 4>(a, s);
+  // tiles per super-tile: about 28 deep blocks (of 32 lanes) per phase 2
+  int st = st_env;
+  if (st < 1 || st > 4) {
+    const double per_tile = 32.0 * (double)deep_rows / (double)(a.n_rows > 0 ? a.n_rows : 1);
+    st = per_tile > 0 ? (int)(28.0 / per_tile + 0.5) : 4;
+    st = st < 1 ? 1 : (st > 4 ? 4 : st);
+  }
+  if (minb == 3) return launch_sliced_k<BETWEEN, MASKED, 3, 3>(a, s);
+  switch (st) {
+    case 1: return launch_sliced_k<BETWEEN, MASKED, 4, 1>(a, s);
+    case 2: return launch_sliced_k<BETWEEN, MASKED, 4, 2>(a, s);
+    case 3: return launch_sliced_k<BETWEEN, MASKED, 4, 3>(a, s);
+    default: return launch_sliced_k<BETWEEN, MASKED, 4, 4>(a, s);
+  }
 }
 
 // Non-stats scan of a SLICED column (BETWEEN fused).  Legs as in ScanArgs.
-int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B, bool between,
+int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const Leg& A,
+                    const Leg& B, bool between,
                     const uint32_t* mask, uint32_t* out, unsigned long long* count,
                     cudaStream_t s) {
   SlicedArgs a;
@@ -333,8 +357,11 @@ int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, const Leg& A, const Leg& B
   a.out = out;
   a.count = count;
   BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
-  if (between) return mask ? launch_sliced<true, true>(a, s) : launch_sliced<true, false>(a, s);
-  return mask ? launch_sliced<false, true>(a, s) : launch_sliced<false, false>(a, s);
+  if (between)
+    return mask ? launch_sliced<true, true>(a, deep_rows, s)
+                : launch_sliced<true, false>(a, deep_rows, s);
+  return mask ? launch_sliced<false, true>(a, deep_rows, s)
+              : launch_sliced<false, false>(a, deep_rows, s);
 }
 
 }  // namespace bsb
