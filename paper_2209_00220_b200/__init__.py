@@ -23,6 +23,7 @@ _LAZY = {
     "VbsColumn": "vbs", "build_vbs": "vbs", "scan_vbs": "vbs", "lookup_vbs": "vbs",
     "lookup_vbs_rows": "vbs", "lookup_vbs_rows_dec": "vbs", "lookup_vbs_bits": "vbs",
     "vbs_size_report": "vbs",
+    "write_store": "store", "read_store": "store", "store_bytes": "store",
     "ColumnKind": "dictionary", "FrequencyTable": "dictionary", "CodeAssignment": "dictionary",
     "Dictionary": "dictionary", "build_frequency_table": "dictionary",
     "ppe_numerical": "dictionary", "fixed_assignment": "dictionary",
