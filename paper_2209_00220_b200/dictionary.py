@@ -1,14 +1,17 @@
-"""Dictionary encoders (mirror of reference dictionary.py, numeric columns).
+"""Dictionary encoders (mirror of reference dictionary.py).
 
-Device work: the frequency table + row ranks come from one radix sort on the
-GPU (bsb_freq_table); encode_rows is a device binary search; row codes are a
-device gather.  Host work (O(distinct)): ppe_numerical in C++
+Numeric columns: the frequency table + row ranks come from one radix sort on
+the GPU (bsb_freq_table); encode_rows is a device binary search; row codes
+are a device gather.  Host work (O(distinct)): ppe_numerical in C++
 (bsb_ppe_numerical_host), literal resolution (scalar searchsorted) and the
 decode tables handed to the lookup kernels.
 
-Scope: numeric (integer) columns, i.e. the ordered kinds the north-star
-configs use.  Categorical / string dictionaries (ppe_categorical, prefix-free
-codes) are out of scope for the device path and raise ValueError.
+Categorical and ordered-string columns: strings do
+not live on the device, so their frequency tables, ranks and ppe_categorical
+codes (Alg. 2) are built on the host exactly as the reference does; the
+codes then go through the same device layouts, scans and lookups, and
+looked-up ranks are mapped back to strings on the host.  Prefix-free
+(PE-VBP) codes stay outside the device path and raise ValueError.
 """
 
 from __future__ import annotations
@@ -26,8 +29,8 @@ from .device import device, stream, to_dev_i64
 from .predicate import Op, Predicate, ResolvedPredicate
 
 __all__ = ["ColumnKind", "FrequencyTable", "build_frequency_table", "CodeAssignment",
-           "ppe_numerical", "fixed_assignment", "Dictionary", "compare_codes",
-           "freq_table_and_ranks"]
+           "ppe_numerical", "ppe_categorical", "fixed_assignment", "Dictionary",
+           "compare_codes", "freq_table_and_ranks"]
 
 MAX_CODE_BYTES = 8
 MAX_FIXED_BITS = 32
@@ -43,10 +46,32 @@ class ColumnKind(enum.Enum):
         return self is not ColumnKind.CATEGORICAL
 
 
-def _require_numeric(kind: ColumnKind):
-    if kind is not ColumnKind.NUMERIC:
-        raise ValueError(f"{kind.value} columns are outside the device path "
-                         "(numeric columns only; see DESIGN.md scope)")
+def _string_array(values) -> np.ndarray:
+    """dictionary.py:72-98 for the string kinds: str array, no NULL/empty."""
+    arr = np.asarray(values)
+    if arr.ndim != 1 or arr.size == 0:
+        raise ValueError("column must be a nonempty 1-d sequence")
+    if arr.dtype == object and any(v is None for v in arr):
+        raise ValueError("NULL value in column")
+    arr = arr.astype(str)
+    if (np.char.str_len(arr) == 0).any():
+        raise ValueError("NULL (empty) value in string column")
+    return arr
+
+
+def _host_table(arr: np.ndarray, kind: ColumnKind):
+    """dictionary.py:101-109 on the host: ordered kinds ascending; categorical
+    by descending count, ties by first appearance.  Also returns the rank of
+    every row."""
+    if kind.ordered:
+        uniq, inv, counts = np.unique(arr, return_inverse=True, return_counts=True)
+        return uniq, counts.astype(np.int64), inv.astype(np.int64)
+    uniq, first, inv, counts = np.unique(arr, return_index=True, return_inverse=True,
+                                         return_counts=True)
+    order = np.lexsort((first, -counts))
+    rank_of = np.empty(len(order), np.int64)
+    rank_of[order] = np.arange(len(order))
+    return uniq[order], counts[order].astype(np.int64), rank_of[inv]
 
 
 @dataclass(frozen=True)
@@ -107,10 +132,22 @@ def freq_table_and_ranks(values):
 
 
 def build_frequency_table(values, kind: ColumnKind) -> FrequencyTable:
-    """dictionary.py:101-109 for numeric columns (device radix sort)."""
-    _require_numeric(kind)
+    """dictionary.py:101-109: numeric columns by a device radix sort, string
+    kinds on the host."""
+    if kind is not ColumnKind.NUMERIC:
+        u, c, _ = _host_table(_string_array(values), kind)
+        return FrequencyTable(u, c, kind)
     u, c, _ = freq_table_and_ranks(values)
     return FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), kind)
+
+
+def table_and_ranks(values, kind: ColumnKind):
+    """(FrequencyTable, device int64 ranks) for any kind (ingest / advisor)."""
+    if kind is ColumnKind.NUMERIC:
+        u, c, r = freq_table_and_ranks(values)
+        return FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), kind), r
+    u, c, r = _host_table(_string_array(values), kind)
+    return FrequencyTable(u, c, kind), to_dev_i64(r)
 
 
 @dataclass(frozen=True)
@@ -148,6 +185,34 @@ def ppe_numerical(weights) -> CodeAssignment:
     _lib.check(_lib.load().bsb_ppe_numerical_host(w.ctypes.data, n, codes.ctypes.data,
                                                   lens.ctypes.data), "ppe_numerical")
     return CodeAssignment(codes, lens, "ppe_numerical")
+
+
+def ppe_categorical(n: int) -> CodeAssignment:
+    """Alg. 2 (dictionary.py:199-230): byte codes for n values ranked by
+    descending weight.  With depth B = ceil(log256(n+1)), depths 1..B-1 are
+    filled densely (255 slots under each of 256^(b-1) nodes, code = node << 8 |
+    slot); the remaining values are dealt round-robin over the 256^(B-1)
+    last-level nodes, slot by slot."""
+    if n <= 0:
+        raise ValueError("need at least one value")
+    depth, cap = 1, 255
+    while cap < n:  # smallest B with 256^B - 1 >= n
+        depth += 1
+        cap = (1 << (8 * depth)) - 1
+    codes, lens = [], []
+    placed = 0
+    for b in range(1, depth):
+        m = 255 * (1 << (8 * (b - 1)))
+        i = np.arange(m, dtype=np.uint64)
+        codes.append(((i // np.uint64(255)) << np.uint64(8)) + i % np.uint64(255) + np.uint64(1))
+        lens.append(np.full(m, b, np.uint8))
+        placed += m
+    rest = n - placed
+    nodes = np.uint64(1 << (8 * (depth - 1)))
+    i = np.arange(rest, dtype=np.uint64)
+    codes.append(((i % nodes) << np.uint64(8)) + i // nodes + np.uint64(1))
+    lens.append(np.full(rest, depth, np.uint8))
+    return CodeAssignment(np.concatenate(codes), np.concatenate(lens), "ppe_categorical")
 
 
 def fixed_assignment(n: int) -> CodeAssignment:
@@ -257,11 +322,12 @@ class Dictionary:
 
     @classmethod
     def build(cls, table: FrequencyTable, scheme: str) -> "Dictionary":
-        _require_numeric(table.kind)
+        """dictionary.py:328-344."""
         if scheme == "fixed":
             return cls(table, fixed_assignment(table.n))
         if scheme == "prefix_preserving":
-            a = ppe_numerical(table.weights)
+            a = (ppe_numerical(table.weights) if table.kind.ordered
+                 else ppe_categorical(table.n))
             if a.max_len > MAX_CODE_BYTES:
                 raise ValueError("code length overflow")
             return cls(table, a)
@@ -294,16 +360,28 @@ class Dictionary:
         return self.padded[order], order
 
     # device-side tables ------------------------------------------------
+    @property
+    def numeric(self) -> bool:
+        return self.table.kind is ColumnKind.NUMERIC
+
     @cached_property
     def dev_values(self) -> torch.Tensor:
+        """rank -> value on the device; for string kinds rank -> rank (the
+        lookups then return ranks, mapped to strings on the host)."""
+        if not self.numeric:
+            return torch.arange(self.n, dtype=torch.int64, device=device())
         return to_dev_i64(self.table.values)
+
+    @cached_property
+    def _rank_of_value(self) -> dict:
+        return {v: i for i, v in enumerate(self.table.values.tolist())}
 
     @cached_property
     def dev_decode(self):
         """(sorted padded codes, values in that order) for lookup decode."""
         srt, order = self._padded_order
-        return (torch.from_numpy(srt.view(np.int64)).to(device()),
-                to_dev_i64(self.table.values[order]))
+        vals = self.table.values[order] if self.numeric else order  # strings: ranks
+        return torch.from_numpy(srt.view(np.int64)).to(device()), to_dev_i64(vals)
 
     @cached_property
     def dev_codes(self):
@@ -352,6 +430,8 @@ class Dictionary:
 
     # row encoding / decoding -------------------------------------------
     def encode_rows_device(self, values) -> torch.Tensor:
+        if not self.numeric:
+            return to_dev_i64(self.encode_rows(values))
         v = _values_tensor(values)
         ranks = torch.empty_like(v)
         _lib.check(_lib.load().bsb_encode_rows(v.data_ptr(), v.numel(),
@@ -361,6 +441,20 @@ class Dictionary:
 
     def encode_rows(self, values) -> np.ndarray:
         """dictionary.py:381-397: ranks of raw values (KeyError if absent)."""
+        if not self.numeric:
+            arr = _string_array(values)
+            uniq, inv = np.unique(arr, return_inverse=True)
+            if self.kind.ordered:
+                pos = np.searchsorted(self.table.values, uniq)
+                if (pos >= self.n).any() or not (self.table.values[pos] == uniq).all():
+                    raise KeyError("value missing from dictionary")
+            else:
+                lut = self._rank_of_value
+                try:
+                    pos = np.fromiter((lut[v] for v in uniq.tolist()), np.int64, len(uniq))
+                except KeyError:
+                    raise KeyError("value missing from dictionary") from None
+            return pos[inv].astype(np.int64)
         try:
             return self.encode_rows_device(values).cpu().numpy()
         except KeyError:
@@ -395,7 +489,11 @@ class Dictionary:
         return self.table.values[np.asarray(ranks, dtype=np.int64)]
 
     # literal resolution (dictionary.py:418-485) -------------------------
-    def _literal_value(self, value) -> int:
+    def _literal_value(self, value):
+        if not self.numeric:
+            if not isinstance(value, str):
+                raise TypeError("string column needs a string literal")
+            return value
         if isinstance(value, bool) or not isinstance(value, (int, np.integer)):
             raise TypeError("numeric column needs an integer literal")
         return int(value)
@@ -408,10 +506,17 @@ class Dictionary:
         vals = self.table.values
         n = self.n
         if op in (Op.EQ, Op.NE):
-            i = int(np.searchsorted(vals, v))
-            if i < n and int(vals[i]) == v:
+            if self.kind.ordered:
+                i = int(np.searchsorted(vals, v))
+                found = i < n and vals[i] == v
+            else:
+                i = self._rank_of_value.get(v, -1)
+                found = i >= 0
+            if found:
                 return ResolvedPredicate.compare(op, *self._code_at(i))
             return ResolvedPredicate.constant(op is Op.NE)
+        if not self.kind.ordered:
+            raise ValueError("range predicate on a categorical column")
         if op in (Op.LT, Op.LE):
             cut = int(np.searchsorted(vals, v, side="left" if op is Op.LT else "right"))
             if cut == 0:

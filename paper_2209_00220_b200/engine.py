@@ -28,7 +28,7 @@ from .byteslice import (ByteSliceColumn, build_byteslice, byteslice_size_report,
                         lookup_byteslice_bits, lookup_byteslice_rows, scan_byteslice)
 from .datagen import PRNG_NAME
 from .device import device, stream
-from .dictionary import ColumnKind, Dictionary, FrequencyTable, freq_table_and_ranks
+from .dictionary import ColumnKind, Dictionary, FrequencyTable, table_and_ranks
 from .predicate import DEFAULT_LANES, LaneConfig, Op, Predicate, ResolvedPredicate
 from .vbs import (VbsColumn, build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs,
                   vbs_size_report)
@@ -153,12 +153,21 @@ def lookup_decode_bits(stored: StoredColumn, selection, out_dtype=torch.int64):
                                  out_dtype)
 
 
+def _to_values(stored: StoredColumn, dev: torch.Tensor) -> np.ndarray:
+    """Device lookup output -> host values: numeric values as they are; for
+    string kinds the device returned ranks (Dictionary.dev_values)."""
+    h = dev.cpu().numpy()
+    if stored.dictionary.numeric:
+        return h
+    return stored.dictionary.table.values[h]
+
+
 def lookup_decode(stored: StoredColumn, selection) -> np.ndarray:
     """engine.py:204-221: selected rows of one column, decoded to values."""
     sel = as_device_bits(selection)
     if sel.count() == 0:
         return stored.dictionary.table.values[:0]
-    return lookup_decode_bits(stored, sel).cpu().numpy()
+    return _to_values(stored, lookup_decode_bits(stored, sel))
 
 
 def size_report(stored: StoredColumn) -> dict:
@@ -253,7 +262,7 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
             timings.append({"column": name, "phase": "lookup", "op": "", "seconds": 0.0})
             continue
         t0 = time.perf_counter()
-        out[name] = lookup_decode_bits(st, selection, out_dtype).cpu().numpy()
+        out[name] = _to_values(st, lookup_decode_bits(st, selection, out_dtype))
         timings.append({"column": name, "phase": "lookup", "op": "",
                         "seconds": time.perf_counter() - t0})
     return QueryResult(n_sel, out, timings, selection)
@@ -291,9 +300,11 @@ def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "ad
             layout = advice.chosen
         _require_device_layout(layout)
         t0 = time.perf_counter()
-        u, c, ranks = freq_table_and_ranks(vals)
-        table = FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), spec.kind)
-        d = Dictionary.build(table, _SCHEME_FOR[layout])
+        try:
+            table, ranks = table_and_ranks(vals, spec.kind)
+            d = Dictionary.build(table, _SCHEME_FOR[layout])
+        except ValueError as exc:
+            raise DataError(f"column {spec.name!r}: {exc}") from None
         col = build_layout(layout, d, ranks, lanes)
         torch.cuda.current_stream().synchronize()
         encode_s = time.perf_counter() - t0

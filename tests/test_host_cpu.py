@@ -118,9 +118,15 @@ def test_decode_and_type_errors(lib):
         d.encode_literal(Predicate("c", Op.EQ, "x"))
     with pytest.raises(TypeError):
         d.encode_literal(Predicate("c", Op.EQ, True))
-    with pytest.raises(ValueError):
+    cat = Dictionary.build(FrequencyTable(np.array(["b", "a"]), np.array([2, 1]),
+                                          ColumnKind.CATEGORICAL), "prefix_preserving")
+    with pytest.raises(ValueError):  # range predicate on a categorical column
+        cat.encode_literal(Predicate("c", Op.LT, "b"))
+    with pytest.raises(TypeError):
+        cat.encode_literal(Predicate("c", Op.EQ, 3))
+    with pytest.raises(ValueError):  # PE-VBP codes are outside the device path
         Dictionary.build(FrequencyTable(np.array(["a"]), np.array([1]), ColumnKind.CATEGORICAL),
-                         "prefix_preserving")
+                         "prefix_free")
 
 
 def test_predicate_and_lane_validation():

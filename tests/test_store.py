@@ -111,3 +111,88 @@ def test_store_read_reference_file_scans_and_lookups(case, tmp_path):
             want = O.naive_filter(v, p.op.name, p.value, p.value_high)
             assert res.n_selected == int(want.sum()), (case, name, p)
             assert np.array_equal(res.columns[name], v[want]), (case, name, p)
+
+
+# ------------------------------------------------ categorical / ordered strings
+def _strings():
+    z = np.load(os.path.join(GOLD, "strings.npz"))
+    return z, json.loads(str(z["meta"]))
+
+
+_STR_KINDS = {"cat_a": "categorical", "cat_b": "categorical", "ostr": "ordered_string",
+              "num": "numeric"}
+
+
+def test_string_dictionaries_match_reference():
+    """ppe_categorical (Alg. 2), frequency tables (categorical: count desc,
+    first appearance) and literal resolution equal the reference's."""
+    from paper_2209_00220_b200.dictionary import (ColumnKind, Dictionary,
+                                                  build_frequency_table, ppe_categorical)
+    from paper_2209_00220_b200.predicate import Op, Predicate
+    z, meta = _strings()
+    for i, n in enumerate(meta["ppecat_sizes"]):
+        a = ppe_categorical(n)
+        assert np.array_equal(a.codes, z[f"ppecat/{i}/codes"]), n
+        assert np.array_equal(a.lengths, z[f"ppecat/{i}/lengths"]), n
+    for k in ("cat_a", "cat_b", "ostr"):
+        kind = ColumnKind(_STR_KINDS[k])
+        t = build_frequency_table(z[f"col/{k}"], kind)
+        assert np.array_equal(t.values.astype(str), z[f"table/{k}/values"])
+        assert np.array_equal(t.weights, z[f"table/{k}/weights"])
+        for scheme in ("fixed", "prefix_preserving"):
+            d = Dictionary.build(t, scheme)
+            for v, op, rop, code, length, triv in meta["literals"][f"{k}/{scheme}"]:
+                r = d.encode_literal(Predicate(k, Op[op], v))
+                assert [r.op.name if r.op else None, r.code, r.length, r.trivial] == \
+                    [rop, code, length, triv], (k, scheme, v, op)
+        # the host dictionary sections of the reference's store files
+        for case in meta["cases"]:
+            secs = _sections(open(os.path.join(GOLD, f"strings_{case}.byst"), "rb").read())
+            e = {c["name"]: c for c in json.loads(secs["manifest"])["columns"]}[k]
+            from paper_2209_00220_b200.store import _dict_payload
+            assert _dict_payload(Dictionary.build(t, e["scheme"])) == secs[f"col:{k}:dict"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["forced", "advised"])
+def test_string_store_and_queries_match_reference(case, tmp_path):
+    """ingest_arrays of string + numeric columns writes the reference's store
+    bytes (advisor included); reading the reference's file and running the
+    reference's queries gives its selections and projected values."""
+    import paper_2209_00220_b200 as B
+    from paper_2209_00220_b200 import engine as E
+    from paper_2209_00220_b200.predicate import Op, Predicate
+    from paper_2209_00220_b200.store import read_store, store_bytes
+    z, meta = _strings()
+    m = meta["cases"][case]
+    names = list(_STR_KINDS)
+    cols = {k: z[f"col/{k}"] for k in names}
+    schema = E.Schema([E.ColumnSpec(k, B.ColumnKind(_STR_KINDS[k]), m["layouts"][k])
+                       for k in names])
+    store, _ = E.ingest_arrays(cols, schema, policy=m["policy"], advise_cost="bytes",
+                               advise_count=m["advise_count"])
+    want = open(os.path.join(GOLD, f"strings_{case}.byst"), "rb").read()
+    gs, ws = _sections(store_bytes(store)), _sections(want)
+    for k in ws:
+        assert gs[k] == ws[k], k
+    loaded = read_store(os.path.join(GOLD, f"strings_{case}.byst"))
+    ca, so = cols["cat_a"], np.sort(cols["ostr"])
+    u, c = np.unique(ca, return_counts=True)
+    top, rare = str(u[np.argmax(c)]), str(u[np.argmin(c)])
+    queries = [
+        [[Predicate("cat_a", Op.EQ, top)]],
+        [[Predicate("cat_a", Op.NE, rare), Predicate("cat_b", Op.EQ, str(cols["cat_b"][7]))]],
+        [[Predicate("cat_a", Op.EQ, "absent")], [Predicate("cat_b", Op.NE, "absent")]],
+        [[Predicate("ostr", Op.BETWEEN, str(so[300]), str(so[1500]))]],
+        [[Predicate("ostr", Op.LT, "s00005"), Predicate("num", Op.GE, 0)]],
+        [[Predicate("ostr", Op.GE, "s00100"), Predicate("cat_b", Op.EQ, str(cols["cat_b"][3]))]],
+    ]
+    for st in (store, loaded):
+        for qi, groups in enumerate(queries):
+            res = E.execute(st, E.Query(groups, ["cat_a", "ostr", "num"]))
+            assert res.n_selected == m["n_selected"][qi], (case, qi)
+            assert np.array_equal(res.selection.to_bools(), z[f"q/{case}/{qi}/sel"])
+            for c in ("cat_a", "ostr"):
+                assert np.array_equal(np.asarray(res.columns[c]).astype(str),
+                                      z[f"q/{case}/{qi}/{c}"]), (case, qi, c)
+            assert np.array_equal(res.columns["num"], z[f"q/{case}/{qi}/num"])
