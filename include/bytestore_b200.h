@@ -311,6 +311,66 @@ int bsb_zipf_from_uniform(const double* u, int64_t n, const double* cdf, int64_t
 void bsb_stats_layout(int32_t* words_off, int32_t* bytes_off, int32_t* total_off,
                       int32_t* skipped_off, int32_t* levels_off);
 
+/* ------------------------------------------- baseline layouts (§8(f) row 4) */
+/* Bit-Packed (bitpacked.py:1-150): code i in stream bits [i*w, (i+1)*w), most
+ * significant bit first, bytes in stream order; stored as uint32 words whose
+ * memory bytes ARE the reference stream (`bits`), zero padded to whole
+ * 32-row groups plus two words.  w in 1..32. */
+typedef struct bsb_bitpacked {
+  int64_t n_rows;
+  int32_t width_bits;
+  int32_t reserved;
+  const uint32_t* words;
+} bsb_bitpacked;
+/* words to allocate for n rows of width w (-1 on bad arguments) */
+int64_t bsb_bitpacked_words_for(int64_t n_rows, int32_t width_bits);
+/* build_bitpacked (bitpacked.py:36-52); a code >= 2^w -> BSB_ERANGE (syncs) */
+int bsb_bitpacked_build(const int64_t* codes, int64_t n, int32_t width_bits, uint32_t* words,
+                        void* stream);
+/* scan_bitpacked (bitpacked.py:94-118): unpack + compare every code, input
+ * mask post-AND-ed, no early stop, no ScanStats.  BETWEEN = code..code2. */
+int bsb_bitpacked_scan(const bsb_bitpacked* col, const bsb_pred* pred, const uint32_t* mask,
+                       uint32_t* out_words, uint64_t* count, void* stream);
+/* lookup_bitpacked (bitpacked.py:127-143) of the set rows of `words`, in
+ * ascending row order; decoder kind 0 (codes) or 1 (values[code]).  With
+ * n_out_dev the row count lands there; out_* need capacity popcount. */
+int bsb_bitpacked_lookup_bits(const bsb_bitpacked* col, const uint32_t* words,
+                              const bsb_decode* dec, uint64_t* out_codes, int64_t* out_values,
+                              int32_t* out_values32, uint64_t* n_out_dev, void* stream);
+
+/* VBP / PE-VBP (vbp.py:1-212): plane j (0 = most significant) holds one
+ * uint32 per 32-row block, planes[j * n_words + b]; kind PADDED stores
+ * prefix-free codes zero-padded to w_max bits and aligns literals the same
+ * way (code << (w_max - length), length in bits). */
+#define BSB_VBP_PLAIN 0
+#define BSB_VBP_PADDED 1
+#define BSB_VBP_MAX_PLANES 32
+#define BSB_VBP_STATS_WORDS 66
+typedef struct bsb_vbp {
+  int64_t n_rows;
+  int32_t w_max;
+  int32_t kind;
+  const uint32_t* planes;
+} bsb_vbp;
+/* build_vbp (vbp.py:51-71): codes (already padded for PE-VBP) -> planes
+ * (w_max * ceil(n/32) words); a code >= 2^w_max -> BSB_ERANGE (syncs). */
+int bsb_vbp_build(const uint64_t* codes, int64_t n, int32_t w_max, uint32_t* planes,
+                  void* stream);
+/* scan_vbp (vbp.py:144-194): bit-serial, early stop per block; BETWEEN fused
+ * (leg 2 sees leg 1's result as its mask).  stats (int64[BSB_VBP_STATS_WORDS],
+ * may be NULL): [0..31] blocks loaded per plane (summed over legs; bytes =
+ * 4 x), [64] blocks skipped by leg 1, [65] by leg 2; depth (int8 per block,
+ * may be NULL) = max over legs -- the reference's merged ScanStats. */
+int bsb_vbp_scan(const bsb_vbp* col, const bsb_pred* pred, const uint32_t* mask,
+                 uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                 void* stream);
+/* lookup_vbp (vbp.py:197-212) of the set rows of `words`, ascending row
+ * order: padded codes, or values through decoder kind 1 (ranks) / 2 (sorted
+ * padded codes, PE-VBP). */
+int bsb_vbp_lookup_bits(const bsb_vbp* col, const uint32_t* words, const bsb_decode* dec,
+                        uint64_t* out_codes, int64_t* out_values, int32_t* out_values32,
+                        uint64_t* n_out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,11 @@ _LAZY = {
     "lookup_vbs_rows": "vbs", "lookup_vbs_rows_dec": "vbs", "lookup_vbs_bits": "vbs",
     "vbs_size_report": "vbs",
     "write_store": "store", "read_store": "store", "store_bytes": "store",
+    "BitPackedColumn": "bitpacked", "build_bitpacked": "bitpacked",
+    "scan_bitpacked": "bitpacked", "lookup_bitpacked": "bitpacked",
+    "bitpacked_size_report": "bitpacked", "VbpColumn": "vbp", "build_vbp": "vbp",
+    "pad_codes": "vbp", "scan_vbp": "vbp", "lookup_vbp": "vbp", "vbp_size_report": "vbp",
+    "ppe_categorical": "dictionary", "prefix_free_assignment": "dictionary",
     "ColumnKind": "dictionary", "FrequencyTable": "dictionary", "CodeAssignment": "dictionary",
     "Dictionary": "dictionary", "build_frequency_table": "dictionary",
     "ppe_numerical": "dictionary", "fixed_assignment": "dictionary",

@@ -26,6 +26,8 @@ OK, EINVAL, ERANGE, ENOTFOUND, ECUDA, EKEY = 0, 1, 2, 3, 4, 5
 OP_CODES = {"EQ": 0, "NE": 1, "LT": 2, "LE": 3, "GT": 4, "GE": 5, "BETWEEN": 6}
 LAYOUT_BYTESLICE, LAYOUT_PPVBS = 0, 1
 DEEP_PACKED, DEEP_RANK2, DEEP_PLANES, DEEP_SLICED = 0, 1, 2, 3
+VBP_PLAIN, VBP_PADDED = 0, 1
+VBP_MAX_PLANES, VBP_STATS_WORDS = 32, 66
 
 
 class BsbPred(ctypes.Structure):
@@ -49,6 +51,16 @@ class BsbDecode(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("reserved", c_int32), ("values", c_void_p),
                 ("sorted_padded", c_void_p), ("n_dict", c_int64), ("e1", c_void_p),
                 ("e2", c_void_p)]
+
+
+class BsbBitPacked(ctypes.Structure):
+    _fields_ = [("n_rows", c_int64), ("width_bits", c_int32), ("reserved", c_int32),
+                ("words", c_void_p)]
+
+
+class BsbVbp(ctypes.Structure):
+    _fields_ = [("n_rows", c_int64), ("w_max", c_int32), ("kind", c_int32),
+                ("planes", c_void_p)]
 
 
 class BsbColumnRef(ctypes.Structure):
@@ -93,6 +105,15 @@ _SIGS = {
     "bsb_gather_codes": (c_int32, [_P, c_int64, _P, _P, _P, _P, _P]),
     "bsb_zipf_from_uniform": (c_int32, [_P, c_int64, _P, c_int64, _P, _P]),
     "bsb_stats_layout": (None, [POINTER(c_int32)] * 5),
+    "bsb_bitpacked_words_for": (c_int64, [c_int64, c_int32]),
+    "bsb_bitpacked_build": (c_int32, [_P, c_int64, c_int32, _P, _P]),
+    "bsb_bitpacked_scan": (c_int32, [POINTER(BsbBitPacked), POINTER(BsbPred), _P, _P, _P, _P]),
+    "bsb_bitpacked_lookup_bits": (c_int32, [POINTER(BsbBitPacked), _P, POINTER(BsbDecode), _P,
+                                            _P, _P, _P, _P]),
+    "bsb_vbp_build": (c_int32, [_P, c_int64, c_int32, _P, _P]),
+    "bsb_vbp_scan": (c_int32, [POINTER(BsbVbp), POINTER(BsbPred), _P, _P, _P, _P, _P, _P]),
+    "bsb_vbp_lookup_bits": (c_int32, [POINTER(BsbVbp), _P, POINTER(BsbDecode), _P, _P, _P, _P,
+                                      _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -29,7 +29,8 @@ from .device import device, stream, to_dev_i64
 from .predicate import Op, Predicate, ResolvedPredicate
 
 __all__ = ["ColumnKind", "FrequencyTable", "build_frequency_table", "CodeAssignment",
-           "ppe_numerical", "ppe_categorical", "fixed_assignment", "Dictionary",
+           "ppe_numerical", "ppe_categorical", "fixed_assignment", "prefix_free_assignment",
+           "Dictionary",
            "compare_codes", "freq_table_and_ranks"]
 
 MAX_CODE_BYTES = 8
@@ -215,6 +216,46 @@ def ppe_categorical(n: int) -> CodeAssignment:
     return CodeAssignment(np.concatenate(codes), np.concatenate(lens), "ppe_categorical")
 
 
+def prefix_free_assignment(weights) -> CodeAssignment:
+    """Order-preserving prefix-free bit codes by weighted bisection
+    (dictionary.py:245-290; PE-VBP baseline layout).  A value range [s, e)
+    splits at the cut k whose heavier side is lightest (the float64 prefix
+    sum's midpoint, then k-1 / k+1 tried), clamped so no code exceeds
+    ceil(log2 n) + 4 bits; the left part appends bit 0, the right bit 1."""
+    w = np.asarray(weights, dtype=np.float64)
+    n = len(w)
+    if n == 0:
+        raise ValueError("empty weight table")
+    codes = np.zeros(n, np.uint64)
+    nbits = np.zeros(n, np.uint8)
+    if n == 1:
+        nbits[0] = 1
+        return CodeAssignment(codes, nbits, "prefix_free", width_bits=1)
+    limit = (n - 1).bit_length() + 4
+    pre = np.concatenate(([0.0], np.cumsum(w)))
+    todo = [(0, n, 0, 0)]
+    while todo:
+        s, e, code, depth = todo.pop()
+        if e - s == 1:
+            codes[s], nbits[s] = code, depth
+            continue
+        reach = 1 << (limit - depth - 1)  # leaves a subtree of this depth may hold
+        lo, hi = max(s + 1, e - reach), min(e - 1, s + reach)
+        k = int(np.searchsorted(pre, (pre[s] + pre[e]) / 2.0, side="left"))
+        k = min(max(k, lo), hi)
+
+        def heavier(c):
+            return max(pre[c] - pre[s], pre[e] - pre[c])
+
+        best = k
+        for c in (k - 1, k + 1):
+            if lo <= c <= hi and heavier(c) < heavier(best):
+                best = c
+        todo.append((best, e, (code << 1) | 1, depth + 1))
+        todo.append((s, best, code << 1, depth + 1))
+    return CodeAssignment(codes, nbits, "prefix_free", width_bits=int(nbits.max()))
+
+
 def fixed_assignment(n: int) -> CodeAssignment:
     """Rank codes at w = max(1, ceil(log2 n)) bits (dictionary.py:233-242)."""
     if n <= 0:
@@ -332,7 +373,7 @@ class Dictionary:
                 raise ValueError("code length overflow")
             return cls(table, a)
         if scheme == "prefix_free":
-            raise ValueError("prefix_free (PE-VBP) dictionaries are outside the device path")
+            return cls(table, prefix_free_assignment(table.weights))
         raise ValueError(f"unknown scheme {scheme!r}")
 
     @property
@@ -349,9 +390,14 @@ class Dictionary:
 
     @cached_property
     def padded(self) -> np.ndarray:
-        """code << 8*(K - len) (dictionary.py:360-368)."""
+        """Codes with the padding zeros in the low bits (dictionary.py:360-368):
+        code << 8*(K - len) for byte codes, code << (w_max - len) for
+        prefix-free bit codes."""
         a = self.assignment
-        shift = np.uint64(8) * (np.uint64(a.max_len) - a.lengths.astype(np.uint64))
+        if a.bit_granular:
+            shift = np.uint64(a.width_bits) - a.lengths.astype(np.uint64)
+        else:
+            shift = np.uint64(8) * (np.uint64(a.max_len) - a.lengths.astype(np.uint64))
         return a.codes << shift
 
     @cached_property
@@ -401,7 +447,8 @@ class Dictionary:
             dec.kind = 1
             dec.values = keep["values"].data_ptr()
         else:
-            tree = ppe_decode_tree(self.assignment.codes, self.assignment.lengths)
+            tree = (None if self.assignment.bit_granular else
+                    ppe_decode_tree(self.assignment.codes, self.assignment.lengths))
             if tree is not None:
                 dev = device()
                 for k, v in tree.items():

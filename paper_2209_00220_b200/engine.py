@@ -7,7 +7,8 @@ blocks already ruled out load nothing from later columns), ORs disjunction
 arms on the device and gathers + decodes each projected column straight from
 the selection bitvector with the fused lookup kernels.
 
-In scope: "byteslice" and "ppvbs" numeric columns.  CSV ingest (file I/O)
+All five reference layouts run on the device: "byteslice" and "ppvbs" (the
+north-star path) plus the paper's baselines "bitpacked", "vbp" and "pevbp".  CSV ingest (file I/O)
 is replaced by ``ingest_arrays`` over in-memory columns; the baseline
 layouts (bitpacked, vbp, pevbp) are out of scope.
 """
@@ -23,6 +24,8 @@ import torch
 
 from . import _lib
 from .advisor import ColumnAdvice, advise_column
+from .bitpacked import (build_bitpacked, bitpacked_size_report, lookup_bitpacked_bits,
+                        scan_bitpacked)
 from .bitvector import DeviceBitVector, ResultBitVector, as_device_bits
 from .byteslice import (ByteSliceColumn, build_byteslice, byteslice_size_report,
                         lookup_byteslice_bits, lookup_byteslice_rows, scan_byteslice)
@@ -30,6 +33,7 @@ from .datagen import PRNG_NAME
 from .device import device, stream
 from .dictionary import ColumnKind, Dictionary, FrequencyTable, table_and_ranks
 from .predicate import DEFAULT_LANES, LaneConfig, Op, Predicate, ResolvedPredicate
+from .vbp import build_vbp, lookup_vbp_bits, pad_codes, scan_vbp, vbp_size_report
 from .vbs import (VbsColumn, build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs,
                   vbs_size_report)
 
@@ -39,10 +43,12 @@ __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Qu
            "conj_scan"]
 
 LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
-DEVICE_LAYOUTS = ("byteslice", "ppvbs")
+DEVICE_LAYOUTS = LAYOUTS
+_CONJ_LAYOUTS = ("byteslice", "ppvbs")  # layouts bsb_conj_scan chains natively
 FORMAT_VERSION = 1
 
-_SCHEME_FOR = {"byteslice": "fixed", "ppvbs": "prefix_preserving"}
+_SCHEME_FOR = {"bitpacked": "fixed", "byteslice": "fixed", "vbp": "fixed",
+               "pevbp": "prefix_free", "ppvbs": "prefix_preserving"}
 
 
 class DataError(Exception):
@@ -110,28 +116,39 @@ class Store:
 
 def _require_device_layout(layout: str):
     if layout not in DEVICE_LAYOUTS:
-        if layout in LAYOUTS:
-            raise ValueError(f"layout {layout!r} is outside the device path "
-                             "(baseline layouts are out of scope; see DESIGN.md)")
         raise ValueError(f"unknown layout {layout!r}")
 
 
 def build_layout(layout: str, dictionary: Dictionary, ranks, lanes: LaneConfig = DEFAULT_LANES):
-    """engine.py:172-188 for the device layouts."""
+    """engine.py:172-188."""
     _require_device_layout(layout)
+    a = dictionary.assignment
     if layout == "ppvbs":
         codes, lens = dictionary.row_codes_device(ranks)
         return build_vbs(codes, lens, lanes)
     r = ranks if isinstance(ranks, torch.Tensor) else np.asarray(ranks, dtype=np.int64)
-    return build_byteslice(r, dictionary.assignment.width_bits, lanes)
+    if layout == "byteslice":
+        return build_byteslice(r, a.width_bits, lanes)
+    lanes.require_device()
+    if layout == "bitpacked":
+        return build_bitpacked(r, a.width_bits)
+    if layout == "vbp":
+        return build_vbp(r, a.width_bits, "plain")
+    rh = r.cpu().numpy() if isinstance(r, torch.Tensor) else r   # pevbp
+    codes, lens = dictionary.row_codes(rh)
+    return build_vbp(pad_codes(codes, lens, a.width_bits), a.width_bits, "padded_encoding")
 
 
 def scan_layout(layout: str, column, pred, mask=None, threads: int = 1):
-    """engine.py:191-201."""
+    """engine.py:191-201: (bitvector, ScanStats or None for bitpacked)."""
     _require_device_layout(layout)
     if layout == "byteslice":
         return scan_byteslice(column, pred, mask, threads)
-    return scan_vbs(column, pred, mask, threads)
+    if layout == "ppvbs":
+        return scan_vbs(column, pred, mask, threads)
+    if layout == "bitpacked":
+        return scan_bitpacked(column, pred, mask, threads), None
+    return scan_vbp(column, pred, mask, threads)
 
 
 def lookup_decode_rows(stored: StoredColumn, rows: torch.Tensor, out_dtype=torch.int64):
@@ -139,18 +156,22 @@ def lookup_decode_rows(stored: StoredColumn, rows: torch.Tensor, out_dtype=torch
     if stored.layout == "ppvbs":
         return lookup_vbs_rows_dec(stored.column, rows, stored.dictionary.dev_decoder,
                                    out_dtype)
-    _require_device_layout(stored.layout)
+    if stored.layout != "byteslice":
+        raise ValueError(f"row-id lookups are not provided for layout {stored.layout!r}")
     return lookup_byteslice_rows(stored.column, rows, stored.dictionary.dev_values, out_dtype)
 
 
 def lookup_decode_bits(stored: StoredColumn, selection, out_dtype=torch.int64):
     """Fused selection -> decoded values on the device (ascending rows)."""
+    dec = stored.dictionary.dev_decoder
     if stored.layout == "ppvbs":
-        return lookup_vbs_bits(stored.column, selection, stored.dictionary.dev_decoder,
-                               out_dtype)
+        return lookup_vbs_bits(stored.column, selection, dec, out_dtype)
+    if stored.layout == "byteslice":
+        return lookup_byteslice_bits(stored.column, selection, dec, out_dtype)
+    if stored.layout == "bitpacked":
+        return lookup_bitpacked_bits(stored.column, selection, dec, out_dtype)
     _require_device_layout(stored.layout)
-    return lookup_byteslice_bits(stored.column, selection, stored.dictionary.dev_decoder,
-                                 out_dtype)
+    return lookup_vbp_bits(stored.column, selection, dec, out_dtype)
 
 
 def _to_values(stored: StoredColumn, dev: torch.Tensor) -> np.ndarray:
@@ -171,6 +192,10 @@ def lookup_decode(stored: StoredColumn, selection) -> np.ndarray:
 
 
 def size_report(stored: StoredColumn) -> dict:
+    if stored.layout == "bitpacked":
+        return bitpacked_size_report(stored.column)
+    if stored.layout in ("vbp", "pevbp"):
+        return vbp_size_report(stored.column)
     if stored.layout == "ppvbs":
         return vbs_size_report(stored.column)
     return byteslice_size_report(stored.column)
@@ -193,6 +218,11 @@ def conj_scan(columns, preds, mask=None) -> DeviceBitVector:
             raise ValueError("columns differ in row count")
     running = None if mask is None else as_device_bits(mask)
     if not columns:
+        return running
+    if any(layout not in _CONJ_LAYOUTS for layout, _ in columns):
+        # baseline layouts: the same pipelined semantics, one scan call each
+        for (layout, col), p in zip(columns, preds):
+            running = as_device_bits(scan_layout(layout, col, p, running)[0])
         return running
     for c0 in range(0, len(columns), _lib.MAX_CONJ):
         chunk = list(zip(columns, preds))[c0:c0 + _lib.MAX_CONJ]

@@ -124,9 +124,9 @@ def test_decode_and_type_errors(lib):
         cat.encode_literal(Predicate("c", Op.LT, "b"))
     with pytest.raises(TypeError):
         cat.encode_literal(Predicate("c", Op.EQ, 3))
-    with pytest.raises(ValueError):  # PE-VBP codes are outside the device path
+    with pytest.raises(ValueError):
         Dictionary.build(FrequencyTable(np.array(["a"]), np.array([1]), ColumnKind.CATEGORICAL),
-                         "prefix_free")
+                         "unknown_scheme")
 
 
 def test_predicate_and_lane_validation():
