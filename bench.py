@@ -452,7 +452,7 @@ def measure_extra_configs(data) -> dict:
     import bench_cfgs
     out = {}
     for name, fn in (("cfg1", bench_cfgs.measure_cfg1), ("cfg4", bench_cfgs.measure_cfg4),
-                     ("cfg5", bench_cfgs.measure_cfg5)):
+                     ("cfg5", bench_cfgs.measure_cfg5), ("layout_sweep", bench_cfgs.measure_sweep)):
         torch.cuda.empty_cache()
         t0 = time.perf_counter()
         try:

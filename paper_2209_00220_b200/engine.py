@@ -39,8 +39,8 @@ from .vbs import (VbsColumn, build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, sc
 
 __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
            "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",
-           "lookup_decode", "lookup_decode_rows", "lookup_decode_bits", "execute", "ingest_arrays", "size_report",
-           "conj_scan"]
+           "lookup_decode", "lookup_decode_rows", "lookup_decode_bits", "execute", "ingest_arrays",
+           "ingest", "read_csv_columns", "IngestReport", "size_report", "conj_scan"]
 
 LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
 DEVICE_LAYOUTS = LAYOUTS
@@ -74,6 +74,22 @@ class Schema:
         names = [c.name for c in self.columns]
         if len(set(names)) != len(names):
             raise ValueError("duplicate column names in schema")
+
+    @staticmethod
+    def parse_kind(text: str) -> ColumnKind:
+        """engine.py:44-50, 79-84 (incl. the semi_categorical_string alias)."""
+        kinds = {"numeric": ColumnKind.NUMERIC, "categorical": ColumnKind.CATEGORICAL,
+                 "ordered_string": ColumnKind.ORDERED_STRING,
+                 "semi_categorical_string": ColumnKind.ORDERED_STRING}
+        if text not in kinds:
+            raise ValueError(f"unknown column kind {text!r}")
+        return kinds[text]
+
+
+@dataclass
+class IngestReport:
+    rows: list = field(default_factory=list)    # per-column timing dicts
+    advice: dict = field(default_factory=dict)  # name -> ColumnAdvice
 
 
 @dataclass
@@ -298,21 +314,86 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
     return QueryResult(n_sel, out, timings, selection)
 
 
+def read_csv_columns(path, schema: Schema) -> dict:
+    """engine.py:114-158: the schema's columns from a header-bearing CSV.
+    Numeric cells must be integers; an empty cell is a NULL and rejected;
+    errors name the 1-based line and the column (DataError)."""
+    import csv
+    with open(path, newline="") as fh:
+        rows = csv.reader(fh)
+        header = next(rows, None)
+        if header is None:
+            raise DataError(f"{path}: empty CSV, header row required")
+        where = {}
+        for spec in schema.columns:
+            if spec.name not in header:
+                raise DataError(f"{path}: column {spec.name!r} missing from header")
+            where[spec.name] = header.index(spec.name)
+        cells = {spec.name: [] for spec in schema.columns}
+        for line, row in enumerate(rows, start=2):
+            if len(row) != len(header):
+                raise DataError(f"{path}:{line}: expected {len(header)} cells, got {len(row)}")
+            for name, col in where.items():
+                if row[col] == "":
+                    raise DataError(f"{path}:{line}: NULL in column {name!r}")
+                cells[name].append(row[col])
+    if not cells or not next(iter(cells.values())):
+        raise DataError(f"{path}: no data rows")
+    out = {}
+    for spec in schema.columns:
+        raw = cells[spec.name]
+        if spec.kind is not ColumnKind.NUMERIC:
+            out[spec.name] = np.array(raw, dtype=object)
+            continue
+        vals = np.empty(len(raw), np.int64)
+        for i, c in enumerate(raw):
+            try:
+                vals[i] = int(c)
+            except ValueError:
+                raise DataError(f"{path}:{i + 2}: non-integer value {c!r} in numeric "
+                                f"column {spec.name!r}") from None
+        out[spec.name] = vals
+    return out
+
+
+def ingest(csv_path, schema: Schema, policy: str = "advisor", *, advise_cost="wall",
+           advise_count: int = 100, subsample: int | None = None,
+           lanes: LaneConfig = DEFAULT_LANES, threads: int = 1,
+           extra_manifest: dict | None = None):
+    """engine.py:239-297: CSV -> (Store, IngestReport); `threads` is accepted
+    for signature compatibility (CPU partitioning only in the reference)."""
+    data = read_csv_columns(csv_path, schema)
+    store, rows, advice = _ingest(data, schema, policy, advise_cost, advise_count, subsample,
+                                  lanes)
+    if extra_manifest:
+        store.manifest.update(extra_manifest)
+    return store, IngestReport(rows, advice)
+
+
 def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "advisor", *,
                   advise_cost="wall", advise_count: int = 100, subsample: int | None = None,
                   lanes: LaneConfig = DEFAULT_LANES):
+    """In-memory columns {name: values} (numpy / torch / lists) -> (Store,
+    per-column report rows), the ingest path without the CSV reader."""
+    store, rows, _ = _ingest(columns, schema, policy, advise_cost, advise_count, subsample,
+                             lanes)
+    return store, rows
+
+
+def _ingest(columns: dict, schema: Schema | None, policy: str, advise_cost, advise_count: int,
+            subsample: int | None, lanes: LaneConfig):
     """engine.py:239-297 over in-memory columns {name: values} (no CSV I/O).
 
     Per column: advise (unless the schema forces a layout), build the
     frequency table + ranks in one device sort, assign codes, build the
-    device layout.  Returns (Store, report rows).
+    device layout.  Returns (Store, report rows, {name: ColumnAdvice}).
     """
     if policy not in ("advisor", "forced"):
         raise ValueError(f"unknown layout policy {policy!r}")
     specs = schema.columns if schema is not None else [
         ColumnSpec(k, ColumnKind.NUMERIC) for k in columns]
     n_rows = None
-    stored, entries, report = {}, [], []
+    stored, entries, report, advised = {}, [], [], {}
     for spec in specs:
         vals = columns[spec.name]
         n = vals.numel() if isinstance(vals, torch.Tensor) else len(vals)
@@ -328,6 +409,7 @@ def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "ad
                                    cost=advise_cost, subsample=subsample, lanes=lanes)
             advise_s = time.perf_counter() - t0
             layout = advice.chosen
+            advised[spec.name] = advice
         _require_device_layout(layout)
         t0 = time.perf_counter()
         try:
@@ -350,4 +432,4 @@ def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "ad
                        "encode_s": encode_s, "advise_s": advise_s})
     manifest = {"format_version": FORMAT_VERSION, "n_rows": n_rows, "prng": PRNG_NAME,
                 "lane_count": lanes.lane_count, "columns": entries}
-    return Store(manifest, stored), report
+    return Store(manifest, stored), report, advised
