@@ -23,7 +23,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "ShardResult", "exchange_counts", "sharded_scan",
-           "global_row_ids", "merge_frequency_tables", "gather_row_ids"]
+           "global_row_ids", "merge_frequency_tables", "gather_row_ids", "global_sum"]
 
 TILE_ROWS = 1024
 
@@ -128,3 +128,13 @@ def merge_frequency_tables(values: torch.Tensor, counts: torch.Tensor, group=Non
     tot = torch.zeros(uniq.numel(), dtype=torch.int64, device=values.device)
     tot.scatter_add_(0, inv, allc)
     return uniq, tot
+
+
+def global_sum(local_sum: torch.Tensor, group=None) -> torch.Tensor:
+    """a projected column's SUM over all shards -- each rank's
+    local int64 sum, then one all_reduce (in place, on the collective's
+    device)."""
+    out = local_sum.reshape(1).to(torch.int64).clone()
+    dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+

@@ -58,11 +58,13 @@ def _worker(rank, world, port, q):
         res = S.sharded_scan(local_scan, N_TOTAL)
         ids = S.global_row_ids(res)
         all_ids = S.gather_row_ids(res, ids)
+        flags = O.words_to_bools(res.local_bits, r1 - r0)
+        tot = S.global_sum(torch.tensor([int(local[flags].sum())]))
         words = torch.from_numpy(res.local_bits.view(np.int32).copy())
         sizes = [None] * world
         dist.all_gather_object(sizes, (res.r0, res.r1, words.numpy().tolist()))
         q.put((rank, res.global_count, res.offset, res.counts, all_ids.numpy().tolist(),
-               sizes, gu.tolist() == np.unique(vals).tolist()))
+               sizes, gu.tolist() == np.unique(vals).tolist(), int(tot.item())))
     finally:
         dist.destroy_process_group()
 
@@ -91,8 +93,9 @@ def test_sharded_scan_matches_unsharded(world):
     words = np.concatenate([np.array(w, np.int32).view(np.uint32) for _, _, w in shards])
     assert np.array_equal(words, want)                 # bit-exact concatenation
     off = 0
-    for rank, total, offset, counts, ids, _, dict_ok in out:
+    for rank, total, offset, counts, ids, _, dict_ok, vsum in out:
         assert dict_ok                                 # merged dictionary == global table
+        assert vsum == int(vals[want_rows].sum())      # SUM: local sums + one all_reduce
         assert total == len(want_rows) == sum(counts)
         assert offset == off
         off += counts[rank]
