@@ -312,15 +312,32 @@ def run_b200(args):
     cnt_buf = torch.zeros(len(scans), dtype=torch.int64, device="cuda")
     gather = [torch.zeros_like(cnt_buf) for _ in range(world)] if world > 1 else None
 
+    # the timed step calls the C ABI directly (the drop-in boundary) with
+    # preallocated result words and count slots: no per-scan allocation and
+    # no extra copy kernels between the scans
+    import ctypes
+
+    from paper_2209_00220_b200.device import stream as cur_stream
+    lib = _lib.load()
+    nwords = -(-n // 32)
+    outs = [torch.empty(nwords, dtype=torch.int32, device="cuda") for _ in scans]
+    cpreds = [pred.to_c() for (_l, _p, _c, pred, _a, _s) in scans]
+    sptr = cur_stream()
+    calls = []
+    for i, (layout, p, col, pred, _, _) in enumerate(scans):
+        fn = lib.bsb_vbs_scan if layout == "ppvbs" else lib.bsb_byteslice_scan
+        calls.append((fn, col.desc_ref, ctypes.byref(cpreds[i]), outs[i].data_ptr(),
+                      cnt_buf.data_ptr() + 8 * i))
+
     def step(events=None):
-        for i, (layout, p, col, pred, _, _) in enumerate(scans):
-            fn = scan_vbs if layout == "ppvbs" else scan_byteslice
+        for i, (fn, desc, cp, optr, cptr) in enumerate(calls):
             if events is not None:
                 events[i][0].record(stream)
-            bv, _ = fn(col, pred)
+            rc = fn(desc, cp, None, optr, cptr, None, None, sptr)
             if events is not None:
                 events[i][1].record(stream)
-            cnt_buf[i:i + 1].copy_(bv._count, non_blocking=True)
+            if rc:
+                _lib.check(rc, "scan")
         if world > 1:
             dist.all_gather(gather, cnt_buf)
 
@@ -352,9 +369,7 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    for k in range(args.steps):  # counts still equal the untimed check
-        pass
-    got = cnt_buf.cpu().tolist()
+    got = cnt_buf.cpu().tolist()  # counts of the last step equal the untimed check
     for i, (layout, p, *_r) in enumerate(scans):
         assert got[i] == counts_ref[p], (layout, p, got[i], counts_ref[p])
 
