@@ -36,6 +36,7 @@ _LAZY = {
     "ppe_numerical": "dictionary", "fixed_assignment": "dictionary",
     "compare_codes": "dictionary",
     "ZipfSpec": "datagen", "gen_zipf": "datagen", "zipf_pmf": "datagen",
+    "gen_zipf_device": "datagen",
     "ProfilePoint": "advisor", "ColumnAdvice": "advisor", "advise": "advisor",
     "advise_column": "advisor", "auc": "advisor", "select_literals": "advisor",
     "LAYOUTS": "engine", "DataError": "engine", "ColumnSpec": "engine", "Schema": "engine",
