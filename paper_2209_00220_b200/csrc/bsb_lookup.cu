@@ -695,10 +695,23 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
       const int64_t i = i0 + u * nthr;
       const int64_t r = i < n_ids ? __ldg(rows + i) : 0;
       const int64_t blk = r >> 5;
-      VbsBlockMeta mt;
-      vbs_block_meta(vd, blk, mt);
       const int lr = (int)(r & 31);
-      code[u] = vbs_row_code_f<MODE>(vd, blk, lr, mt, __ldg(vd.bs1 + (blk * 32 + swz(lr))), len[u]);
+      const uint32_t first = __ldg(vd.bs1 + (blk * 32 + swz(lr)));
+      // a row outside M_2 has a 1-byte code: no deeper existence words,
+      // directory entry or deep bytes to fetch
+      const uint32_t m2 = vd.K >= 2 ? __ldg(vd.exist[1] + blk) : 0u;
+      if (!((m2 >> lr) & 1u)) {
+        code[u] = first;
+        len[u] = 1;
+      } else {
+        VbsBlockMeta mt;
+        mt.m[0] = 0u;
+        mt.m[1] = m2;
+#pragma unroll
+        for (int j = 3; j <= kMaxLevels; ++j) mt.m[j - 1] = j <= vd.K ? __ldg(vd.exist[j - 1] + blk) : 0u;
+        mt.dir2 = MODE != BSB_DEEP_PACKED ? __ldg(vd.dir[1] + blk) : 0;
+        code[u] = vbs_row_code_f<MODE>(vd, blk, lr, mt, first, len[u]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
