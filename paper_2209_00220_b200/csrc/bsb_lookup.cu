@@ -561,10 +561,13 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
       if (VBS) {
         const bool in = blk < nb;
         if (w) {
+          // deeper words only matter when a selected row owns a level-2 byte
+          m[2] = (in && KL >= 2) ? __ldg(vd.exist[1] + blk) : 0u;
+          const bool deep = (m[2] & w) != 0u;
 #pragma unroll
-          for (int j = 2; j <= kMaxLevels; ++j)
-            if (j <= KL) m[j] = in ? __ldg(vd.exist[j - 1] + blk) : 0u;
-          sdir[lane] = (in && MODE != BSB_DEEP_PACKED && KL >= 2) ? __ldg(vd.dir[1] + blk) : 0;
+          for (int j = 3; j <= kMaxLevels; ++j)
+            if (j <= KL) m[j] = (in && deep) ? __ldg(vd.exist[j - 1] + blk) : 0u;
+          sdir[lane] = (in && deep && MODE != BSB_DEEP_PACKED) ? __ldg(vd.dir[1] + blk) : 0;
           uint32_t v[8];
           ldg256(vd.bs1 + blk * 32, v);
           sts256(stage + lane * 32, v);
