@@ -242,34 +242,49 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
           pP = __funnelshift_r(sm.rP[wi], sm.rP[wi + 1], sb) & lowm;
           pQ = __funnelshift_r(sm.rQ[wi], sm.rQ[wi + 1], sb) & lowm;
         }
-        // deep-row results -> row space (pdep by M_2), trivial cases first
-        uint32_t eP = pP ? m2 : 0u, eQ = pQ ? m2 : 0u;
-        uint32_t ntm = __ballot_sync(kFull, (pP != 0 && pP != lowm) || (pQ != 0 && pQ != lowm));
-        if (ntm) {
-          if (__popc(ntm) > a.serial_blocks) {
+        // deep-row results -> row space (pdep by M_2).  A fused BETWEEN whose
+        // two legs tie on the same rows (the common case: the literals share
+        // their first byte) needs only the combined word "passes lo and not
+        // above hi" -- one pdep, and trivial (all or nothing) for most
+        // blocks of a selective window.
+        const bool same = BETWEEN && zeqA == zeqB;
+        const uint32_t x1 = same ? (pP & ~pQ) : pP;
+        const uint32_t x2 = same ? 0u : pQ;
+        uint32_t e1 = x1 ? m2 : 0u, e2 = x2 ? m2 : 0u;
+        const uint32_t nt1 = __ballot_sync(kFull, x1 != 0 && x1 != lowm);
+        const uint32_t nt2 = __ballot_sync(kFull, x2 != 0 && x2 != lowm);
+        if (nt1 | nt2) {
+          if (__popc(nt1 | nt2) > a.serial_blocks) {
             const ExpandNet net = expand_setup(m2);
-            eP = expand_apply(net, pP);
-            eQ = expand_apply(net, pQ);
+            e1 = expand_apply(net, x1);
+            e2 = expand_apply(net, x2);
           } else {
-            while (ntm) {
+            for (uint32_t ntm = nt1; ntm; ntm &= ntm - 1) {
               const int L = __ffs(ntm) - 1;
-              ntm &= ntm - 1;
-              const uint32_t mL = __shfl_sync(kFull, m2, L);
-              const uint32_t x = warp_pdep(mL, __shfl_sync(kFull, pP, L), lane);
-              const uint32_t y = warp_pdep(mL, __shfl_sync(kFull, pQ, L), lane);
-              if (lane == L) {
-                eP = x;
-                eQ = y;
-              }
+              const uint32_t x = warp_pdep(__shfl_sync(kFull, m2, L),
+                                           __shfl_sync(kFull, x1, L), lane);
+              if (lane == L) e1 = x;
+            }
+            for (uint32_t ntm = nt2; ntm; ntm &= ntm - 1) {
+              const int L = __ffs(ntm) - 1;
+              const uint32_t x = warp_pdep(__shfl_sync(kFull, m2, L),
+                                           __shfl_sync(kFull, x2, L), lane);
+              if (lane == L) e2 = x;
             }
           }
         }
-        if (BETWEEN) {
-          zgtA |= zeqA & eP;
-          zgtB |= zeqB & eQ;
+        if (same) {
+          // tied rows take the deep verdict; the rest were decided at level 1
+          const uint32_t l1 = (zgtA | eqfA) & ~zgtB;
+          zgtA = (l1 & ~zeqA) | (e1 & zeqA);
+          eqfA = 0u;
+          zgtB = 0u;
+        } else if (BETWEEN) {
+          zgtA |= zeqA & e1;
+          zgtB |= zeqB & e2;
         } else {
-          zgtA |= zeqA & eP;
-          eqfA |= zeqA & eQ;
+          zgtA |= zeqA & e1;
+          eqfA |= zeqA & e2;
         }
       }
       const uint32_t res = BETWEEN ? (valid & (zgtA | eqfA) & ~zgtB)
