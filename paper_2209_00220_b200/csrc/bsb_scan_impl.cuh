@@ -93,6 +93,10 @@ __device__ __forceinline__ void fetch_vbs(const VbsDesc& d, int64_t tile, int64_
 }
 
 // ---------------------------------------------------------------- ByteSlice
+// levels >= 2 where every live block has at most this many tied rows compare
+// those rows' bytes one by one instead of the 32-byte SWAR compare
+constexpr int kSparseRows = 4;
+
 template <bool BETWEEN, bool STATS>
 __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, const Leg& B,
                                                  int64_t b, uint32_t valid, const TileIn& in,
@@ -124,6 +128,32 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
   for (int j = 1; j < d.K; ++j) {
     const bool act = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
     if (!__any_sync(kFull, act)) break;
+    const uint32_t cand = BETWEEN ? (zeqA | zeqB) : zeqA;
+    if (BETWEEN && !STATS && !__any_sync(kFull, __popc(cand) > kSparseRows)) {
+      // every live block has only a few tied rows: compare just their bytes
+      if (act) {
+        uint32_t w[8];
+        ldg256(base + (int64_t)j * d.stride, w);
+        const uint32_t la = A.byte[j], lb = B.byte[j];
+        uint32_t gA = 0, eA = 0, gB = 0, eB = 0;
+        for (uint32_t rest = cand; rest; rest &= rest - 1) {
+          const int r = __ffs(rest) - 1;
+          uint32_t x = w[0];
+#pragma unroll
+          for (int q = 1; q < 8; ++q) x = (r & 7) == q ? w[q] : x;
+          const uint32_t by = (x >> ((r >> 3) << 3)) & 0xFFu, bit = 1u << r;
+          gA |= by > la ? bit : 0u;
+          eA |= by == la ? bit : 0u;
+          gB |= by > lb ? bit : 0u;
+          eB |= by == lb ? bit : 0u;
+        }
+        zgtA |= zeqA & gA;
+        zeqA &= eA;
+        zgtB |= zeqB & gB;
+        zeqB &= eB & (zeqA | zgtA);
+      }
+      continue;
+    }
     if (act) {
       uint32_t w[8];
       ldg256(base + (int64_t)j * d.stride, w);
