@@ -109,6 +109,26 @@ __device__ __forceinline__ void cmp_block(const uint32_t (&w)[8], LevelLit L, ui
   ge = e;
 }
 
+// cmp_block for PP-VBS levels: a literal byte 0xFF (PPE's right-most pointer
+// slot, the first byte of every long code in the skewed columns) has nothing
+// above it, so only the >= (here: ==) carries are computed.
+__device__ __forceinline__ void cmp_block_vbs(const uint32_t (&w)[8], LevelLit L, uint32_t& gt,
+                                              uint32_t& ge) {
+  if (L.cgt != 0u) {
+    cmp_block(w, L, gt, ge);
+    return;
+  }
+  uint32_t e = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
+    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
+    e += __byte_perm(ev + L.cge, od + L.cge, 0x7351) << i;
+  }
+  gt = 0u;
+  ge = e;
+}
+
 // Two literals at once (fused BETWEEN), sharing the byte split.
 __device__ __forceinline__ void cmp_block2(const uint32_t (&w)[8], LevelLit A, LevelLit B,
                                            uint32_t& gtA, uint32_t& geA, uint32_t& gtB,

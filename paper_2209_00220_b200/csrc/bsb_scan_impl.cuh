@@ -275,7 +275,7 @@ __device__ __forceinline__ void vbs_level1(const Leg& A, const Leg& B, int K, ui
   if (BETWEEN && A.byte[0] != B.byte[0]) {
     cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
   } else {
-    cmp_block(in.w, A.lv[0], gA, eA);
+    cmp_block_vbs(in.w, A.lv[0], gA, eA);
     gB = gA;
     eB = eA;
   }

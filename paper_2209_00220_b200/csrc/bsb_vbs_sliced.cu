@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
           if (BETWEEN && A.byte[j - 1] != B.byte[j - 1]) {
             cmp_block2(w, A.lv[j - 1], B.lv[j - 1], gA, eA, gB, eB);
           } else {
-            cmp_block(w, A.lv[j - 1], gA, eA);
+            cmp_block_vbs(w, A.lv[j - 1], gA, eA);
             gB = gA;
             eB = eA;
           }
