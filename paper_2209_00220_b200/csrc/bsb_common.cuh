@@ -149,6 +149,30 @@ __device__ __forceinline__ void cmp_block2(const uint32_t (&w)[8], LevelLit A, L
   geB = eb;
 }
 
+// cmp_block2 for PP-VBS levels: when the hi literal byte is 0xFF only its
+// >= carries are needed (nothing is above 0xFF).
+__device__ __forceinline__ void cmp_block2_vbs(const uint32_t (&w)[8], LevelLit A, LevelLit B,
+                                               uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
+                                               uint32_t& geB) {
+  if (B.cgt != 0u) {
+    cmp_block2(w, A, B, gtA, geA, gtB, geB);
+    return;
+  }
+  uint32_t ga = 0, ea = 0, eb = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
+    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
+    ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
+    ea += __byte_perm(ev + A.cge, od + A.cge, 0x7351) << i;
+    eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
+  }
+  gtA = ga;
+  geA = ea;
+  gtB = 0u;
+  geB = eb;
+}
+
 // Packed-order compare of 4 consecutive bytes (rank 4i..4i+3): 4-bit masks.
 __device__ __forceinline__ uint32_t nib4(uint32_t flags) {
   // flags bytes are 0/1; gather bit 0 of each byte into bits 0..3
