@@ -149,6 +149,39 @@ __device__ __forceinline__ void cmp_block2(const uint32_t (&w)[8], LevelLit A, L
   geB = eb;
 }
 
+// Level-1 compares for a lo literal byte 0x00 (the top byte of every small
+// rank): everything is >= it, so only the > carries are computed.  Selected
+// by a kernel template argument, never by a branch inside the compare.
+__device__ __forceinline__ void cmp_block_z(const uint32_t (&w)[8], LevelLit L, uint32_t& gt,
+                                            uint32_t& ge) {
+  uint32_t g = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
+    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
+    g += __byte_perm(ev + L.cgt, od + L.cgt, 0x7351) << i;
+  }
+  gt = g;
+  ge = kFull;
+}
+__device__ __forceinline__ void cmp_block2_z(const uint32_t (&w)[8], LevelLit A, LevelLit B,
+                                             uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
+                                             uint32_t& geB) {
+  uint32_t ga = 0, gb = 0, eb = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
+    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
+    ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
+    gb += __byte_perm(ev + B.cgt, od + B.cgt, 0x7351) << i;
+    eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
+  }
+  gtA = ga;
+  geA = kFull;
+  gtB = gb;
+  geB = eb;
+}
+
 // cmp_block2 for PP-VBS levels: when the hi literal byte is 0xFF only its
 // >= carries are needed (nothing is above 0xFF).
 __device__ __forceinline__ void cmp_block2_vbs(const uint32_t (&w)[8], LevelLit A, LevelLit B,

@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t tile_valid(int64_t tile, int64_t b, int64_t 
 // Persistent grid-stride kernel: one warp per tile, the next tile's level-1
 // operands (and two tiles ahead, its input-mask word) are fetched while the
 // current tile is scanned.
-template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED>
+template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED, bool L1Z = false>
 __global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
     scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
     int depth = 0;
     uint32_t res;
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
-      res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
+      res = scan_tile_bs<BETWEEN, STATS, L1Z>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
       res = scan_tile_vbs<BETWEEN, STATS, LAYOUT - 1>(a.vbs, a.A, a.B, tile, b, valid, in, &st,
                                                      &depth);
@@ -218,6 +218,16 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   const bool stats = a.stats != nullptr;
   BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
+    // ByteSlice with a level-1 literal byte 0x00: the variant without the >=
+    // carries of that literal
+    if (LAYOUT == BSB_LAYOUT_BYTESLICE && a.A.byte[0] == 0u) {
+      if (a.mask) {
+        if (between) return launch_scan(scan_kernel<LAYOUT, true, false, true, true>, a, s);
+        return launch_scan(scan_kernel<LAYOUT, false, false, true, true>, a, s);
+      }
+      if (between) return launch_scan(scan_kernel<LAYOUT, true, false, false, true>, a, s);
+      return launch_scan(scan_kernel<LAYOUT, false, false, false, true>, a, s);
+    }
     if (a.mask) {
       if (between) return launch_scan(scan_kernel<LAYOUT, true, false, true>, a, s);
       return launch_scan(scan_kernel<LAYOUT, false, false, true>, a, s);

@@ -97,7 +97,8 @@ __device__ __forceinline__ void fetch_vbs(const VbsDesc& d, int64_t tile, int64_
 // those rows' bytes one by one instead of the 32-byte SWAR compare
 constexpr int kSparseRows = 4;
 
-template <bool BETWEEN, bool STATS>
+// L1Z: the (lo) literal's level-1 byte is 0x00 (host-selected variant).
+template <bool BETWEEN, bool STATS, bool L1Z = false>
 __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, const Leg& B,
                                                  int64_t b, uint32_t valid, const TileIn& in,
                                                  StatAcc* st, int* depth_out) {
@@ -107,9 +108,15 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
   {
     uint32_t gA, eA, gB, eB;
     if (BETWEEN && A.byte[0] != B.byte[0]) {
-      cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+      if (L1Z)
+        cmp_block2_z(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+      else
+        cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
     } else {
-      cmp_block(in.w, A.lv[0], gA, eA);
+      if (L1Z)
+        cmp_block_z(in.w, A.lv[0], gA, eA);
+      else
+        cmp_block(in.w, A.lv[0], gA, eA);
       gB = gA;
       eB = eA;
     }
