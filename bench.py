@@ -527,7 +527,7 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
     from paper_2209_00220_b200.device import to_dev_u32
     from paper_2209_00220_b200.dictionary import freq_table_and_ranks
     from paper_2209_00220_b200.roofline import hbm_peak, lookup_alg_bytes_rows
-    from paper_2209_00220_b200.vbs import build_vbs, lookup_vbs_rows
+    from paper_2209_00220_b200.vbs import build_vbs
 
     n = 1 << log2n
     m = 1 << (log2n - 4)

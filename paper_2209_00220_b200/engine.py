@@ -23,19 +23,18 @@ import numpy as np
 import torch
 
 from . import _lib
-from .advisor import ColumnAdvice, advise_column
+from .advisor import advise_column
 from .bitpacked import (build_bitpacked, bitpacked_size_report, lookup_bitpacked_bits,
                         scan_bitpacked)
-from .bitvector import DeviceBitVector, ResultBitVector, as_device_bits
-from .byteslice import (ByteSliceColumn, build_byteslice, byteslice_size_report,
-                        lookup_byteslice_bits, lookup_byteslice_rows, scan_byteslice)
+from .bitvector import DeviceBitVector, as_device_bits
+from .byteslice import (build_byteslice, byteslice_size_report, lookup_byteslice_bits,
+                        lookup_byteslice_rows, scan_byteslice)
 from .datagen import PRNG_NAME
 from .device import device, stream
-from .dictionary import ColumnKind, Dictionary, FrequencyTable, table_and_ranks
-from .predicate import DEFAULT_LANES, LaneConfig, Op, Predicate, ResolvedPredicate
+from .dictionary import ColumnKind, Dictionary, table_and_ranks
+from .predicate import DEFAULT_LANES, LaneConfig, Predicate, ResolvedPredicate
 from .vbp import build_vbp, lookup_vbp_bits, pad_codes, scan_vbp, vbp_size_report
-from .vbs import (VbsColumn, build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs,
-                  vbs_size_report)
+from .vbs import build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs, vbs_size_report
 
 __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
            "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",

@@ -3,7 +3,6 @@ host-side logic of the product (literal resolution, PPE assignment, bitvector
 host type, advisor AUC/literal rules) matches the oracle / golden vectors.
 No device compute happens here."""
 
-import ctypes
 import os
 import re
 import subprocess
