@@ -55,3 +55,35 @@ def test_fullsize_windows_layouts_agree_and_between_is_ge_and_le(cfg2):
                 got = E.lookup_decode_bits(store.columns[name], bits[name])
                 rows = bits[name].row_ids()
                 assert torch.equal(got, vals[rows]), (name, p)
+
+
+@pytest.mark.parametrize("s,d", [(0.6, 16), (1.1, 24), (1.2, 20), (2.0, 12)])
+def test_ragged_columns_every_supertile_size(s, d):
+    """Ragged row counts and columns whose deep-row fraction selects each
+    super-tile size of the SLICED kernel: PP-VBS == ByteSlice == a device
+    filter of the raw values, with and without an input mask."""
+    n = (1 << 24) + 12345
+    vals = B.gen_zipf_device(B.ZipfSpec(s, d, n, 77))
+    schema = E.Schema([E.ColumnSpec("v", B.ColumnKind.NUMERIC, "ppvbs"),
+                       E.ColumnSpec("w", B.ColumnKind.NUMERIC, "byteslice")])
+    store, _ = E.ingest_arrays({"v": vals, "w": vals}, schema, policy="forced")
+    srt = torch.sort(vals).values
+    g = torch.Generator(device="cuda").manual_seed(5)
+    maskb = torch.rand(n, device="cuda", generator=g) < 0.7
+    words = torch.zeros(-(-n // 32) * 32, dtype=torch.int64, device="cuda")
+    words[:n] = maskb.to(torch.int64)
+    shifts = torch.arange(32, device="cuda", dtype=torch.int64)
+    mw = (words.view(-1, 32) << shifts).sum(1).to(torch.int64).to(torch.int32)
+    mask = B.bitvector.DeviceBitVector(n, mw)
+    for a, b in ((0.1, 0.3), (0.995, 0.999), (0.0, 0.6)):
+        lo, hi = int(srt[int(a * (n - 1))]), int(srt[int(b * (n - 1))])
+        want = (vals >= lo) & (vals <= hi)
+        for m, wm in ((None, want), (mask, want & maskb)):
+            res = []
+            for name in ("v", "w"):
+                st = store.columns[name]
+                p = st.dictionary.encode_literal(Predicate(name, Op.BETWEEN, lo, hi))
+                bv, _ = E.scan_layout(st.layout, st.column, p, m)
+                res.append(bv)
+            assert torch.equal(res[0].dwords, res[1].dwords), (s, d, a, b)
+            assert res[0].count() == int(wm.sum().item()), (s, d, a, b, m is None)
