@@ -2,8 +2,9 @@
 conjunctions and the layout advisor, as hand-written sm_100a CUDA behind the
 C ABI in include/bytestore_b200.h.
 
-The names re-exported here mirror the reference package's drop-in surface
-(reference __init__.py:10-52) for the in-scope layouts.  Importing the
+The names re-exported here cover the reference package's whole public
+surface (reference __init__.py:10-52, every layout and column kind) plus the
+device-specific entry points.  Importing the
 package does not touch the GPU; the first device call loads
 libbytestore_b200.so and fails loudly if it (or a CUDA device) is missing.
 """

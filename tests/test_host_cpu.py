@@ -197,3 +197,22 @@ def test_device_path_fails_loudly_without_cuda():
         pytest.skip("has a GPU")
     with pytest.raises(RuntimeError, match="CUDA"):
         build_byteslice(np.arange(10), 4)
+
+
+def test_bits_module_matches_oracle():
+    """Host bit helpers (reference bits.py API) agree with the oracle's
+    restatement on random words, and keep the reference's edge cases."""
+    import random
+    from paper_2209_00220_b200 import bits as H
+    rnd = random.Random(3)
+    for _ in range(2000):
+        x, m = rnd.getrandbits(32), rnd.getrandbits(32)
+        assert H.pdep(x, m) == O.pdep(x, m)
+        assert H.pext(x, m) == O.pext(x, m)
+        assert H.pext(H.pdep(x, m), m) == x & ((1 << bin(m).count("1")) - 1)
+        if x:
+            assert H.lowest_set_index(x) == (x & -x).bit_length() - 1
+            assert H.erase_rightmost(x) == x & (x - 1)
+    assert H.erase_rightmost(0) == 0 and H.propagate_rightmost(0) == 0
+    with pytest.raises(ValueError):
+        H.lowest_set_index(0)
