@@ -172,6 +172,9 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
           cmp_block(w, A.lv[j], gA, eA);
           gB = gA;
           eB = eA;
+        } else if (L1Z && A.byte[j] == 0u) {
+          // the L1Z variant also covers deeper lo bytes 0x00 (small ranks)
+          cmp_block2_z(w, A.lv[j], B.lv[j], gA, eA, gB, eB);
         } else {
           cmp_block2(w, A.lv[j], B.lv[j], gA, eA, gB, eB);
         }
