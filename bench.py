@@ -629,6 +629,8 @@ def col_bytes(col) -> int:
     if hasattr(col, "planes"):
         return col.planes.numel()
     b = col.bs1.numel()
+    if col.deep[0] is not None:
+        b += col.deep[0].numel()
     for j in range(1, col.max_len):
         if col.deep[j] is not None:
             b += col.deep[j].numel() * col.deep[j].element_size()
@@ -659,6 +661,7 @@ def measure_e2e(data, scans, steps, n, world):
     host_r = [None] + [None if (col_v.rexist is None or col_v.rexist[j] is None)
                        else col_v.rexist[j].cpu().pin_memory() for j in range(1, K)]
     host_b = col_b.planes.cpu().pin_memory()
+    host_d0 = None if col_v.deep[0] is None else col_v.deep[0].cpu().pin_memory()
 
     def device_copy():
         dv = [None if h is None else torch.empty(h.shape, dtype=h.dtype, device="cuda")
@@ -666,13 +669,15 @@ def measure_e2e(data, scans, steps, n, world):
         dr = [None if h is None else torch.empty(h.shape, dtype=h.dtype, device="cuda")
               for h in host_r]
         db = torch.empty_like(col_b.planes)
+        d0 = None if host_d0 is None else torch.empty_like(host_d0, device="cuda")
         cv = VbsColumn(col_v.n_rows, K, col_v.lanes, col_v.stride, dv[0],
-                       [None] + [dv[1 + 3 * (j - 1)] for j in range(1, K)],
+                       [d0] + [dv[1 + 3 * (j - 1)] for j in range(1, K)],
                        [None] + [dv[2 + 3 * (j - 1)] for j in range(1, K)],
                        [None] + [dv[3 + 3 * (j - 1)] for j in range(1, K)], col_v.level_rows,
                        col_v.deep_mode, dr)
         cb = ByteSliceColumn(col_b.n_rows, col_b.width_bits, col_b.lanes, col_b.stride, db)
-        pairs = [(h, d) for h, d in zip(host_v + host_r + [host_b], dv + dr + [db])
+        pairs = [(h, d) for h, d in zip(host_v + host_r + [host_b, host_d0],
+                                        dv + dr + [db, d0])
                  if h is not None]
         return cv, cb, pairs
 

@@ -102,8 +102,12 @@ typedef struct bsb_byteslice {
  *             without that byte); rexist[j] (j = 2..max_len-1) holds one uint32
  *             per deep block: bit i = deep row 32k+i has byte j+1.  Scanned with
  *             the ByteSlice SWAR compare, one lane per deep block.
- * deep allocations are padded by >= 64 bytes.  Index 0 of deep/exist/
- * block_dir/rexist is unused (level 1 is bs1). */
+ *             deep[0] (optional, SLICED only) holds byte 1 of every deep row
+ *             in the same deep-block layout; when present, unmasked scans
+ *             run entirely in deep-row space for the deep rows.
+ * deep allocations are padded by >= 64 bytes.  Index 0 of exist/block_dir/
+ * rexist is unused (level 1 is bs1); index 0 of deep is unused except as
+ * above. */
 #define BSB_DEEP_PACKED 0
 #define BSB_DEEP_RANK2 1
 #define BSB_DEEP_PLANES 2

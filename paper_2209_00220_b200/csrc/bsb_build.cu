@@ -190,6 +190,7 @@ __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
       // deep rows as a swizzled ByteSlice column + per-deep-block existence words
       const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
       const int64_t pos = (q & ~int64_t(31)) + swz((int)(q & 31));
+      if (deep[0]) deep[0][pos] = (uint8_t)(c >> (8 * (l - 1)));  // level 1 in deep-row space
       for (int j = 2; j <= K; ++j)
         deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
       for (int j = 3; j <= (int)l; ++j)
@@ -356,6 +357,7 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   std::memset(&h, 0, sizeof(h));
   const int mode = col->deep_mode;
   if (mode < BSB_DEEP_PACKED || mode > BSB_DEEP_SLICED) return BSB_EINVAL;
+  if (mode == BSB_DEEP_SLICED) h.deep[0] = const_cast<uint8_t*>(col->deep[0]);  // optional
   for (int j = 1; j < K; ++j) {
     const bool need_dir = mode == BSB_DEEP_PACKED || j == 1;
     const bool need_deep = mode != BSB_DEEP_PLANES || j <= (K >> 1);

@@ -51,6 +51,9 @@ class VbsColumn:
         d.max_len = self.max_len
         d.deep_mode = self.deep_mode
         d.bs1 = self.bs1.data_ptr()
+        if self.deep and self.deep[0] is not None:  # SLICED: deep rows' first byte
+            d.deep[0] = self.deep[0].data_ptr()
+            d.deep_len[0] = self.deep[0].numel() - DEEP_PAD
         for j in range(1, self.max_len):
             if self.deep[j] is not None:
                 d.deep[j] = self.deep[j].data_ptr()
@@ -172,6 +175,9 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
     bs1 = torch.empty(stride, dtype=torch.uint8, device=dev)
     deep, exist, bdir, rex = [None], [None], [None], [None]
     cnt2 = level_rows[1] if K >= 2 else 0
+    if mode == _lib.DEEP_SLICED:
+        # level 1 of the deep rows in deep-row space (deep-space scan kernel)
+        deep[0] = torch.zeros(-(-cnt2 // 32) * 32 + DEEP_PAD, dtype=torch.uint8, device=dev)
     for j in range(1, K):
         if mode == _lib.DEEP_SLICED:
             # byte j+1 of every deep row, swizzled 32-deep-row blocks

@@ -234,6 +234,52 @@ def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
             assert st.block_depth.tolist() == st_w.block_depth.tolist()
 
 
+def test_vbs_sliced_deep_space_scan_vs_oracle():
+    """Unmasked scans of SLICED columns run in deep-row space (deep[0]).
+    Code bytes from a small alphabet with 0x00 / 0xFF (the compare shortcuts)
+    and many ties; literals of every length 1..K, present or not; every op and
+    BETWEEN with lo/hi bytes in either order below the first level (both the
+    shallow-rows-cannot-match variant and the level-1 variant)."""
+    rng = np.random.default_rng(2209)
+    alpha = np.array([0x00, 0x01, 0x7F, 0x80, 0xFE, 0xFF], dtype=np.uint64)
+    for n, K in ((70_001, 2), (50_000, 3), (33_333, 5), (4097, 8), (31, 4)):
+        lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+        lens[rng.random(n) < 0.5] = 1  # ~half the rows shallow
+        byts = alpha[rng.integers(0, len(alpha), size=(n, 8))]
+        byts[:, 0] |= np.uint64(1)
+        codes = np.zeros(n, np.uint64)
+        for k in range(8):
+            use = lens > k
+            codes[use] |= byts[use, k] << np.uint64(8 * k)
+        col = B.build_vbs(codes, lens, deep_mode="sliced")
+        assert col.deep[0] is not None
+        ocol = O.vbs_build(codes, lens)
+
+        def lit():
+            ll = int(rng.integers(1, K + 1))
+            bs = alpha[rng.integers(0, len(alpha), size=ll)]
+            bs[-1] |= np.uint64(1)
+            return sum(int(b) << (8 * (ll - 1 - i)) for i, b in enumerate(bs)), ll
+
+        for _ in range(6):
+            c, ll = lit()
+            for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                p = O.pred_compare(op, c, ll)
+                want, _ = O.vbs_scan(ocol, p)
+                bv, _ = B.scan_vbs(col, rp(list(p)))
+                assert np.array_equal(bv.words, want), (n, K, op, hex(c), ll)
+                assert bv.count() == O.words_count(want)
+            c2, l2 = lit()
+            if K >= 2 and rng.random() < 0.5:  # share the first byte (no level-1 pass)
+                c2 = (c >> (8 * (ll - 1)) << (8 * (l2 - 1))) | (c2 & ((1 << (8 * (l2 - 1))) - 1))
+            for lo, hi in (((c, ll), (c2, l2)), ((c2, l2), (c, ll))):
+                p = O.pred_between(lo[0], lo[1], hi[0], hi[1])
+                want, _ = O.vbs_scan(ocol, p)
+                bv, _ = B.scan_vbs(col, rp(list(p)))
+                assert np.array_equal(bv.words, want), (n, K, hex(lo[0]), hex(hi[0]))
+                assert bv.count() == O.words_count(want)
+
+
 @pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_row_lookup_decode_vs_oracle(mode):
     n = 200_000
