@@ -72,6 +72,7 @@ _P = c_void_p
 _SIGS = {
     "bsb_version": (c_char_p, []),
     "bsb_last_error": (c_char_p, []),
+    "bsb_tune": (c_int32, [c_char_p, c_int64]),
     "bsb_stride_for": (c_int64, [c_int64]),
     "bsb_byteslice_build": (c_int32, [_P, c_int64, c_int32, _P, c_int64, _P]),
     "bsb_byteslice_build_ranks": (c_int32, [_P, c_int64, c_int32, _P, c_int64, _P]),

@@ -337,19 +337,13 @@ int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const L
                     const Leg& B, bool between,
                     const uint32_t* mask, uint32_t* out, unsigned long long* count,
                     cudaStream_t s);
-int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const Leg& A,
-                const Leg& B, bool between, uint32_t* out, unsigned long long* count,
-                cudaStream_t s);
+int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
+                const Leg& A, const Leg& B, bool between, uint32_t* out,
+                unsigned long long* count, cudaStream_t s);
 }
 
-// Deep-row-space kernel for unmasked SLICED scans (BSB_DS=0 disables it).
-static bool ds_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("BSB_DS");
-    on = (e && std::atoi(e) == 0) ? 0 : 1;
-  }
-  return on == 1;
+namespace bsb {
+bool ds_enabled();  // bsb_tune("ds_enable") / BSB_DS
 }
 
 // The cooperative plane scan needs every multi-byte literal to end in a
@@ -401,8 +395,8 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
       return K <= 5 ? scan_dispatch<1 + BSB_DEEP_PLANES>(a, pred, K, s)
                     : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
     case BSB_DEEP_SLICED:
-      if (!mask && K >= 2 && col->deep[0] && ds_enabled())
-        return vbs_ds_scan(a.vbs, a.n_rows, col->deep_len[1], a.A, a.B,
+      if (!mask && K >= 2 && col->deep[0] && bsb::ds_enabled())
+        return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], a.A, a.B,
                            pred->op == BSB_BETWEEN, out_words, a.count, s);
       return vbs_sliced_scan(a.vbs, a.n_rows, K >= 2 ? col->deep_len[1] : 0, a.A, a.B,
                              pred->op == BSB_BETWEEN, mask, out_words, a.count, s);

@@ -16,9 +16,16 @@
 // final-result word per deep block; phase 3 deposits each row block's window
 // of deep results at its M_2 lanes (pdep) and writes the result word.
 //
-// L1 = false: the shallow rows cannot match (a BETWEEN whose legs share their
-// first byte with a multi-byte lo literal, or EQ with a multi-byte literal),
-// so phase 1 reads only the M_2 words -- no first-slice bytes at all.
+// The shallow rows' result is a function of two byte thresholds (host-chosen
+// from the operator and the literals' first bytes).  L1 = false: no shallow
+// row can match (e.g. a BETWEEN whose legs share their first byte with a
+// multi-byte lo literal, or EQ with a multi-byte literal), so phase 1 reads
+// only the M_2 words -- no first-slice bytes at all.
+// The L1 variant prefetches the next super-tile's first-slice bytes into L2
+// (cp.async.bulk.prefetch) instead of holding them in registers across
+// phases 2-3.  (Measured and dropped: L2 prefetch of the next super-tile's
+// deep levels, and requesting level j+1 together with level j -- neither
+// moved the time.)
 // Unmasked scans only; masked scans (conjunction chains) use the SLICED
 // kernel, which skips the loads of masked-out blocks.
 #include <cstdlib>
@@ -34,72 +41,106 @@ constexpr int kDsWarps = kDsThreads / 32;
 struct DsArgs {
   int64_t n_rows, nb, ntiles;
   int64_t full_tiles;
-  int serial_blocks;
+  int64_t nbpad;      // blocks covered by exist[1] / block_dir[1] (stride / 32)
+  int serial_blocks;  // warp-cooperative pdep up to this many blocks per tile
+  // Row-space level 1 (L1 variant): shallow result = valid & ~M_2 &
+  // ((P & ~Q) ^ inv) with P = [byte >= tP], Q = [byte >= tQ]; cP / cQ are the
+  // carry constants (256 - t) * 0x00010001 (t = 256 -> 0: never), cQ == 0
+  // skips the Q compare.
+  uint32_t cP, cQ, inv;
   VbsDesc d;
   Leg A, B;
   uint32_t* out;
   unsigned long long* count;
 };
 
-// Compare the 32 swizzled bytes of a block against literal bytes; GA/EA/GB/EB
-// select which of (gt, ge) per leg are computed.  Not computed: gt = 0 (the
-// literal byte is 0xFF, nothing is greater), ge = all (the byte is 0x00).
-template <bool GA, bool EA, bool GB, bool EB>
-__device__ __forceinline__ void cmp_sel(const uint32_t (&w)[8], LevelLit A, LevelLit B,
-                                        uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
-                                        uint32_t& geB) {
-  uint32_t ga = 0, ea = 0, gb = 0, eb = 0;
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Threshold compares of the 32 swizzled bytes of a block: P = [byte >= tP],
+// Q = [byte >= tQ] (constants as in DsArgs), lane masks in row order.
+template <bool TWO>
+__device__ __forceinline__ void thr_cmp(const uint32_t (&w)[8], uint32_t cP, uint32_t cQ,
+                                        uint32_t& P, uint32_t& Q) {
+  uint32_t p = 0, q = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
     const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    if (GA) ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
-    if (EA) ea += __byte_perm(ev + A.cge, od + A.cge, 0x7351) << i;
-    if (GB) gb += __byte_perm(ev + B.cgt, od + B.cgt, 0x7351) << i;
-    if (EB) eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
+    p += __byte_perm(ev + cP, od + cP, 0x7351) << i;
+    if (TWO) q += __byte_perm(ev + cQ, od + cQ, 0x7351) << i;
   }
-  gtA = GA ? ga : 0u;
-  geA = EA ? ea : kFull;
-  gtB = GB ? gb : 0u;
-  geB = EB ? eb : kFull;
+  P = p;
+  Q = TWO ? q : 0u;
 }
 
-// literal byte class: 0 = other, 1 = 0xFF (no gt), 2 = 0x00 (ge = all)
-__device__ __forceinline__ int byte_class(uint32_t b) { return b == 0xFFu ? 1 : (b == 0u ? 2 : 0); }
-
-// (gt, eq) of both legs at level index j0 (0-based) -- eq = ge & ~gt.
+// (gt, eq) of both legs at level index j0 (0-based).  One literal byte 0xFF
+// (PPE's right-most pointer slot) needs only the equality carries; two
+// different bytes take the four-compare form (whose constants already give
+// gt = 0 for 0xFF and ge = all for 0x00).
 template <bool BETWEEN>
 __device__ __forceinline__ void cmp_level(const uint32_t (&w)[8], const Leg& A, const Leg& B,
                                           int j0, uint32_t& gA, uint32_t& eA, uint32_t& gB,
                                           uint32_t& eB) {
-  const uint32_t ba = A.byte[j0], bb = B.byte[j0];
-  const LevelLit la = A.lv[j0], lb = B.lv[j0];
-  uint32_t geA, geB;
-  if (!BETWEEN || ba == bb) {
-    switch (byte_class(ba)) {
-      case 1: cmp_sel<false, true, false, false>(w, la, la, gA, geA, gB, geB); break;
-      case 2: cmp_sel<true, false, false, false>(w, la, la, gA, geA, gB, geB); break;
-      default: cmp_sel<true, true, false, false>(w, la, la, gA, geA, gB, geB); break;
+  const LevelLit la = A.lv[j0];
+  if (!BETWEEN || A.byte[j0] == B.byte[j0]) {
+    uint32_t ge;
+    if (la.cgt == 0u) {
+      cmp_block_vbs(w, la, gA, ge);  // equality only
+    } else {
+      cmp_block(w, la, gA, ge);
     }
+    eA = ge & ~gA;
     gB = gA;
-    geB = geA;
+    eB = eA;
   } else {
-    switch (byte_class(ba) * 3 + byte_class(bb)) {
-      case 0: cmp_sel<true, true, true, true>(w, la, lb, gA, geA, gB, geB); break;
-      case 1: cmp_sel<true, true, false, true>(w, la, lb, gA, geA, gB, geB); break;
-      case 2: cmp_sel<true, true, true, false>(w, la, lb, gA, geA, gB, geB); break;
-      case 3: cmp_sel<false, true, true, true>(w, la, lb, gA, geA, gB, geB); break;
-      case 5: cmp_sel<false, true, true, false>(w, la, lb, gA, geA, gB, geB); break;
-      case 6: cmp_sel<true, false, true, true>(w, la, lb, gA, geA, gB, geB); break;
-      case 7: cmp_sel<true, false, false, true>(w, la, lb, gA, geA, gB, geB); break;
-      default: cmp_sel<true, true, true, true>(w, la, lb, gA, geA, gB, geB); break;
-    }
+    uint32_t geA, geB;
+    cmp_block2(w, la, B.lv[j0], gA, geA, gB, geB);
+    eA = geA & ~gA;
+    eB = geB & ~gB;
   }
-  eA = geA & ~gA;
-  eB = geB & ~gB;
 }
 
-template <bool BETWEEN, bool L1, int ST>
+__device__ __forceinline__ uint32_t lane_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+// One Alg. 3 level over the lane's deep block (vbs.py:258-284 in deep-row
+// space); false once no lane of the warp has a tied row left.
+template <bool BETWEEN>
+__device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, uint32_t& zA,
+                                         uint32_t& zB, uint32_t& gtA, uint32_t& eqA,
+                                         uint32_t& gtB, uint32_t& eqB) {
+  const VbsDesc& d = a.d;
+  const int K = d.K;
+  const bool act = BETWEEN ? ((zA | zB) != 0) : (zA != 0);
+  if (!__any_sync(kFull, act)) return false;
+  uint32_t w[8];
+  if (act) {
+    ldg256(d.deep[j - 1] + dbk * 32, w);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = 0;
+  }
+  // existence of byte j+1 among the deep rows (byte 2 always exists)
+  const uint32_t nxt = j >= K ? 0u : (j == 1 ? kFull : (act ? __ldg(d.rexist[j] + dbk) : 0u));
+  uint32_t gA, eA, gB, eB;
+  cmp_level<BETWEEN>(w, a.A, a.B, j - 1, gA, eA, gB, eB);
+  vbs_transition(j, a.A.len, K, gA, eA, nxt, zA, gtA, eqA);
+  if (BETWEEN) {
+    vbs_transition(j, a.B.len, K, gB, eB, nxt, zB, gtB, eqB);
+    zB &= zA | gtA | eqA;  // hi-leg ties that already fail GE(lo) are settled
+  }
+  return true;
+}
+
+template <bool BETWEEN, bool L1, int ST, bool UNR>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
   __shared__ uint32_t rd_all[kDsWarps][kRd];
@@ -117,9 +158,9 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   unsigned long long cnt = 0;
 
   // level-1 sector (L1 only) and M_2 word of block b; zeros past the column
-  auto fetch = [&](int64_t b, uint32_t (&w)[8], uint32_t& m2) {
+  auto fetch = [&](int64_t b, uint32_t (&w)[8], uint32_t& m2, bool bytes) {
     const bool in = b < a.nb;
-    if (L1) {
+    if (L1 && bytes) {
       if (in) {
         ldg256(d.bs1 + b * 32, w);
       } else {
@@ -129,19 +170,24 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     }
     m2 = in ? __ldg(d.exist[1] + b) : 0u;
   };
-  auto valid_of = [&](int64_t tile, int64_t b) -> uint32_t {
-    return tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
+  auto dir_at = [&](int64_t blk) -> int64_t {
+    return __ldg(d.dir[1] + (blk < a.nbpad ? blk : a.nbpad));
   };
 
   int64_t st = warp;
   uint32_t wN[8];
   uint32_t m2N = 0;
-  if (st < nsuper) fetch(st * ST * 32 + lane, wN, m2N);
+  if (st < nsuper) fetch(st * ST * 32 + lane, wN, m2N, false);
   for (; st < nsuper; st += nwarps) {
-    const int64_t dfirst = __ldg(d.dir[1] + st * ST * 32);  // first deep row of the super-tile
+    const int64_t dfirst = dir_at(st * ST * 32);  // first deep row of the super-tile
+    const int64_t nxt_b0 = (st + nwarps) * ST * 32;
+    const bool has_next = st + nwarps < nsuper;
     uint32_t rs[ST], m2s[ST];
     int offs[ST];
     int soff = 0;  // deep rows of this super-tile so far
+    // first tile's bytes (L2-prefetched by the previous super-tile); not held
+    // in registers across phases 2-3
+    if (L1) fetch(st * ST * 32 + lane, wN, m2N, true);
     // ---------------- phase 1: shallow rows (lane = row block)
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
@@ -152,25 +198,30 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       for (int i = 0; i < 8; ++i) w[i] = wN[i];
       const uint32_t m2 = m2N;
       const int64_t ntile = (u + 1 < ST) ? tile + 1 : (st + nwarps) * ST;
-      fetch(ntile * 32 + lane, wN, m2N);  // zeros past the column
+      fetch(ntile * 32 + lane, wN, m2N, u + 1 < ST);  // zeros past the column
       uint32_t res = 0;
       if (L1) {
-        const uint32_t valid = valid_of(tile, b);
-        uint32_t gA, eA, gB, eB;
-        cmp_level<BETWEEN>(w, A, B, 0, gA, eA, gB, eB);
-        if (BETWEEN) {
-          res = valid & (lenA == 1 ? (gA | eA) : gA) & ~gB;
-        } else {
-          res = finalize_op(A.op, gA, lenA == 1 ? eA : 0u, valid);
-        }
-        res &= ~m2;
+        const uint32_t valid =
+            tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
+        uint32_t P, Q;
+        if (a.cQ)
+          thr_cmp<true>(w, a.cP, a.cQ, P, Q);
+        else
+          thr_cmp<false>(w, a.cP, 0u, P, Q);
+        res = valid & ~m2 & ((P & ~Q) ^ a.inv);
       }
       rs[u] = res;
       m2s[u] = m2;
       const int c2 = __popc(m2);
-      const uint32_t incl = warp_incl_scan((uint32_t)c2);
+      const uint32_t incl = lane_incl_scan((uint32_t)c2, lane);
       offs[u] = soff + (int)(incl - (uint32_t)c2);
       soff += (int)__shfl_sync(kFull, incl, 31);
+    }
+    // next super-tile's first-slice bytes -> L2 (its first tile is loaded at
+    // the top of the next iteration)
+    if (L1 && has_next && lane == 0) {
+      const int64_t nblk = a.nbpad - nxt_b0 < ST * 32 ? a.nbpad - nxt_b0 : ST * 32;
+      l2_prefetch(d.bs1 + nxt_b0 * 32, (uint32_t)(nblk * 32));
     }
     // ---------------- phase 2: deep rows (lane = deep block)
     const int64_t db0 = dfirst >> 5;
@@ -182,27 +233,14 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       const int64_t dbk = db0 + t;
       uint32_t zA = has ? kFull : 0u, zB = (BETWEEN && has) ? kFull : 0u;
       uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
+      if (UNR) {
 #pragma unroll
-      for (int j = 1; j <= kMaxLevels; ++j) {
-        if (j > maxlen) break;
-        const bool act = BETWEEN ? ((zA | zB) != 0) : (zA != 0);
-        if (!__any_sync(kFull, act)) break;
-        uint32_t w[8];
-        if (act) {
-          ldg256(d.deep[j - 1] + dbk * 32, w);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) w[q] = 0;
-        }
-        // existence of byte j+1 among the deep rows (byte 2 always exists)
-        const uint32_t nxt = j >= K ? 0u : (j == 1 ? kFull : (act ? __ldg(d.rexist[j] + dbk) : 0u));
-        uint32_t gA, eA, gB, eB;
-        cmp_level<BETWEEN>(w, A, B, j - 1, gA, eA, gB, eB);
-        vbs_transition(j, lenA, K, gA, eA, nxt, zA, gtA, eqA);
-        if (BETWEEN) {
-          vbs_transition(j, lenB, K, gB, eB, nxt, zB, gtB, eqB);
-          zB &= zA | gtA | eqA;  // hi-leg ties that already fail GE(lo) are settled
-        }
+        for (int j = 1; j <= kMaxLevels; ++j)
+          if (j > maxlen || !ds_level<BETWEEN>(a, j, dbk, zA, zB, gtA, eqA, gtB, eqB)) break;
+      } else {
+#pragma unroll 1
+        for (int j = 1; j <= maxlen; ++j)
+          if (!ds_level<BETWEEN>(a, j, dbk, zA, zB, gtA, eqA, gtB, eqB)) break;
       }
       if (has) rd[t] = BETWEEN ? ((gtA | eqA) & ~gtB) : finalize_op(A.op, gtA, eqA, kFull);
     }
@@ -211,8 +249,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     // ---------------- phase 3: deep results back to row space (lane = row block)
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
-      const int64_t tile = st * ST + u;
-      const int64_t b = tile * 32 + lane;
+      const int64_t b = (st * ST + u) * 32 + lane;
       const uint32_t m2 = m2s[u];
       const int o = sh0 + offs[u];
       const int wi = o >> 5, sb = o & 31;
@@ -245,9 +282,9 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool L1, int ST>
+template <bool BETWEEN, bool L1, int ST, bool UNR>
 static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_ds_kernel<BETWEEN, L1, ST>;
+  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -260,35 +297,54 @@ static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 
-template <bool BETWEEN, bool L1>
-static int launch_ds(const DsArgs& a, int st, cudaStream_t s) {
+template <bool BETWEEN, bool L1, bool UNR>
+static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
-    case 1: return launch_ds_k<BETWEEN, L1, 1>(a, s);
-    case 2: return launch_ds_k<BETWEEN, L1, 2>(a, s);
-    case 3: return launch_ds_k<BETWEEN, L1, 3>(a, s);
-    default: return launch_ds_k<BETWEEN, L1, 4>(a, s);
+    case 1: return launch_ds_k<BETWEEN, L1, 1, UNR>(a, s);
+    case 2: return launch_ds_k<BETWEEN, L1, 2, UNR>(a, s);
+    case 3: return launch_ds_k<BETWEEN, L1, 3, UNR>(a, s);
+    default: return launch_ds_k<BETWEEN, L1, 4, UNR>(a, s);
   }
 }
+template <bool BETWEEN, bool L1>
+static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
+  return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
+}
 
-// Unmasked scan of a SLICED column that carries deep[0].  Returns
-// BSB_EINVAL when the column lacks deep[0] (caller falls back).
-int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const Leg& A,
-                const Leg& B, bool between, uint32_t* out, unsigned long long* count,
-                cudaStream_t s) {
+// Run-time tunables (bsb_tune): 0 enable, 1 serial pdep blocks, 2 tiles per
+// super-tile (0 = auto), 3 unrolled levels.
+constexpr int kTunes = 4;
+static int g_tune[kTunes] = {-1, -1, -1, -1};
+static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles",
+                                              "ds_unroll"};
+static int tune(int i) {
+  if (g_tune[i] < 0) {
+    static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
+                                            "BSB_DS_UNROLL"};
+    static const int dflt[kTunes] = {1, 6, 0, 1};
+    const char* e = std::getenv(env[i]);
+    g_tune[i] = e ? std::atoi(e) : dflt[i];
+  }
+  return g_tune[i];
+}
+bool ds_enabled() { return tune(0) != 0; }
+
+static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
+
+// Unmasked scan of a SLICED column that carries deep[0] (K >= 2).
+int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
+                const Leg& A, const Leg& B, bool between, uint32_t* out,
+                unsigned long long* count, cudaStream_t s) {
   DsArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n_rows = n_rows;
   a.nb = (n_rows + 31) / 32;
   a.ntiles = (a.nb + 31) / 32;
   a.full_tiles = n_rows / kTileRows;
-  static int serial = -1, st_env = -1;
-  if (serial < 0) {
-    const char* e = std::getenv("BSB_DS_SERIAL");
-    serial = e ? std::atoi(e) : 6;
-    const char* t = std::getenv("BSB_DS_TILES");
-    st_env = t ? std::atoi(t) : 0;
-  }
-  a.serial_blocks = serial;
+  a.nbpad = stride / 32;
+  const int st_env = tune(2);
+  const bool unr = tune(3) != 0;
+  a.serial_blocks = tune(1);
   a.d = d;
   a.A = A;
   a.B = B;
@@ -301,12 +357,48 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const Leg& 
     st = per_tile > 0 ? (int)(28.0 / per_tile + 0.5) : 4;
     st = st < 1 ? 1 : (st > 4 ? 4 : st);
   }
-  // shallow rows can only match when the level-1 compare can tell them apart
-  const bool l1 = between ? !(A.len >= 2 && A.byte[0] == B.byte[0])
-                          : !(A.op == BSB_EQ && A.len >= 2);
+  // shallow rows (vbs.py:272-284 with M_2 = 0): gt = byte > lit, eq_final =
+  // byte == lit only for a 1-byte literal
+  const int la = (int)A.byte[0], lb = (int)B.byte[0];
+  const int ge_a = la + (A.len >= 2 ? 1 : 0);  // [byte >= ge_a] == gt | eq_final
+  int tP = 256, tQ = 256;
+  uint32_t inv = 0;
+  if (between) {
+    tP = ge_a;
+    tQ = lb + 1;
+  } else {
+    switch (A.op) {
+      case BSB_GT: tP = la + 1; break;
+      case BSB_GE: tP = ge_a; break;
+      case BSB_LT: tP = ge_a; inv = kFull; break;
+      case BSB_LE: tP = la + 1; inv = kFull; break;
+      case BSB_EQ:
+        if (A.len == 1) { tP = la; tQ = la + 1; }
+        break;
+      default:  // NE
+        if (A.len == 1) { tP = la; tQ = la + 1; }
+        inv = kFull;
+        break;
+    }
+  }
+  a.cP = carry_const(tP);
+  a.cQ = carry_const(tQ);
+  a.inv = inv;
+  const bool l1 = inv != 0 || (tP < 256 && tP < tQ);  // else no shallow row can match
   BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
-  if (between) return l1 ? launch_ds<true, true>(a, st, s) : launch_ds<true, false>(a, st, s);
-  return l1 ? launch_ds<false, true>(a, st, s) : launch_ds<false, false>(a, st, s);
+  if (between)
+    return l1 ? launch_ds<true, true>(a, st, unr, s) : launch_ds<true, false>(a, st, unr, s);
+  return l1 ? launch_ds<false, true>(a, st, unr, s) : launch_ds<false, false>(a, st, unr, s);
 }
 
 }  // namespace bsb
+
+extern "C" int bsb_tune(const char* key, int64_t value) {
+  if (!key) return BSB_EINVAL;
+  for (int i = 0; i < bsb::kTunes; ++i)
+    if (std::strcmp(key, bsb::kTuneKeys[i]) == 0) {
+      bsb::g_tune[i] = value < 0 ? 0 : (int)value;
+      return BSB_OK;
+    }
+  return BSB_EINVAL;
+}

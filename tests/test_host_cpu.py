@@ -45,6 +45,14 @@ def test_library_exports_every_header_symbol(lib):
         assert re.search(rf"\bT {name}$", out, re.M), name
 
 
+def test_tune_knobs(lib):
+    # host-side knobs of the deep-row-space PP-VBS scan; unknown keys rejected
+    for key, val in ((b"ds_serial", 6), (b"ds_tiles", 0), (b"ds_unroll", 1), (b"ds_enable", 1)):
+        assert lib.bsb_tune(key, val) == 0
+    assert lib.bsb_tune(b"no_such_knob", 1) != 0
+    assert lib.bsb_tune(None, 1) != 0
+
+
 def test_library_is_sm100a(lib):
     from paper_2209_00220_b200 import _lib
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
