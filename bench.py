@@ -448,7 +448,7 @@ def run_b200(args):
         if world == 1 and not args.profile and not args.no_cpu_baseline:
             cpu = cpu_baseline(n, 1 << 22, os.cpu_count() or 1)
         dom_e = by_layout[dom]
-        kname = ("vbs_sliced_kernel<BETWEEN> (PP-VBS, SLICED deep layout)"
+        kname = ("vbs_ds_kernel<BETWEEN> (PP-VBS, SLICED layout scanned in deep-row space)"
                  if dom == "ppvbs" and col_v.deep_mode == _lib.DEEP_SLICED else
                  f"scan_kernel<{dom}, BETWEEN>")
         out = {
@@ -471,6 +471,13 @@ def run_b200(args):
                          "traffic": traffic,
                          "traffic_source": "profiles/ncu_traffic.json (dram read+write per "
                                            "launch, mean of the 4 windows)",
+                         # physical DRAM bytes per launch over the same launch time: below
+                         # the algorithmic fraction when the kernel skips bytes the
+                         # reference reads (PP-VBS: level-1 slice of rows that cannot match)
+                         "dram_gbs": (round(traffic / (dom_e["ms"] / 4 * 1e-3) / 1e9, 1)
+                                      if traffic else None),
+                         "dram_frac": (round(traffic / (dom_e["ms"] / 4 * 1e-3) / 1e9 / peak, 4)
+                                       if traffic else None),
                          "alg_bytes_per_launch": int(dom_e["alg_bytes"] / 4),
                          "alg_bytes_per_step": int(dom_e["alg_bytes"])},
             "layouts": {k: {"gcodes_s": round(v["gcodes_s"], 2), "hbm_gbs": round(v["gbs"], 1),

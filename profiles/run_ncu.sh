@@ -10,10 +10,10 @@ OUT=${OUT:-gpurun_out}
 mkdir -p "$OUT"
 CMD="python bench.py --profile --steps 3 --warmup 1 --no-lookup"
 $CMD > "$OUT/profile_plain.log" 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'bsb|cub' \
+ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -c 400 \
     --csv --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:'vbs_sliced_kernel' -s 4 -c 4 -o "$OUT/prof_vbs" $CMD > "$OUT/ncu_vbs.log" 2>&1
+    -k regex:'vbs_ds_kernel' -s 4 -c 4 -o "$OUT/prof_vbs" $CMD > "$OUT/ncu_vbs.log" 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k regex:'scan_kernel<.int.0, .bool.1, .bool.0, .bool.0' -s 4 -c 4 -o "$OUT/prof_bs" $CMD \
     > "$OUT/ncu_bs.log" 2>&1
