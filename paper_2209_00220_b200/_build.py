@@ -51,7 +51,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     for src in _sources():
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) <= max(
                 os.path.getmtime(src), dep_t):
             jobs.append((src, obj))
 

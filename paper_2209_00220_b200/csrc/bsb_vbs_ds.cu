@@ -312,22 +312,24 @@ static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
 }
 
 // Run-time tunables (bsb_tune): 0 enable, 1 serial pdep blocks, 2 tiles per
-// super-tile (0 = auto), 3 unrolled levels.
-constexpr int kTunes = 4;
-static int g_tune[kTunes] = {-1, -1, -1, -1};
+// super-tile (0 = auto), 3 unrolled levels; 4 ByteSlice BETWEEN level-1
+// row-by-row ties up to (value - 1) inside rows per block (0 = never).
+constexpr int kTunes = 5;
+static int g_tune[kTunes] = {-1, -1, -1, -1, -1};
 static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles",
-                                              "ds_unroll"};
+                                              "ds_unroll", "bs_sparse1"};
 static int tune(int i) {
   if (g_tune[i] < 0) {
     static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
-                                            "BSB_DS_UNROLL"};
-    static const int dflt[kTunes] = {1, 6, 0, 1};
+                                            "BSB_DS_UNROLL", "BSB_BS_SPARSE1"};
+    static const int dflt[kTunes] = {1, 6, 0, 1, 2};
     const char* e = std::getenv(env[i]);
     g_tune[i] = e ? std::atoi(e) : dflt[i];
   }
   return g_tune[i];
 }
 bool ds_enabled() { return tune(0) != 0; }
+int bs_sparse1() { return tune(4) - 1; }  // knob 0 = always the SWAR compares
 
 static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 

@@ -106,6 +106,35 @@ def test_byteslice_random_large_between_and_masks():
                     assert bv.count() == O.words_count(want)
 
 
+def test_byteslice_narrow_between_windows():
+    """Narrow BETWEEN windows (level-1 inside rows found row by row), windows
+    whose bounds share or neighbour their first byte, lo byte 0x00, lo > hi,
+    skewed columns with many ties, with and without a mask."""
+    rng = np.random.default_rng(321)
+    for w, n in ((20, (1 << 19) + 5), (16, 100_003), (24, 65_536), (12, 777)):
+        codes = np.minimum(rng.zipf(1.3, size=n) - 1, (1 << w) - 1).astype(np.uint64)
+        codes[rng.random(n) < 0.3] = rng.integers(0, 1 << w, size=int((rng.random(n) < 0.3).sum()) or 1,
+                                                  dtype=np.uint64)[:1]
+        codes ^= rng.integers(0, 1 << w, size=n, dtype=np.uint64) * (rng.random(n) < 0.5)
+        col = B.build_byteslice(codes, w)
+        planes = O.bs_build(codes, w)
+        K = planes.shape[0]
+        mw = O.bools_to_words(rng.random(n) < 0.6)
+        top = 1 << w
+        srt = np.sort(codes)
+        wins = [(int(srt[int(q * (n - 1))]), int(srt[int(min(1.0, q + d) * (n - 1))]))
+                for q in (0.1, 0.5, 0.9, 0.999) for d in (0.0, 0.0005, 0.01, 0.2)]
+        wins += [(0, 5), (0, top - 1), (top - 1, top - 1), (9, 3), (top // 2, top // 2 + 1),
+                 (top // 2 - 1, top // 2), ((1 << (w - 8)) * 7, (1 << (w - 8)) * 8)]
+        for a, b in wins:
+            p = O.pred_between(a, K, b, K)
+            for m_o, m_d in ((None, None), (mw, B.ResultBitVector(n, mw))):
+                want, _ = O.bs_scan(planes, w, n, p, m_o)
+                bv, _ = B.scan_byteslice(col, rp(list(p)), m_d)
+                assert np.array_equal(bv.words, want), (w, n, a, b)
+                assert bv.count() == O.words_count(want)
+
+
 def test_byteslice_row_lookup_unsorted_duplicates():
     rng = np.random.default_rng(5)
     n, w = 100_003, 24
