@@ -114,15 +114,18 @@ __device__ __forceinline__ uint32_t lane_incl_scan(uint32_t v, int lane) {
 // One Alg. 3 level over the lane's deep block (vbs.py:258-284 in deep-row
 // space); false once no lane of the warp has a tied row left.
 template <bool BETWEEN>
-__device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, uint32_t& zA,
-                                         uint32_t& zB, uint32_t& gtA, uint32_t& eqA,
-                                         uint32_t& gtB, uint32_t& eqB) {
+__device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, const uint32_t* pre,
+                                         uint32_t& zA, uint32_t& zB, uint32_t& gtA,
+                                         uint32_t& eqA, uint32_t& gtB, uint32_t& eqB) {
   const VbsDesc& d = a.d;
   const int K = d.K;
   const bool act = BETWEEN ? ((zA | zB) != 0) : (zA != 0);
   if (!__any_sync(kFull, act)) return false;
   uint32_t w[8];
-  if (act) {
+  if (j == 1 && pre != nullptr) {  // level-1 sector requested one phase earlier
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = pre[q];
+  } else if (act) {
     ldg256(d.deep[j - 1] + dbk * 32, w);
   } else {
 #pragma unroll
@@ -174,33 +177,62 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     return __ldg(d.dir[1] + (blk < a.nbpad ? blk : a.nbpad));
   };
 
+  // Software pipeline over this warp's super-tiles: the next super-tile's
+  // directory bounds are requested at the top of an iteration, its M_2 words
+  // and level-1 deep sectors right after phase 2, so that phase 3 and the
+  // next phase 1 cover their latency.
+  auto load_m2 = [&](int64_t s, uint32_t (&m)[ST]) {
+#pragma unroll
+    for (int u = 0; u < ST; ++u) {
+      const int64_t b = (s * ST + u) * 32 + lane;
+      m[u] = b < a.nb ? __ldg(d.exist[1] + b) : 0u;
+    }
+  };
+  auto load_l1 = [&](int64_t lo, int64_t hi, uint32_t (&w)[8]) {
+    const int64_t dbk = (lo >> 5) + lane;
+    if (dbk < ((hi + 31) >> 5)) {
+      ldg256(d.deep[0] + dbk * 32, w);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = 0;
+    }
+  };
+
   int64_t st = warp;
-  uint32_t wN[8];
-  uint32_t m2N = 0;
-  if (st < nsuper) fetch(st * ST * 32 + lane, wN, m2N, false);
+  uint32_t m2P[ST], wP[8], wN[8];
+  int64_t dlo = 0;
+  if (st < nsuper) {
+    dlo = dir_at(st * ST * 32);
+    load_m2(st, m2P);
+    if (!L1) load_l1(dlo, dir_at(st * ST * 32 + ST * 32), wP);
+  }
   for (; st < nsuper; st += nwarps) {
-    const int64_t dfirst = dir_at(st * ST * 32);  // first deep row of the super-tile
-    const int64_t nxt_b0 = (st + nwarps) * ST * 32;
-    const bool has_next = st + nwarps < nsuper;
+    const int64_t sn = st + nwarps;
+    const bool has_next = sn < nsuper;
+    const int64_t nxt_b0 = sn * ST * 32;
+    int64_t nlo = 0, nhi = 0;
+    if (has_next) {
+      nlo = dir_at(nxt_b0);
+      if (!L1) nhi = dir_at(nxt_b0 + ST * 32);
+    }
     uint32_t rs[ST], m2s[ST];
     int offs[ST];
     int soff = 0;  // deep rows of this super-tile so far
-    // first tile's bytes (L2-prefetched by the previous super-tile); not held
-    // in registers across phases 2-3
-    if (L1) fetch(st * ST * 32 + lane, wN, m2N, true);
+    // first tile's bytes (L2-prefetched by the previous super-tile)
+    if (L1) fetch(st * ST * 32 + lane, wN, m2s[0], true);
     // ---------------- phase 1: shallow rows (lane = row block)
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
       const int64_t tile = st * ST + u;
       const int64_t b = tile * 32 + lane;
-      uint32_t w[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = wN[i];
-      const uint32_t m2 = m2N;
-      const int64_t ntile = (u + 1 < ST) ? tile + 1 : (st + nwarps) * ST;
-      fetch(ntile * 32 + lane, wN, m2N, u + 1 < ST);  // zeros past the column
+      const uint32_t m2 = m2P[u];
       uint32_t res = 0;
       if (L1) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = wN[i];
+        uint32_t unused;
+        if (u + 1 < ST) fetch(b + 32, wN, unused, true);
         const uint32_t valid =
             tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
         uint32_t P, Q;
@@ -224,27 +256,36 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       l2_prefetch(d.bs1 + nxt_b0 * 32, (uint32_t)(nblk * 32));
     }
     // ---------------- phase 2: deep rows (lane = deep block)
-    const int64_t db0 = dfirst >> 5;
-    const int sh0 = (int)(dfirst & 31);
+    const int64_t db0 = dlo >> 5;
+    const int sh0 = (int)(dlo & 31);
     const int ndt = (sh0 + soff + 31) >> 5;
     for (int t0 = 0; t0 < ndt; t0 += 32) {
       const int t = t0 + lane;
       const bool has = t < ndt;
       const int64_t dbk = db0 + t;
+      // (the L1 variant's registers go to phase 1: no level-1 prefetch there)
+      const uint32_t* pre = (!L1 && t0 == 0) ? wP : nullptr;
       uint32_t zA = has ? kFull : 0u, zB = (BETWEEN && has) ? kFull : 0u;
       uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
       if (UNR) {
 #pragma unroll
         for (int j = 1; j <= kMaxLevels; ++j)
-          if (j > maxlen || !ds_level<BETWEEN>(a, j, dbk, zA, zB, gtA, eqA, gtB, eqB)) break;
+          if (j > maxlen ||
+              !ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB))
+            break;
       } else {
 #pragma unroll 1
         for (int j = 1; j <= maxlen; ++j)
-          if (!ds_level<BETWEEN>(a, j, dbk, zA, zB, gtA, eqA, gtB, eqB)) break;
+          if (!ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB)) break;
       }
       if (has) rd[t] = BETWEEN ? ((gtA | eqA) & ~gtB) : finalize_op(A.op, gtA, eqA, kFull);
     }
     if (lane == 0) rd[ndt] = 0u;  // guard word of the last window
+    if (has_next) {
+      load_m2(sn, m2P);
+      if (!L1) load_l1(nlo, nhi, wP);
+    }
+    dlo = nlo;
     __syncwarp();
     // ---------------- phase 3: deep results back to row space (lane = row block)
 #pragma unroll
@@ -322,7 +363,7 @@ static int tune(int i) {
   if (g_tune[i] < 0) {
     static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
                                             "BSB_DS_UNROLL", "BSB_BS_SPARSE1"};
-    static const int dflt[kTunes] = {1, 6, 0, 1, 2};
+    static const int dflt[kTunes] = {1, 3, 0, 1, 2};
     const char* e = std::getenv(env[i]);
     g_tune[i] = e ? std::atoi(e) : dflt[i];
   }
