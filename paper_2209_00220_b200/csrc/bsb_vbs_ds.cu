@@ -24,8 +24,10 @@
 // The L1 variant prefetches the next super-tile's first-slice bytes into L2
 // (cp.async.bulk.prefetch) instead of holding them in registers across
 // phases 2-3.  (Measured and dropped: L2 prefetch of the next super-tile's
-// deep levels, and requesting level j+1 together with level j -- neither
-// moved the time.)
+// deep levels, requesting level j+1 together with level j, 5-6 CTAs/SM at
+// 40-48 registers, and cp.async staging of deep levels 1-4 into shared
+// memory one super-tile ahead -- none moved the time by more than the
+// run-to-run noise: the kernel is issue-bound, not load-latency-bound.)
 // Unmasked scans only; masked scans (conjunction chains) use the SLICED
 // kernel, which skips the loads of masked-out blocks.
 #include <cstdlib>
