@@ -137,7 +137,8 @@ typedef struct bsb_column_ref {
 /* ----------------------------------------------------------------- misc */
 const char* bsb_version(void);
 /* Run-time tuning knobs of the PP-VBS deep-row-space scan (benchmarks and
- * experiments; never changes results): "ds_enable" (0/1), "ds_serial"
+ * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
+ * scans only), "ds_serial"
  * (warp-cooperative pdep up to this many blocks per tile), "ds_tiles" (tiles
  * per super-tile, 0 = auto), "ds_unroll" (0/1).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);

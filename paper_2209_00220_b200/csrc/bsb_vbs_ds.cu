@@ -52,6 +52,7 @@ struct DsArgs {
   uint32_t cP, cQ, inv;
   VbsDesc d;
   Leg A, B;
+  const uint32_t* mask;  // input mask words (MASKED variant)
   uint32_t* out;
   unsigned long long* count;
 };
@@ -145,11 +146,19 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
   return true;
 }
 
-template <bool BETWEEN, bool L1, int ST, bool UNR>
+// MASKED: rows outside the input mask are dropped from the shallow result and
+// from the deposited deep results; a deep block is scanned only when a row
+// block with masked-in deep rows overlaps it (block-granular: the deep block's
+// unmasked rows are compared too, without changing any result), and the
+// first-slice bytes of fully masked-out row blocks are not loaded.
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
+  constexpr int kLive = (kRd + 31) / 32;
   __shared__ uint32_t rd_all[kDsWarps][kRd];
+  __shared__ uint32_t live_all[kDsWarps][MASKED ? kLive : 1];
   uint32_t* rd = rd_all[threadIdx.x >> 5];
+  uint32_t* live = live_all[threadIdx.x >> 5];  // MASKED: deep blocks to scan
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -183,11 +192,12 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   // directory bounds are requested at the top of an iteration, its M_2 words
   // and level-1 deep sectors right after phase 2, so that phase 3 and the
   // next phase 1 cover their latency.
-  auto load_m2 = [&](int64_t s, uint32_t (&m)[ST]) {
+  auto load_m2 = [&](int64_t s, uint32_t (&m)[ST], uint32_t (&mk)[ST]) {
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
       const int64_t b = (s * ST + u) * 32 + lane;
       m[u] = b < a.nb ? __ldg(d.exist[1] + b) : 0u;
+      if (MASKED) mk[u] = b < a.nb ? __ldg(a.mask + b) : 0u;
     }
   };
   auto load_l1 = [&](int64_t lo, int64_t hi, uint32_t (&w)[8]) {
@@ -201,11 +211,11 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   };
 
   int64_t st = warp;
-  uint32_t m2P[ST], wP[8], wN[8];
+  uint32_t m2P[ST], mP[ST], wP[8], wN[8];
   int64_t dlo = 0;
   if (st < nsuper) {
     dlo = dir_at(st * ST * 32);
-    load_m2(st, m2P);
+    load_m2(st, m2P, mP);
     if (!L1) load_l1(dlo, dir_at(st * ST * 32 + ST * 32), wP);
   }
   for (; st < nsuper; st += nwarps) {
@@ -217,26 +227,46 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       nlo = dir_at(nxt_b0);
       if (!L1) nhi = dir_at(nxt_b0 + ST * 32);
     }
-    uint32_t rs[ST], m2s[ST];
+    uint32_t rs[ST], m2s[ST], vs[ST];
     int offs[ST];
     int soff = 0;  // deep rows of this super-tile so far
+    const int sh0 = (int)(dlo & 31);
+    if (MASKED) {
+      if (lane < kLive) live[lane] = 0u;
+      __syncwarp();
+    }
     // first tile's bytes (L2-prefetched by the previous super-tile)
-    if (L1) fetch(st * ST * 32 + lane, wN, m2s[0], true);
+    if (L1) {
+      if (!MASKED || mP[0]) {
+        fetch(st * ST * 32 + lane, wN, m2s[0], true);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) wN[i] = 0;
+      }
+    }
     // ---------------- phase 1: shallow rows (lane = row block)
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
       const int64_t tile = st * ST + u;
       const int64_t b = tile * 32 + lane;
       const uint32_t m2 = m2P[u];
+      uint32_t valid =
+          tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
+      if (MASKED) valid &= mP[u];
       uint32_t res = 0;
       if (L1) {
         uint32_t w[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i] = wN[i];
         uint32_t unused;
-        if (u + 1 < ST) fetch(b + 32, wN, unused, true);
-        const uint32_t valid =
-            tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
+        if (u + 1 < ST) {
+          if (!MASKED || mP[u + 1]) {
+            fetch(b + 32, wN, unused, true);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) wN[i] = 0;
+          }
+        }
         uint32_t P, Q;
         if (a.cQ)
           thr_cmp<true>(w, a.cP, a.cQ, P, Q);
@@ -246,10 +276,17 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       }
       rs[u] = res;
       m2s[u] = m2;
+      if (MASKED) vs[u] = valid;
       const int c2 = __popc(m2);
       const uint32_t incl = lane_incl_scan((uint32_t)c2, lane);
       offs[u] = soff + (int)(incl - (uint32_t)c2);
       soff += (int)__shfl_sync(kFull, incl, 31);
+      if (MASKED && (valid & m2)) {  // deep blocks holding this block's masked-in deep rows
+        const int o = sh0 + offs[u];
+        const int lo = o >> 5, hi = (o + c2 - 1) >> 5;
+        atomicOr(&live[lo >> 5], 1u << (lo & 31));
+        if (hi != lo) atomicOr(&live[hi >> 5], 1u << (hi & 31));
+      }
     }
     // next super-tile's first-slice bytes -> L2 (its first tile is loaded at
     // the top of the next iteration)
@@ -259,15 +296,16 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     }
     // ---------------- phase 2: deep rows (lane = deep block)
     const int64_t db0 = dlo >> 5;
-    const int sh0 = (int)(dlo & 31);
     const int ndt = (sh0 + soff + 31) >> 5;
+    if (MASKED) __syncwarp();
     for (int t0 = 0; t0 < ndt; t0 += 32) {
       const int t = t0 + lane;
       const bool has = t < ndt;
       const int64_t dbk = db0 + t;
       // (the L1 variant's registers go to phase 1: no level-1 prefetch there)
       const uint32_t* pre = (!L1 && t0 == 0) ? wP : nullptr;
-      uint32_t zA = has ? kFull : 0u, zB = (BETWEEN && has) ? kFull : 0u;
+      const bool go = has && (!MASKED || ((live[t >> 5] >> (t & 31)) & 1u));
+      uint32_t zA = go ? kFull : 0u, zB = (BETWEEN && go) ? kFull : 0u;
       uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
       if (UNR) {
 #pragma unroll
@@ -284,7 +322,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     }
     if (lane == 0) rd[ndt] = 0u;  // guard word of the last window
     if (has_next) {
-      load_m2(sn, m2P);
+      load_m2(sn, m2P, mP);
       if (!L1) load_l1(nlo, nhi, wP);
     }
     dlo = nlo;
@@ -314,7 +352,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
           }
         }
       }
-      const uint32_t res = rs[u] | e;
+      const uint32_t res = rs[u] | (MASKED ? (e & vs[u]) : e);
       if (b < a.nb) a.out[b] = res;
       cnt += __popc(res);
     }
@@ -325,9 +363,9 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool L1, int ST, bool UNR>
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false>
 static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR>;
+  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, MASKED>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -340,6 +378,15 @@ static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 
+template <bool BETWEEN, bool L1>
+static int launch_ds_masked(const DsArgs& a, int st, cudaStream_t s) {
+  switch (st) {
+    case 1: return launch_ds_k<BETWEEN, L1, 1, true, true>(a, s);
+    case 2: return launch_ds_k<BETWEEN, L1, 2, true, true>(a, s);
+    case 3: return launch_ds_k<BETWEEN, L1, 3, true, true>(a, s);
+    default: return launch_ds_k<BETWEEN, L1, 4, true, true>(a, s);
+  }
+}
 template <bool BETWEEN, bool L1, bool UNR>
 static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
@@ -351,6 +398,7 @@ static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
 }
 template <bool BETWEEN, bool L1>
 static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
+  if (a.mask) return launch_ds_masked<BETWEEN, L1>(a, st, s);
   return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
 }
 
@@ -371,14 +419,15 @@ static int tune(int i) {
   }
   return g_tune[i];
 }
-bool ds_enabled() { return tune(0) != 0; }
+// ds_enable: 0 off, 1 all scans, 2 unmasked scans only
+bool ds_enabled(bool masked) { return masked ? tune(0) == 1 : tune(0) != 0; }
 int bs_sparse1() { return tune(4) - 1; }  // knob 0 = always the SWAR compares
 
 static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 
-// Unmasked scan of a SLICED column that carries deep[0] (K >= 2).
+// Scan of a SLICED column that carries deep[0] (K >= 2), optionally masked.
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
-                const Leg& A, const Leg& B, bool between, uint32_t* out,
+                const Leg& A, const Leg& B, bool between, const uint32_t* mask, uint32_t* out,
                 unsigned long long* count, cudaStream_t s) {
   DsArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -393,6 +442,7 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.d = d;
   a.A = A;
   a.B = B;
+  a.mask = mask;
   a.out = out;
   a.count = count;
   // tiles per super-tile: about 28 deep blocks per phase-2 pass

@@ -264,7 +264,8 @@ def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
 
 
 def test_vbs_sliced_deep_space_scan_vs_oracle():
-    """Unmasked scans of SLICED columns run in deep-row space (deep[0]).
+    """Scans of SLICED columns run in deep-row space (deep[0]), with and
+    without input masks.
     Code bytes from a small alphabet with 0x00 / 0xFF (the compare shortcuts)
     and many ties; literals of every length 1..K, present or not; every op and
     BETWEEN with lo/hi bytes in either order below the first level (both the
@@ -290,23 +291,32 @@ def test_vbs_sliced_deep_space_scan_vs_oracle():
             bs[-1] |= np.uint64(1)
             return sum(int(b) << (8 * (ll - 1 - i)) for i, b in enumerate(bs)), ll
 
+        # masks: dense, sparse, and whole 32-row blocks / 1024-row tiles masked out
+        dense = O.bools_to_words(rng.random(n) < 0.7)
+        sparse = O.bools_to_words(rng.random(n) < 0.02)
+        holes = O.bools_to_words((np.arange(n) // 1024) % 3 != 1)
+        masks = [None, dense, sparse, holes]
         for _ in range(6):
             c, ll = lit()
             for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
                 p = O.pred_compare(op, c, ll)
-                want, _ = O.vbs_scan(ocol, p)
-                bv, _ = B.scan_vbs(col, rp(list(p)))
-                assert np.array_equal(bv.words, want), (n, K, op, hex(c), ll)
-                assert bv.count() == O.words_count(want)
+                for m_o in masks:
+                    want, _ = O.vbs_scan(ocol, p, m_o)
+                    bv, _ = B.scan_vbs(col, rp(list(p)),
+                                       None if m_o is None else B.ResultBitVector(n, m_o))
+                    assert np.array_equal(bv.words, want), (n, K, op, hex(c), ll)
+                    assert bv.count() == O.words_count(want)
             c2, l2 = lit()
             if K >= 2 and rng.random() < 0.5:  # share the first byte (no level-1 pass)
                 c2 = (c >> (8 * (ll - 1)) << (8 * (l2 - 1))) | (c2 & ((1 << (8 * (l2 - 1))) - 1))
             for lo, hi in (((c, ll), (c2, l2)), ((c2, l2), (c, ll))):
                 p = O.pred_between(lo[0], lo[1], hi[0], hi[1])
-                want, _ = O.vbs_scan(ocol, p)
-                bv, _ = B.scan_vbs(col, rp(list(p)))
-                assert np.array_equal(bv.words, want), (n, K, hex(lo[0]), hex(hi[0]))
-                assert bv.count() == O.words_count(want)
+                for m_o in masks:
+                    want, _ = O.vbs_scan(ocol, p, m_o)
+                    bv, _ = B.scan_vbs(col, rp(list(p)),
+                                       None if m_o is None else B.ResultBitVector(n, m_o))
+                    assert np.array_equal(bv.words, want), (n, K, hex(lo[0]), hex(hi[0]))
+                    assert bv.count() == O.words_count(want)
 
 
 @pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
