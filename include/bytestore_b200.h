@@ -123,6 +123,11 @@ typedef struct bsb_vbs {
   const int64_t* block_dir[BSB_MAX_LEVELS];
   int64_t deep_len[BSB_MAX_LEVELS];
   const uint32_t* rexist[BSB_MAX_LEVELS];
+  /* Range of the first byte over the deep rows (a zone map; SLICED with
+   * deep[0]).  deep1_min == deep1_max lets scans settle level 1 of every deep
+   * row without reading deep[0]; deep1_min > deep1_max = unknown. */
+  int32_t deep1_min;
+  int32_t deep1_max;
 } bsb_vbs;
 
 /* One column reference for bsb_conj_scan (engine.py:322-332). */
@@ -140,7 +145,9 @@ const char* bsb_version(void);
  * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
  * scans only), "ds_serial"
  * (warp-cooperative pdep up to this many blocks per tile), "ds_tiles" (tiles
- * per super-tile, 0 = auto), "ds_unroll" (0/1).  Unknown key: BSB_EINVAL. */
+ * per super-tile, 0 = auto), "ds_unroll" (0/1), "bs_sparse1" (ByteSlice BETWEEN
+ * level-1 ties found row by row up to value-1 rows per block), "ds_zonemap"
+ * (0/1: settle level 1 from deep1_min/max).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

@@ -44,7 +44,8 @@ class BsbVbs(ctypes.Structure):
     _fields_ = [("n_rows", c_int64), ("stride", c_int64), ("max_len", c_int32),
                 ("deep_mode", c_int32), ("bs1", c_void_p), ("deep", c_void_p * MAX_LEVELS),
                 ("exist", c_void_p * MAX_LEVELS), ("block_dir", c_void_p * MAX_LEVELS),
-                ("deep_len", c_int64 * MAX_LEVELS), ("rexist", c_void_p * MAX_LEVELS)]
+                ("deep_len", c_int64 * MAX_LEVELS), ("rexist", c_void_p * MAX_LEVELS),
+                ("deep1_min", c_int32), ("deep1_max", c_int32)]
 
 
 class BsbDecode(ctypes.Structure):

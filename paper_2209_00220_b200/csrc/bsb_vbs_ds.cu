@@ -50,6 +50,10 @@ struct DsArgs {
   // carry constants (256 - t) * 0x00010001 (t = 256 -> 0: never), cQ == 0
   // skips the Q compare.
   uint32_t cP, cQ, inv;
+  // Level 1 of the deep rows when they all share one first byte (zone map):
+  // d1 = 1, and the per-leg (gt, eq) masks are constants (kFull or 0).
+  int d1;
+  uint32_t d1gA, d1eA, d1gB, d1eB;
   VbsDesc d;
   Leg A, B;
   const uint32_t* mask;  // input mask words (MASKED variant)
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   if (st < nsuper) {
     dlo = dir_at(st * ST * 32);
     load_m2(st, m2P, mP);
-    if (!L1) load_l1(dlo, dir_at(st * ST * 32 + ST * 32), wP);
+    if (!L1 && !a.d1) load_l1(dlo, dir_at(st * ST * 32 + ST * 32), wP);
   }
   for (; st < nsuper; st += nwarps) {
     const int64_t sn = st + nwarps;
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     int64_t nlo = 0, nhi = 0;
     if (has_next) {
       nlo = dir_at(nxt_b0);
-      if (!L1) nhi = dir_at(nxt_b0 + ST * 32);
+      if (!L1 && !a.d1) nhi = dir_at(nxt_b0 + ST * 32);
     }
     uint32_t rs[ST], m2s[ST], vs[ST];
     int offs[ST];
@@ -307,15 +311,26 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       const bool go = has && (!MASKED || ((live[t >> 5] >> (t & 31)) & 1u));
       uint32_t zA = go ? kFull : 0u, zB = (BETWEEN && go) ? kFull : 0u;
       uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
+      int j0 = 1;
+      if (a.d1) {  // level 1 settled by the zone map: no deep[0] bytes read
+        vbs_transition(1, A.len, K, a.d1gA, a.d1eA, kFull, zA, gtA, eqA);
+        if (BETWEEN) {
+          vbs_transition(1, B.len, K, a.d1gB, a.d1eB, kFull, zB, gtB, eqB);
+          zB &= zA | gtA | eqA;
+        }
+        j0 = 2;
+      }
       if (UNR) {
 #pragma unroll
-        for (int j = 1; j <= kMaxLevels; ++j)
+        for (int j = 1; j <= kMaxLevels; ++j) {
+          if (j < j0) continue;
           if (j > maxlen ||
               !ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB))
             break;
+        }
       } else {
 #pragma unroll 1
-        for (int j = 1; j <= maxlen; ++j)
+        for (int j = j0; j <= maxlen; ++j)
           if (!ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB)) break;
       }
       if (has) rd[t] = BETWEEN ? ((gtA | eqA) & ~gtB) : finalize_op(A.op, gtA, eqA, kFull);
@@ -323,7 +338,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     if (lane == 0) rd[ndt] = 0u;  // guard word of the last window
     if (has_next) {
       load_m2(sn, m2P, mP);
-      if (!L1) load_l1(nlo, nhi, wP);
+      if (!L1 && !a.d1) load_l1(nlo, nhi, wP);
     }
     dlo = nlo;
     __syncwarp();
@@ -404,16 +419,17 @@ static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
 
 // Run-time tunables (bsb_tune): 0 enable, 1 serial pdep blocks, 2 tiles per
 // super-tile (0 = auto), 3 unrolled levels; 4 ByteSlice BETWEEN level-1
-// row-by-row ties up to (value - 1) inside rows per block (0 = never).
-constexpr int kTunes = 5;
-static int g_tune[kTunes] = {-1, -1, -1, -1, -1};
+// row-by-row ties up to (value - 1) inside rows per block (0 = never); 5
+// settle the deep rows' level 1 from the column's zone map (0/1).
+constexpr int kTunes = 6;
+static int g_tune[kTunes] = {-1, -1, -1, -1, -1, -1};
 static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles",
-                                              "ds_unroll", "bs_sparse1"};
+                                              "ds_unroll", "bs_sparse1", "ds_zonemap"};
 static int tune(int i) {
   if (g_tune[i] < 0) {
     static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
-                                            "BSB_DS_UNROLL", "BSB_BS_SPARSE1"};
-    static const int dflt[kTunes] = {1, 3, 0, 1, 2};
+                                            "BSB_DS_UNROLL", "BSB_BS_SPARSE1", "BSB_DS_ZONEMAP"};
+    static const int dflt[kTunes] = {1, 3, 0, 1, 2, 1};
     const char* e = std::getenv(env[i]);
     g_tune[i] = e ? std::atoi(e) : dflt[i];
   }
@@ -427,8 +443,9 @@ static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 
 // Scan of a SLICED column that carries deep[0] (K >= 2), optionally masked.
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
-                const Leg& A, const Leg& B, bool between, const uint32_t* mask, uint32_t* out,
-                unsigned long long* count, cudaStream_t s) {
+                int deep1_min, int deep1_max, const Leg& A, const Leg& B, bool between,
+                const uint32_t* mask, uint32_t* out, unsigned long long* count,
+                cudaStream_t s) {
   DsArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n_rows = n_rows;
@@ -445,6 +462,14 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.mask = mask;
   a.out = out;
   a.count = count;
+  if (deep1_min == deep1_max && deep1_min >= 0 && deep1_min < 256 && tune(5)) {
+    const uint32_t x = (uint32_t)deep1_min;
+    a.d1 = 1;
+    a.d1gA = x > A.byte[0] ? kFull : 0u;
+    a.d1eA = x == A.byte[0] ? kFull : 0u;
+    a.d1gB = x > B.byte[0] ? kFull : 0u;
+    a.d1eB = x == B.byte[0] ? kFull : 0u;
+  }
   // tiles per super-tile: about 28 deep blocks per phase-2 pass
   int st = st_env;
   if (st < 1 || st > 4) {

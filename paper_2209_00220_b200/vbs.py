@@ -42,6 +42,7 @@ class VbsColumn:
     level_rows: list                      # rows owning byte j (j = 1..K), reference counts
     deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED / DEEP_RANK2 / DEEP_PLANES (header)
     rexist: list = None                   # PLANES: deep-row bitmaps of byte j+1 (j>=2)
+    deep1_range: tuple = (1, 0)           # (min, max) first byte of the deep rows; (1, 0) unknown
     _desc: _lib.BsbVbs = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -51,6 +52,7 @@ class VbsColumn:
         d.max_len = self.max_len
         d.deep_mode = self.deep_mode
         d.bs1 = self.bs1.data_ptr()
+        d.deep1_min, d.deep1_max = self.deep1_range
         if self.deep and self.deep[0] is not None:  # SLICED: deep rows' first byte
             d.deep[0] = self.deep[0].data_ptr()
             d.deep_len[0] = self.deep[0].numel() - DEEP_PAD
@@ -198,7 +200,15 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
         exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
         need_dir = mode == _lib.DEEP_PACKED or j == 1
         bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev) if need_dir else None)
-    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode, rex)
+    d1 = (1, 0)
+    if deep[0] is not None and cnt2 > 0:
+        # zone map of the deep rows' first byte (lets scans skip deep[0])
+        lt = dl.to(torch.int64)
+        deep_rows = lt >= 2
+        first = (dc.view(torch.int64) >> (8 * (lt - 1))) & 0xFF
+        first = first[deep_rows]
+        d1 = (int(first.min().item()), int(first.max().item()))
+    col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode, rex, d1)
     _lib.check(lib.bsb_vbs_build(dc.data_ptr(), dl.data_ptr(), col.desc_ref, stream()),
                "build_vbs")
     return col

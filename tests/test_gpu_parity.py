@@ -319,6 +319,48 @@ def test_vbs_sliced_deep_space_scan_vs_oracle():
                     assert bv.count() == O.words_count(want)
 
 
+@pytest.mark.parametrize("x", [0x00, 0x80, 0xFF])
+def test_vbs_sliced_zone_map_uniform_first_byte(x):
+    """All deep rows share their first byte (PPE's right-most pointer in the
+    skewed columns): level 1 of the deep rows is settled from the column's
+    zone map.  Literals whose first byte is below, equal to and above it."""
+    rng = np.random.default_rng(77 + x)
+    n, K = 90_001, 5
+    lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+    byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+    byts[:, 0] |= np.uint64(1)
+    codes = np.zeros(n, np.uint64)
+    for k in range(8):
+        use = lens > k
+        codes[use] |= byts[use, k] << np.uint64(8 * k)
+    deep = lens >= 2
+    top = (lens.astype(np.uint64) - np.uint64(1)) * np.uint64(8)
+    codes[deep] = (codes[deep] & ~(np.uint64(0xFF) << top[deep])) | (np.uint64(x) << top[deep])
+    col = B.build_vbs(codes, lens, deep_mode="sliced")
+    assert col.deep1_range == (x, x)
+    ocol = O.vbs_build(codes, lens)
+    mw = O.bools_to_words(rng.random(n) < 0.5)
+    for r in rng.integers(0, n, size=8):
+        c, ll = int(codes[r]), int(lens[r])
+        for fb in {max(x - 1, 0), x, min(x + 1, 255)}:
+            c2 = (fb << (8 * (ll - 1))) | (c & ((1 << (8 * (ll - 1))) - 1))
+            for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                p = O.pred_compare(op, c2, ll)
+                for m_o in (None, mw):
+                    want, _ = O.vbs_scan(ocol, p, m_o)
+                    bv, _ = B.scan_vbs(col, rp(list(p)),
+                                       None if m_o is None else B.ResultBitVector(n, m_o))
+                    assert np.array_equal(bv.words, want), (x, op, hex(c2), ll)
+            r2 = int(rng.integers(0, n))
+            lo, hi = sorted([(c2 << (8 * (K - ll)), c2, ll),
+                             (int(codes[r2]) << (8 * (K - int(lens[r2]))), int(codes[r2]),
+                              int(lens[r2]))])
+            p = O.pred_between(lo[1], lo[2], hi[1], hi[2])
+            want, _ = O.vbs_scan(ocol, p)
+            bv, _ = B.scan_vbs(col, rp(list(p)))
+            assert np.array_equal(bv.words, want), (x, "BETWEEN")
+
+
 @pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
 def test_vbs_row_lookup_decode_vs_oracle(mode):
     n = 200_000
