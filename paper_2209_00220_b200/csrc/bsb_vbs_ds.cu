@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t lane_incl_scan(uint32_t v, int lane) {
 
 // One Alg. 3 level over the lane's deep block (vbs.py:258-284 in deep-row
 // space); false once no lane of the warp has a tied row left.
-template <bool BETWEEN>
+template <bool BETWEEN, bool DEADLEG>
 __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, const uint32_t* pre,
                                          uint32_t& zA, uint32_t& zB, uint32_t& gtA,
                                          uint32_t& eqA, uint32_t& gtB, uint32_t& eqB) {
@@ -141,7 +141,21 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
   // existence of byte j+1 among the deep rows (byte 2 always exists)
   const uint32_t nxt = j >= K ? 0u : (j == 1 ? kFull : (act ? __ldg(d.rexist[j] + dbk) : 0u));
   uint32_t gA, eA, gB, eB;
-  cmp_level<BETWEEN>(w, a.A, a.B, j - 1, gA, eA, gB, eB);
+  if (BETWEEN && DEADLEG && a.A.byte[j - 1] != a.B.byte[j - 1]) {
+    // a leg past its literal's last byte has no tied row left: no compare
+    // (compiled into the L1 kernels only: the extra compare bodies cost the
+    // other variants more than they save, measured)
+    const bool liveA = j <= a.A.len, liveB = j <= a.B.len;
+    if (liveA && liveB) {
+      cmp_level<true>(w, a.A, a.B, j - 1, gA, eA, gB, eB);
+    } else if (liveA) {
+      cmp_level<false>(w, a.A, a.A, j - 1, gA, eA, gB, eB);
+    } else {
+      cmp_level<false>(w, a.B, a.B, j - 1, gB, eB, gA, eA);
+    }
+  } else {
+    cmp_level<BETWEEN>(w, a.A, a.B, j - 1, gA, eA, gB, eB);
+  }
   vbs_transition(j, a.A.len, K, gA, eA, nxt, zA, gtA, eqA);
   if (BETWEEN) {
     vbs_transition(j, a.B.len, K, gB, eB, nxt, zB, gtB, eqB);
@@ -325,13 +339,13 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
         for (int j = 1; j <= kMaxLevels; ++j) {
           if (j < j0) continue;
           if (j > maxlen ||
-              !ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB))
+              !ds_level<BETWEEN, L1>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB))
             break;
         }
       } else {
 #pragma unroll 1
         for (int j = j0; j <= maxlen; ++j)
-          if (!ds_level<BETWEEN>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB)) break;
+          if (!ds_level<BETWEEN, L1>(a, j, dbk, pre, zA, zB, gtA, eqA, gtB, eqB)) break;
       }
       if (has) rd[t] = BETWEEN ? ((gtA | eqA) & ~gtB) : finalize_op(A.op, gtA, eqA, kFull);
     }
