@@ -534,7 +534,7 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
     from paper_2209_00220_b200.device import to_dev_u32
     from paper_2209_00220_b200.dictionary import freq_table_and_ranks
     from paper_2209_00220_b200.roofline import hbm_peak, lookup_alg_bytes_rows
-    from paper_2209_00220_b200.vbs import build_vbs
+    from paper_2209_00220_b200.vbs import build_vbs, lookup_vbs_rows_dec
 
     n = 1 << log2n
     m = 1 << (log2n - 4)
@@ -561,6 +561,7 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
     peak, _ = hbm_peak(ROOT)
     exist_v = [col_v.mask_words(j) for j in range(2, col_v.max_len + 1)]
     out = {}
+    gathered = {}
 
     def timed(fn):
         fn()
@@ -604,18 +605,15 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
                     col_v.desc_ref, dbits.dwords.data_ptr(), ctypes.byref(dec_v), None, None,
                     o32.data_ptr(), cnt.data_ptr(), stream())
             elif layout == "byteslice":
+                # public API: long unsorted id lists are gathered in row order
                 fn = lambda: lookup_byteslice_rows(col_b, drows)
             else:
-                o32i = torch.empty(drows.numel(), dtype=torch.int32, device="cuda")
-                errw = torch.zeros(1, dtype=torch.int32, device="cuda")
-                fn = lambda: lib.bsb_vbs_lookup_rows_dec(
-                    col_v.desc_ref, drows.data_ptr(), drows.numel(), ctypes.byref(dec_v), None,
-                    None, o32i.data_ptr(), errw.data_ptr(), stream())
+                fn = lambda: lookup_vbs_rows_dec(col_v, drows, dec_v, out_dtype=torch.int32)
             ms = timed(fn)
+            if not is_bits:
+                gathered[(layout, name)] = fn()
             if is_bits and int(cnt.item()) != nsel:
                 raise RuntimeError(f"{layout}/{name}: fused lookup count mismatch")
-            if not is_bits and layout == "ppvbs" and int(errw.item()) != 0:
-                raise RuntimeError("ppvbs lookup: code not in dictionary")
             K = col_b.n_slices if layout == "byteslice" else col_v.max_len
             ob = 8 if layout == "byteslice" else 4
             ab = lookup_alg_bytes_rows(
@@ -629,6 +627,14 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
                 "mrows_s": round(len(rows) / (ms * 1e-3) / 1e6, 1),
                 "alg_gbs": round(ab / (ms * 1e-3) / 1e9, 1),
                 "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4)}
+    # the unsorted-id gathers (sorted internally, scattered back) must equal
+    # the sorted-id gathers in input order
+    back = torch.from_numpy(np.argsort(ids, kind="stable")).cuda()
+    for layout in ("byteslice", "ppvbs"):
+        if (layout, "ids_unsorted") in gathered and (layout, "ids_sorted") in gathered:
+            if not torch.equal(gathered[(layout, "ids_unsorted")][back],
+                               gathered[(layout, "ids_sorted")]):
+                raise RuntimeError(f"{layout}: unsorted and sorted id lookups disagree")
     return out
 
 

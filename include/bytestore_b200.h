@@ -270,6 +270,20 @@ int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_i
                             const bsb_decode* dec, uint64_t* out_padded, int64_t* out_values,
                             int32_t* out_values32, uint32_t* err_dev, void* stream);
 
+/* ------------------------------------------------------- gather locality */
+/* A row-id list for a gather (cfg3's unsorted ids): if rows[] (n_ids ids of
+ * a column of n_rows rows) is not ascending, sorted_rows = the ids ordered by
+ * row bucket (at most 2^16 buckets of consecutive rows; input order inside a
+ * bucket) and perm[i] = the input position of sorted_rows[i]; a lookup of
+ * sorted_rows walks the column in order and bsb_scatter puts its output back
+ * in input order.  *was_sorted = 1 (outputs untouched) when the list is
+ * already ascending.  Syncs (the order check). */
+int bsb_rows_sort(const int64_t* rows, int64_t n_ids, int64_t n_rows, int64_t* sorted_rows,
+                  int64_t* perm, int32_t* was_sorted, void* stream);
+/* out[perm[i]] = in[i] for n elements of elem_bytes (4 or 8). */
+int bsb_scatter(const void* in, const int64_t* perm, int64_t n, int32_t elem_bytes, void* out,
+                void* stream);
+
 /* ------------------------------------------------------------ bitvectors */
 /* ResultBitVector.to_indices (bitvector.py:71-72): ascending int64 row ids of
  * the set bits into rows_out (capacity >= popcount); count written to

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import device, host_u64, stream, to_dev_i64, to_dev_u64
+from .device import device, gather_order, host_u64, scatter_back, stream, to_dev_i64, to_dev_u64
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
@@ -149,25 +149,30 @@ def scan_byteslice(col: ByteSliceColumn, pred: ResolvedPredicate, mask=None,
 
 
 def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=None,
-                          out_dtype=torch.int64):
-    """Device lookup of a row-id list (any order).  Returns codes, or decoded
-    values rank_values[code] when a device value table is given."""
+                          out_dtype=torch.int64, order: str = "auto"):
+    """Device lookup of a row-id list (any order, duplicates allowed; output
+    in input order).  Returns codes, or decoded values rank_values[code] when
+    a device value table is given.  order="sort" gathers a long unsorted list
+    in row order and scatters the output back (device.gather_order); "auto"
+    is "keep" for ByteSlice: K random sectors per id cost less than the sort
+    and the scatter (measured)."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
+    g, perm = gather_order(rows, col.n_rows, "keep" if order == "auto" else order)
     if rank_values is None:
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
-        _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, rows.data_ptr(), n,
+        _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n,
                                                  out.data_ptr(), None, None, None, stream()),
                    "lookup_byteslice")
-        return out
+        return scatter_back(out, perm)
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
-    _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, rows.data_ptr(), n, None,
+    _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n, None,
                                              rank_values.data_ptr(), p64, p32, stream()),
                "lookup_byteslice")
-    return out
+    return scatter_back(out, perm)
 
 
 def lookup_byteslice_bits(col: ByteSliceColumn, selection, decoder=None,

@@ -78,3 +78,40 @@ def host_u32(t: torch.Tensor) -> np.ndarray:
 
 def host_u64(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy().view(np.uint64)
+
+
+# Row-id gathers: lists at least this long that are not ascending are sorted
+# before the lookup and the output is scattered back (bsb_rows_sort).
+SORT_GATHER_MIN = 1 << 16
+
+
+def gather_order(rows: torch.Tensor, n_rows: int, order: str = "auto"):
+    """(ids to gather, perm or None).  order="sort": an ascending list is
+    gathered as it is, any other list of >= SORT_GATHER_MIN ids in row-bucket
+    order with perm mapping back to input positions (bsb_rows_sort); "keep":
+    as given.  The lookups choose per layout what "auto" means."""
+    import ctypes
+
+    if order not in ("sort", "keep"):
+        raise ValueError(f"unknown order {order!r}")
+    n = rows.numel()
+    if order == "keep" or n < SORT_GATHER_MIN:
+        return rows, None
+    lib = _lib.load()
+    srt = torch.empty_like(rows)
+    perm = torch.empty_like(rows)
+    was = ctypes.c_int32(1)
+    _lib.check(lib.bsb_rows_sort(rows.data_ptr(), n, int(n_rows), srt.data_ptr(),
+                                 perm.data_ptr(), ctypes.byref(was), stream()), "gather_order")
+    return (rows, None) if was.value else (srt, perm)
+
+
+def scatter_back(out: torch.Tensor, perm) -> torch.Tensor:
+    """Output of a gather over sorted ids back in input order."""
+    if perm is None:
+        return out
+    res = torch.empty_like(out)
+    _lib.check(_lib.load().bsb_scatter(out.data_ptr(), perm.data_ptr(), out.numel(),
+                                       out.element_size(), res.data_ptr(), stream()),
+               "scatter_back")
+    return res

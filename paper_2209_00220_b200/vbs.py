@@ -17,7 +17,8 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import device, host_u32, host_u64, stream, to_dev_i64, to_dev_u8, to_dev_u64
+from .device import (device, gather_order, host_u32, host_u64, scatter_back, stream, to_dev_i64,
+                     to_dev_u8, to_dev_u64)
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
@@ -270,43 +271,56 @@ def scan_vbs(col: VbsColumn, pred: ResolvedPredicate, mask=None, threads: int = 
         lambda: _scan_stats(col, pred, m))
 
 
+def _vbs_order(col: VbsColumn, order: str) -> str:
+    if order == "auto":
+        return "sort" if col.max_len >= 3 else "keep"
+    return order
+
+
 def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
-                    out_dtype=torch.int64, level_counts=None):
-    """Device lookup of a row-id list: padded codes, or decoded values when
-    the dictionary's sorted padded codes / values are given."""
+                    out_dtype=torch.int64, level_counts=None, order: str = "auto"):
+    """Device lookup of a row-id list (any order, output in input order):
+    padded codes, or decoded values when the dictionary's sorted padded codes
+    / values are given.  order: see lookup_byteslice_rows; "auto" sorts for
+    columns with codes of 3+ bytes (a deep row costs up to ~2K random
+    sectors: bs1, existence words, directory, deep bytes)."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
+    g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order))
     lc = None if level_counts is None else level_counts.data_ptr()
     if sorted_padded is None:
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
-        _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, rows.data_ptr(), n, out.data_ptr(),
+        _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, g.data_ptr(), n, out.data_ptr(),
                                            None, None, 0, None, None, lc, stream()),
                    "lookup_vbs")
-        return out
+        return scatter_back(out, perm)
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
-    _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, rows.data_ptr(), n, None,
+    _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, g.data_ptr(), n, None,
                                        sorted_padded.data_ptr(), dict_values.data_ptr(),
                                        sorted_padded.numel(), p64, p32, lc, stream()),
                "lookup_vbs")
-    return out
+    return scatter_back(out, perm)
 
 
-def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64):
-    """Row-id lookup decoded through a C-ABI decoder (Dictionary.dev_decoder)."""
+def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64,
+                        order: str = "auto"):
+    """Row-id lookup decoded through a C-ABI decoder (Dictionary.dev_decoder).
+    order: see lookup_vbs_rows."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
+    g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order))
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
-    _lib.check(lib.bsb_vbs_lookup_rows_dec(col.desc_ref, rows.data_ptr(), n,
+    _lib.check(lib.bsb_vbs_lookup_rows_dec(col.desc_ref, g.data_ptr(), n,
                                            ctypes.byref(decoder), None, p64, p32, None,
                                            stream()),
                "lookup_vbs")
-    return out
+    return scatter_back(out, perm)
 
 
 def lookup_vbs_bits(col: VbsColumn, selection, decoder=None, out_dtype=torch.int64):

@@ -149,6 +149,38 @@ def test_byteslice_row_lookup_unsorted_duplicates():
     assert np.array_equal(vals, table.cpu().numpy()[codes[rows].astype(np.int64)])
 
 
+def test_row_lookups_sorted_gather():
+    """Long unsorted id lists (>= device.SORT_GATHER_MIN) are gathered in row
+    order and scattered back: output in input order, duplicates, both
+    layouts, codes and decoded values, and the order="keep" path."""
+    from paper_2209_00220_b200.device import SORT_GATHER_MIN
+    rng = np.random.default_rng(8)
+    n = 300_007
+    ids = rng.integers(0, n, size=max(2 * SORT_GATHER_MIN, 150_000))
+    ids[:1000] = ids[1000:2000]  # duplicates
+    codes = rng.integers(0, 1 << 20, size=n, dtype=np.uint64)
+    col = B.build_byteslice(codes, 20)
+    for order in ("auto", "keep", "sort"):
+        got = B.lookup_byteslice_rows(col, torch.from_numpy(ids), order=order).cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), codes[ids]), order
+    got = B.lookup_byteslice_rows(col, torch.from_numpy(np.sort(ids))).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), codes[np.sort(ids)])
+    vals, od, vcodes, lens = _ppe_column(1.1, 16, n, 9)
+    vcol = B.build_vbs(vcodes, lens)
+    K = vcol.max_len
+    padded = vcodes << (np.uint64(8) * (np.uint64(K) - lens.astype(np.uint64)))
+    assert K >= 3  # "auto" sorts
+    for order in ("auto", "keep"):
+        got = B.lookup_vbs_rows(vcol, torch.from_numpy(ids), order=order).cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), padded[ids]), order
+    d = B.Dictionary.build(B.build_frequency_table(vals, B.ColumnKind.NUMERIC),
+                           "prefix_preserving")
+    assert np.array_equal(d.row_codes(d.encode_rows(vals))[0], vcodes)
+    got = B.lookup_vbs_rows_dec(vcol, torch.from_numpy(ids), d.dev_decoder,
+                                out_dtype=torch.int32).cpu().numpy()
+    assert np.array_equal(got, vals[ids].astype(np.int32))
+
+
 def test_byteslice_errors():
     with pytest.raises(ValueError):
         B.build_byteslice([], 8)
