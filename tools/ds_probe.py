@@ -61,6 +61,9 @@ def main(settings, reps=20, log2n=28, layout="ppvbs"):
 
 if __name__ == "__main__":
     args = sys.argv[1:]
+    if args and args[0].startswith("--lib="):  # A/B against another build of the library
+        _lib.load(args[0][len("--lib="):])
+        args = args[1:]
     layout = "ppvbs"
     if args and args[0] in ("ppvbs", "byteslice"):
         layout, args = args[0], args[1:]
