@@ -82,16 +82,13 @@ __device__ __forceinline__ void thr_cmp(const uint32_t (&w)[8], uint32_t cP, uin
   Q = TWO ? q : 0u;
 }
 
-#ifndef BSB_DS_ZERO_BYTES
-#define BSB_DS_ZERO_BYTES 1
-#endif
-constexpr bool kZeroBytes = BSB_DS_ZERO_BYTES;  // literal byte 0x00 shortcut (experiment switch)
-
+// (A literal byte 0x00 shortcut -- gt-only compares -- measured 15-20 %
+// slower: the extra compare bodies cost more than the carries they save.)
 // (gt, eq) of both legs at level index j0 (0-based).  One literal byte 0xFF
 // (PPE's right-most pointer slot) needs only the equality carries; two
 // different bytes take the four-compare form (whose constants already give
 // gt = 0 for 0xFF and ge = all for 0x00).
-template <bool BETWEEN, bool ZB = kZeroBytes>
+template <bool BETWEEN>
 __device__ __forceinline__ void cmp_level(const uint32_t (&w)[8], const Leg& A, const Leg& B,
                                           int j0, uint32_t& gA, uint32_t& eA, uint32_t& gB,
                                           uint32_t& eB) {
@@ -99,9 +96,7 @@ __device__ __forceinline__ void cmp_level(const uint32_t (&w)[8], const Leg& A, 
   if (!BETWEEN || A.byte[j0] == B.byte[j0]) {
     uint32_t ge;
     if (la.cgt == 0u) {
-      cmp_block_vbs(w, la, gA, ge);  // 0xFF: equality only
-    } else if (ZB && A.byte[j0] == 0u) {
-      cmp_block_z(w, la, gA, ge);    // 0x00: greater-than only
+      cmp_block_vbs(w, la, gA, ge);  // equality only
     } else {
       cmp_block(w, la, gA, ge);
     }
@@ -110,10 +105,7 @@ __device__ __forceinline__ void cmp_level(const uint32_t (&w)[8], const Leg& A, 
     eB = eA;
   } else {
     uint32_t geA, geB;
-    if (ZB && A.byte[j0] == 0u)
-      cmp_block2_z(w, la, B.lv[j0], gA, geA, gB, geB);  // lo byte 0x00: no >= lo carries
-    else
-      cmp_block2(w, la, B.lv[j0], gA, geA, gB, geB);
+    cmp_block2(w, la, B.lv[j0], gA, geA, gB, geB);
     eA = geA & ~gA;
     eB = geB & ~gB;
   }
