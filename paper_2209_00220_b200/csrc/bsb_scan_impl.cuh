@@ -141,17 +141,23 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
     const uint32_t inside = valid & geA & ~gtB;
     uint32_t eqA = 0, eqB = 0;
     if (__any_sync(kFull, __popc(inside) > sparse1)) {
+      // (re-splitting the sector here measured faster than holding the
+      // first split's 16 registers across the branch)
       uint32_t gtA, geB;
       cmp_thr2(in.w, A.lv[0].cgt, B.lv[0].cge, gtA, geB);
       eqA = geA & ~gtA;
       eqB = geB & ~gtB;
     } else {
       const uint32_t la = A.byte[0], lb = B.byte[0];
+      uint32_t wl[8];  // register copy: selects below, not a local-memory array
+#pragma unroll
+      for (int q = 0; q < 8; ++q) wl[q] = in.w[q];
       for (uint32_t rest = inside; rest; rest &= rest - 1) {
         const int r = __ffs(rest) - 1;
-        uint32_t x = in.w[0];
+        const int rq = r & 7;
+        uint32_t x = wl[0];
 #pragma unroll
-        for (int q = 1; q < 8; ++q) x = (r & 7) == q ? in.w[q] : x;
+        for (int q = 1; q < 8; ++q) x = rq == q ? wl[q] : x;
         const uint32_t by = (x >> ((r >> 3) << 3)) & 0xFFu, bit = 1u << r;
         eqA |= by == la ? bit : 0u;
         eqB |= by == lb ? bit : 0u;
