@@ -103,8 +103,9 @@ typedef struct bsb_byteslice {
  *             per deep block: bit i = deep row 32k+i has byte j+1.  Scanned with
  *             the ByteSlice SWAR compare, one lane per deep block.
  *             deep[0] (optional, SLICED only) holds byte 1 of every deep row
- *             in the same deep-block layout; when present, unmasked scans
- *             run entirely in deep-row space for the deep rows.
+ *             in the same deep-block layout; with it (or with a uniform
+ *             deep1_min == deep1_max zone map, which makes it unnecessary)
+ *             scans run entirely in deep-row space for the deep rows.
  * deep allocations are padded by >= 64 bytes.  Index 0 of exist/block_dir/
  * rexist is unused (level 1 is bs1); index 0 of deep is unused except as
  * above. */

@@ -349,6 +349,7 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
 
 namespace bsb {
 bool ds_enabled(bool masked);  // bsb_tune("ds_enable") / BSB_DS
+bool ds_zonemap_enabled();     // bsb_tune("ds_zonemap") / BSB_DS_ZONEMAP
 }
 
 // The cooperative plane scan needs every multi-byte literal to end in a
@@ -400,7 +401,8 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
       return K <= 5 ? scan_dispatch<1 + BSB_DEEP_PLANES>(a, pred, K, s)
                     : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
     case BSB_DEEP_SLICED:
-      if (K >= 2 && col->deep[0] && bsb::ds_enabled(mask != nullptr))
+      if (K >= 2 && bsb::ds_enabled(mask != nullptr) &&
+          (col->deep[0] || (col->deep1_min == col->deep1_max && bsb::ds_zonemap_enabled())))
         return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], col->deep1_min,
                            col->deep1_max, a.A, a.B, pred->op == BSB_BETWEEN, mask, out_words,
                            a.count, s);

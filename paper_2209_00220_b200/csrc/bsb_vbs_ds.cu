@@ -453,6 +453,7 @@ static int tune(int i) {
 }
 // ds_enable: 0 off, 1 all scans, 2 unmasked scans only
 bool ds_enabled(bool masked) { return masked ? tune(0) == 1 : tune(0) != 0; }
+bool ds_zonemap_enabled() { return tune(5) != 0; }
 int bs_sparse1() { return tune(4) - 1; }  // knob 0 = always the SWAR compares
 
 static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }

@@ -178,7 +178,15 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
     bs1 = torch.empty(stride, dtype=torch.uint8, device=dev)
     deep, exist, bdir, rex = [None], [None], [None], [None]
     cnt2 = level_rows[1] if K >= 2 else 0
-    if mode == _lib.DEEP_SLICED:
+    d1 = (1, 0)
+    if mode == _lib.DEEP_SLICED and cnt2 > 0:
+        # zone map of the deep rows' first byte: when they all share it the
+        # deep-space scan settles their level 1 without reading any bytes
+        lt = dl.to(torch.int64)
+        first = ((dc >> (8 * (lt - 1))) & 0xFF)[lt >= 2]
+        d1 = (int(first.min().item()), int(first.max().item()))
+        del lt, first
+    if mode == _lib.DEEP_SLICED and d1[0] != d1[1]:
         # level 1 of the deep rows in deep-row space (deep-space scan kernel)
         deep[0] = torch.zeros(-(-cnt2 // 32) * 32 + DEEP_PAD, dtype=torch.uint8, device=dev)
     for j in range(1, K):
@@ -201,14 +209,6 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
         exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
         need_dir = mode == _lib.DEEP_PACKED or j == 1
         bdir.append(torch.empty(nbpad + 1, dtype=torch.int64, device=dev) if need_dir else None)
-    d1 = (1, 0)
-    if deep[0] is not None and cnt2 > 0:
-        # zone map of the deep rows' first byte (lets scans skip deep[0])
-        lt = dl.to(torch.int64)
-        deep_rows = lt >= 2
-        first = (dc.view(torch.int64) >> (8 * (lt - 1))) & 0xFF
-        first = first[deep_rows]
-        d1 = (int(first.min().item()), int(first.max().item()))
     col = VbsColumn(n, K, lanes, stride, bs1, deep, exist, bdir, level_rows, mode, rex, d1)
     _lib.check(lib.bsb_vbs_build(dc.data_ptr(), dl.data_ptr(), col.desc_ref, stream()),
                "build_vbs")

@@ -370,6 +370,7 @@ def test_vbs_sliced_zone_map_uniform_first_byte(x):
     codes[deep] = (codes[deep] & ~(np.uint64(0xFF) << top[deep])) | (np.uint64(x) << top[deep])
     col = B.build_vbs(codes, lens, deep_mode="sliced")
     assert col.deep1_range == (x, x)
+    assert col.deep[0] is None  # the zone map makes the level-1 plane unnecessary
     ocol = O.vbs_build(codes, lens)
     mw = O.bools_to_words(rng.random(n) < 0.5)
     for r in rng.integers(0, n, size=8):
@@ -383,6 +384,17 @@ def test_vbs_sliced_zone_map_uniform_first_byte(x):
                     bv, _ = B.scan_vbs(col, rp(list(p)),
                                        None if m_o is None else B.ResultBitVector(n, m_o))
                     assert np.array_equal(bv.words, want), (x, op, hex(c2), ll)
+            if fb == x:  # without the zone map the row-space kernel serves the column
+                B.scan_vbs(col, rp(list(O.pred_compare("EQ", c2, ll))))
+                lib = B._lib.load()
+                assert lib.bsb_tune(b"ds_zonemap", 0) == 0
+                try:
+                    p = O.pred_compare("GE", c2, ll)
+                    want, _ = O.vbs_scan(ocol, p)
+                    bv, _ = B.scan_vbs(col, rp(list(p)))
+                    assert np.array_equal(bv.words, want), (x, "no zone map")
+                finally:
+                    lib.bsb_tune(b"ds_zonemap", 1)
             r2 = int(rng.integers(0, n))
             lo, hi = sorted([(c2 << (8 * (K - ll)), c2, ll),
                              (int(codes[r2]) << (8 * (K - int(lens[r2]))), int(codes[r2]),
