@@ -144,11 +144,10 @@ typedef struct bsb_column_ref {
 const char* bsb_version(void);
 /* Run-time tuning knobs of the PP-VBS deep-row-space scan (benchmarks and
  * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
- * scans only), "ds_serial"
- * (warp-cooperative pdep up to this many blocks per tile), "ds_tiles" (tiles
- * per super-tile, 0 = auto), "ds_unroll" (0/1), "bs_sparse1" (ByteSlice BETWEEN
- * level-1 ties found row by row up to value-1 rows per block), "ds_zonemap"
- * (0/1: settle level 1 from deep1_min/max).  Unknown key: BSB_EINVAL. */
+ * scans only), "ds_serial" (warp-cooperative pdep up to this many blocks per
+ * tile), "ds_tiles" (tiles per super-tile, 0 = auto), "ds_unroll" (0/1),
+ * "ds_zonemap" (0/1: settle level 1 from deep1_min/max).  Unknown key:
+ * BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

@@ -8,7 +8,6 @@
 namespace bsb {
 
 constexpr int kScanThreads = 256;
-int bs_sparse1();  // bsb_tune("bs_sparse1") / BSB_BS_SPARSE1 (bsb_vbs_ds.cu)
 
 struct ScanArgs {
   int64_t n_rows;
@@ -24,7 +23,6 @@ struct ScanArgs {
   int8_t* depth;
   int32_t skipped_slot;
   int32_t depth_max;  // STATS: 1 = depth[b] = max(depth[b], d) (second BETWEEN leg)
-  int32_t sparse1;    // ByteSlice BETWEEN level 1: row-by-row ties up to this many per block
 };
 
 template <bool STATS>
@@ -112,8 +110,7 @@ __global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
     int depth = 0;
     uint32_t res;
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
-      res = scan_tile_bs<BETWEEN, STATS, L1Z>(a.bs, a.A, a.B, b, valid, in, &st, &depth,
-                                                a.sparse1);
+      res = scan_tile_bs<BETWEEN, STATS, L1Z>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
       res = scan_tile_vbs<BETWEEN, STATS, LAYOUT - 1>(a.vbs, a.A, a.B, tile, b, valid, in, &st,
                                                      &depth);
@@ -316,7 +313,6 @@ extern "C" int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred
   a.count = reinterpret_cast<unsigned long long*>(count);
   a.stats = stats;
   a.depth = depth;
-  a.sparse1 = bs_sparse1();
   return scan_dispatch<BSB_LAYOUT_BYTESLICE>(a, pred, K, s);
 }
 

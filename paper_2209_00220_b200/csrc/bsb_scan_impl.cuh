@@ -96,78 +96,16 @@ __device__ __forceinline__ void fetch_vbs(const VbsDesc& d, int64_t tile, int64_
 // levels >= 2 where every live block has at most this many tied rows compare
 // those rows' bytes one by one instead of the 32-byte SWAR compare
 constexpr int kSparseRows = 4;
-// level 1 of a BETWEEN: inside rows per block up to which the ties are found
-// row by row
-constexpr int kSparseRows1 = 1;
-
-// Two byte thresholds at once: P = [byte + cP carries], Q = [byte + cQ
-// carries] (LevelLit constants), lane masks in row order.
-__device__ __forceinline__ void cmp_thr2(const uint32_t (&w)[8], uint32_t cP, uint32_t cQ,
-                                         uint32_t& P, uint32_t& Q) {
-  uint32_t p = 0, q = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    p += __byte_perm(ev + cP, od + cP, 0x7351) << i;
-    q += __byte_perm(ev + cQ, od + cQ, 0x7351) << i;
-  }
-  P = p;
-  Q = q;
-}
 
 // L1Z: the (lo) literal's level-1 byte is 0x00 (host-selected variant).
 template <bool BETWEEN, bool STATS, bool L1Z = false>
 __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, const Leg& B,
                                                  int64_t b, uint32_t valid, const TileIn& in,
-                                                 StatAcc* st, int* depth_out,
-                                                 int sparse1 = kSparseRows1) {
+                                                 StatAcc* st, int* depth_out) {
   uint32_t zeqA = valid, zgtA = 0, zeqB = valid, zgtB = 0;
   int depth = 0;
   // level 1: every lane, branch free (invalid lanes carry zero state)
-  if (BETWEEN && !STATS && A.byte[0] != B.byte[0]) {
-    // Outer thresholds first: in = [lo byte <= x <= hi byte].  Rows outside
-    // are decided; inside, only the rows equal to a literal byte tie.  When
-    // every lane has at most kSparseRows1 inside rows (narrow windows), those
-    // rows' bytes are compared one by one instead of two more SWAR compares.
-    uint32_t geA, gtB;
-    if (L1Z) {
-      uint32_t dummy;
-      cmp_block_z(in.w, B.lv[0], gtB, dummy);  // x > hi byte; everything is >= 0x00
-      geA = kFull;
-    } else {
-      cmp_thr2(in.w, A.lv[0].cge, B.lv[0].cgt, geA, gtB);
-    }
-    const uint32_t inside = valid & geA & ~gtB;
-    uint32_t eqA = 0, eqB = 0;
-    if (__any_sync(kFull, __popc(inside) > sparse1)) {
-      // (re-splitting the sector here measured faster than holding the
-      // first split's 16 registers across the branch)
-      uint32_t gtA, geB;
-      cmp_thr2(in.w, A.lv[0].cgt, B.lv[0].cge, gtA, geB);
-      eqA = geA & ~gtA;
-      eqB = geB & ~gtB;
-    } else {
-      const uint32_t la = A.byte[0], lb = B.byte[0];
-      uint32_t wl[8];  // register copy: selects below, not a local-memory array
-#pragma unroll
-      for (int q = 0; q < 8; ++q) wl[q] = in.w[q];
-      for (uint32_t rest = inside; rest; rest &= rest - 1) {
-        const int r = __ffs(rest) - 1;
-        const int rq = r & 7;
-        uint32_t x = wl[0];
-#pragma unroll
-        for (int q = 1; q < 8; ++q) x = rq == q ? wl[q] : x;
-        const uint32_t by = (x >> ((r >> 3) << 3)) & 0xFFu, bit = 1u << r;
-        eqA |= by == la ? bit : 0u;
-        eqB |= by == lb ? bit : 0u;
-      }
-    }
-    zgtA = valid & geA & ~eqA;
-    zeqA = valid & eqA;
-    zgtB = valid & gtB;
-    zeqB = valid & eqB & (zeqA | zgtA);
-  } else {
+  {
     uint32_t gA, eA, gB, eB;
     if (BETWEEN && A.byte[0] != B.byte[0]) {
       if (L1Z)

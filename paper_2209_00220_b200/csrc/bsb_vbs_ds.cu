@@ -433,19 +433,18 @@ static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
   return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
 }
 
-// Run-time tunables (bsb_tune): 0 enable, 1 serial pdep blocks, 2 tiles per
-// super-tile (0 = auto), 3 unrolled levels; 4 ByteSlice BETWEEN level-1
-// row-by-row ties up to (value - 1) inside rows per block (0 = never); 5
-// settle the deep rows' level 1 from the column's zone map (0/1).
-constexpr int kTunes = 6;
-static int g_tune[kTunes] = {-1, -1, -1, -1, -1, -1};
+// Run-time tunables (bsb_tune): 0 enable (0 off, 1 all scans, 2 unmasked
+// only), 1 serial pdep blocks, 2 tiles per super-tile (0 = auto), 3 unrolled
+// levels, 4 settle the deep rows' level 1 from the column's zone map (0/1).
+constexpr int kTunes = 5;
+static int g_tune[kTunes] = {-1, -1, -1, -1, -1};
 static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles",
-                                              "ds_unroll", "bs_sparse1", "ds_zonemap"};
+                                              "ds_unroll", "ds_zonemap"};
 static int tune(int i) {
   if (g_tune[i] < 0) {
     static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
-                                            "BSB_DS_UNROLL", "BSB_BS_SPARSE1", "BSB_DS_ZONEMAP"};
-    static const int dflt[kTunes] = {1, 3, 0, 1, 2, 1};
+                                            "BSB_DS_UNROLL", "BSB_DS_ZONEMAP"};
+    static const int dflt[kTunes] = {1, 3, 0, 1, 1};
     const char* e = std::getenv(env[i]);
     g_tune[i] = e ? std::atoi(e) : dflt[i];
   }
@@ -453,8 +452,7 @@ static int tune(int i) {
 }
 // ds_enable: 0 off, 1 all scans, 2 unmasked scans only
 bool ds_enabled(bool masked) { return masked ? tune(0) == 1 : tune(0) != 0; }
-bool ds_zonemap_enabled() { return tune(5) != 0; }
-int bs_sparse1() { return tune(4) - 1; }  // knob 0 = always the SWAR compares
+bool ds_zonemap_enabled() { return tune(4) != 0; }
 
 static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 
@@ -479,7 +477,7 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.mask = mask;
   a.out = out;
   a.count = count;
-  if (deep1_min == deep1_max && deep1_min >= 0 && deep1_min < 256 && tune(5)) {
+  if (deep1_min == deep1_max && deep1_min >= 0 && deep1_min < 256 && tune(4)) {
     const uint32_t x = (uint32_t)deep1_min;
     a.d1 = 1;
     a.d1gA = x > A.byte[0] ? kFull : 0u;

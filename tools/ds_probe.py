@@ -20,14 +20,19 @@ from paper_2209_00220_b200.device import stream as cur_stream  # noqa: E402
 from paper_2209_00220_b200.predicate import Op, Predicate  # noqa: E402
 
 
-def main(settings, reps=20, log2n=28, layout="ppvbs"):
+def main(settings, reps=20, log2n=28, layout="ppvbs", scan_lib=None):
     torch.cuda.set_device(0)
     lib = _lib.load()
     n = 1 << log2n
     data = bench.build_cfg2(n)
     col = data["col_v"] if layout == "ppvbs" else data["col_b"]
     d = data["d_ppe"] if layout == "ppvbs" else data["d_fix"]
-    fn = lib.bsb_vbs_scan if layout == "ppvbs" else lib.bsb_byteslice_scan
+    slib = lib if scan_lib is None else scan_lib
+    fn = slib.bsb_vbs_scan if layout == "ppvbs" else slib.bsb_byteslice_scan
+    if scan_lib is not None:  # another build: same C ABI for the scans
+        for name in ("bsb_vbs_scan", "bsb_byteslice_scan"):
+            getattr(slib, name).restype = getattr(lib, name).restype
+            getattr(slib, name).argtypes = getattr(lib, name).argtypes
     wins = bench.window_bounds(data["table"].values, data["table"].weights, n)
     preds = [d.encode_literal(Predicate("c", Op.BETWEEN, lo, hi)).to_c() for _, lo, hi in wins]
     out = torch.empty(-(-n // 32), dtype=torch.int32, device="cuda")
@@ -37,7 +42,7 @@ def main(settings, reps=20, log2n=28, layout="ppvbs"):
     for setting in settings:
         for kv in filter(None, setting.split(",")):
             k, v = kv.split("=")
-            assert lib.bsb_tune(k.encode(), int(v)) == 0, kv
+            assert slib.bsb_tune(k.encode(), int(v)) == 0, kv
         row = []
         for wi, cp in enumerate(preds):
             ts = []
@@ -61,10 +66,12 @@ def main(settings, reps=20, log2n=28, layout="ppvbs"):
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    if args and args[0].startswith("--lib="):  # A/B against another build of the library
-        _lib.load(args[0][len("--lib="):])
+    scan_lib = None
+    if args and args[0].startswith("--lib="):  # scans from another build of the library
+        import ctypes
+        scan_lib = ctypes.CDLL(os.path.abspath(args[0][len("--lib="):]))
         args = args[1:]
     layout = "ppvbs"
     if args and args[0] in ("ppvbs", "byteslice"):
         layout, args = args[0], args[1:]
-    main(args or [""], layout=layout)
+    main(args or [""], layout=layout, scan_lib=scan_lib)
