@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-lookup", action="store_true")
     ap.add_argument("--lookup-steps", type=int, default=10)
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1/cfg4/cfg5")
+    ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
+                    help="graph step: PP-VBS and ByteSlice scans on 1 or 2 forked streams")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the step as eager launches instead of a CUDA graph replay")
     ap.add_argument("--deep-mode", default="auto",
@@ -350,12 +352,21 @@ def run_b200(args):
     if not args.no_graph:
         # the 8-scan step as one CUDA graph (launch-bound inner loop): the C ABI
         # calls are captured on a side stream; no allocation happens inside
+        # The 8 scans are independent: with --streams 2 the PP-VBS and the
+        # ByteSlice scans are captured on two forked streams, so one layout's
+        # kernel fills the SMs the other's last wave leaves idle.
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
+        side = torch.cuda.Stream()
         cap.wait_stream(stream)
         with torch.cuda.graph(graph, stream=cap):
-            for fn, desc, cp, optr, cptr in calls:
-                _lib.check(fn(desc, cp, None, optr, cptr, None, None, cap.cuda_stream), "scan")
+            if args.streams > 1:
+                side.wait_stream(cap)
+            for (fn, desc, cp, optr, cptr), (layout, *_r) in zip(calls, scans):
+                st_ = side if (args.streams > 1 and layout == "byteslice") else cap
+                _lib.check(fn(desc, cp, None, optr, cptr, None, None, st_.cuda_stream), "scan")
+            if args.streams > 1:
+                cap.wait_stream(side)
         stream.wait_stream(cap)
         for _ in range(3):
             graph.replay()
@@ -463,7 +474,9 @@ def run_b200(args):
                        "l2": f"inputs larger than L2 (PP-VBS {col_bytes(col_v) / 1e6:.0f} MB, "
                              f"ByteSlice {col_bytes(col_b) / 1e6:.0f} MB per column)",
                        "parallelism": f"row shards x{world}" if world > 1 else "single GPU",
-                       "launch": "CUDA graph of the 8 scans (C ABI calls captured)"
+                       "launch": (f"CUDA graph of the 8 scans (C ABI calls captured; "
+                                  f"{args.streams} stream{'s' if args.streams > 1 else ''}: "
+                                  f"{'PP-VBS | ByteSlice forked' if args.streams > 1 else 'serial'})")
                                  if graph is not None else "eager C ABI calls"},
             "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": round(dom_e["gbs"], 1), "peak": peak, "unit": "GB/s",
