@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--no-lookup", action="store_true")
     ap.add_argument("--lookup-steps", type=int, default=10)
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1/cfg4/cfg5")
-    ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
-                    help="graph step: PP-VBS and ByteSlice scans on 1 or 2 forked streams")
+    ap.add_argument("--streams", type=int, default=8, choices=(1, 2, 4, 8),
+                    help="graph step: the 8 scans on this many forked streams")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the step as eager launches instead of a CUDA graph replay")
     ap.add_argument("--deep-mode", default="auto",
@@ -352,21 +352,22 @@ def run_b200(args):
     if not args.no_graph:
         # the 8-scan step as one CUDA graph (launch-bound inner loop): the C ABI
         # calls are captured on a side stream; no allocation happens inside
-        # The 8 scans are independent: with --streams 2 the PP-VBS and the
-        # ByteSlice scans are captured on two forked streams, so one layout's
-        # kernel fills the SMs the other's last wave leaves idle.
+        # The 8 scans are independent: with --streams S they are captured on S
+        # forked streams (scan i on stream i mod S; S = 2 puts the PP-VBS and
+        # the ByteSlice scans on their own streams), so one kernel fills the
+        # SMs another's last wave leaves idle.
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
-        side = torch.cuda.Stream()
+        sides = [cap] + [torch.cuda.Stream() for _ in range(args.streams - 1)]
         cap.wait_stream(stream)
         with torch.cuda.graph(graph, stream=cap):
-            if args.streams > 1:
-                side.wait_stream(cap)
-            for (fn, desc, cp, optr, cptr), (layout, *_r) in zip(calls, scans):
-                st_ = side if (args.streams > 1 and layout == "byteslice") else cap
+            for sd in sides[1:]:
+                sd.wait_stream(cap)
+            for i, (fn, desc, cp, optr, cptr) in enumerate(calls):
+                st_ = sides[i % args.streams]
                 _lib.check(fn(desc, cp, None, optr, cptr, None, None, st_.cuda_stream), "scan")
-            if args.streams > 1:
-                cap.wait_stream(side)
+            for sd in sides[1:]:
+                cap.wait_stream(sd)
         stream.wait_stream(cap)
         for _ in range(3):
             graph.replay()
@@ -476,7 +477,7 @@ def run_b200(args):
                        "parallelism": f"row shards x{world}" if world > 1 else "single GPU",
                        "launch": (f"CUDA graph of the 8 scans (C ABI calls captured; "
                                   f"{args.streams} stream{'s' if args.streams > 1 else ''}: "
-                                  f"{'PP-VBS | ByteSlice forked' if args.streams > 1 else 'serial'})")
+                                  f"{'scan i on stream i mod ' + str(args.streams) if args.streams > 1 else 'serial'})")
                                  if graph is not None else "eager C ABI calls"},
             "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": round(dom_e["gbs"], 1), "peak": peak, "unit": "GB/s",
