@@ -12,6 +12,9 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1].startswith("--lib="):  # another build, all symbols
+        from paper_2209_00220_b200 import _lib
+        _lib.load(os.path.abspath(sys.argv.pop(1)[len("--lib="):]))
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     log2n = int(sys.argv[2]) if len(sys.argv) > 2 else 28
     only = sys.argv[3] if len(sys.argv) > 3 else None
