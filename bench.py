@@ -619,8 +619,9 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
                     col_v.desc_ref, dbits.dwords.data_ptr(), ctypes.byref(dec_v), None, None,
                     o32.data_ptr(), cnt.data_ptr(), stream())
             elif layout == "byteslice":
-                # public API: long unsorted id lists are gathered in row order
-                fn = lambda: lookup_byteslice_rows(col_b, drows)
+                # public API, int32 values out (identity codes: code = value);
+                # long unsorted id lists are gathered in row order
+                fn = lambda: lookup_byteslice_rows(col_b, drows, out_dtype=torch.int32)
             else:
                 fn = lambda: lookup_vbs_rows_dec(col_v, drows, dec_v, out_dtype=torch.int32)
             ms = timed(fn)
@@ -629,7 +630,7 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
             if is_bits and int(cnt.item()) != nsel:
                 raise RuntimeError(f"{layout}/{name}: fused lookup count mismatch")
             K = col_b.n_slices if layout == "byteslice" else col_v.max_len
-            ob = 8 if layout == "byteslice" else 4
+            ob = 8 if (is_bits and layout == "byteslice") else 4
             ab = lookup_alg_bytes_rows(
                 rows, K, layout, None if layout == "byteslice" else exist_v,
                 out_bytes=ob, id_bytes=0 if is_bits else 8,

@@ -179,7 +179,9 @@ int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred, const uin
  * duplicates allowed; output in input order).  Writes right-aligned codes to
  * out_codes (may be NULL) and, when rank_values (int64[dict size]) is given,
  * decoded values values[code] (dictionary.py:413-414) to out_values (int64,
- * may be NULL) and/or out_values32 (int32, may be NULL). */
+ * may be NULL) and/or out_values32 (int32, may be NULL).  Without
+ * rank_values, out_values32 receives the codes truncated to int32 (columns
+ * whose codes are the values). */
 int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t* rows, int64_t n_ids,
                               uint64_t* out_codes, const int64_t* rank_values,
                               int64_t* out_values, int32_t* out_values32, void* stream);

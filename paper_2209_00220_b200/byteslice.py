@@ -154,13 +154,20 @@ def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=
     in input order).  Returns codes, or decoded values rank_values[code] when
     a device value table is given.  order="sort" gathers a long unsorted list
     in row order and scatters the output back (device.gather_order); "auto"
-    is "keep" for ByteSlice: K random sectors per id cost less than the sort
-    and the scatter (measured)."""
+    is "keep" for ByteSlice: the order check, the sort and the scatter back
+    cost about what the K random sectors per id they save (measured, DESIGN.md
+    §5).  rank_values None + out_dtype int32: the codes as int32."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
     g, perm = gather_order(rows, col.n_rows, "keep" if order == "auto" else order)
     if rank_values is None:
+        if out_dtype == torch.int32:  # codes as int32 (identity dictionaries)
+            out = torch.empty(n, dtype=torch.int32, device=rows.device)
+            _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n, None, None,
+                                                     None, out.data_ptr(), stream()),
+                       "lookup_byteslice")
+            return scatter_back(out, perm)
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
         _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n,
                                                  out.data_ptr(), None, None, None, stream()),

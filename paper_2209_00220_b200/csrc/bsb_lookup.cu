@@ -57,6 +57,8 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
         const int64_t v = __ldg(rank_values + cd);
         if (out_values) out_values[i] = v;
         if (out_values32) out_values32[i] = (int32_t)v;
+      } else if (out_values32) {
+        out_values32[i] = (int32_t)cd;  // codes that are the values (identity dictionary)
       }
     }
   }

@@ -165,6 +165,10 @@ def test_row_lookups_sorted_gather():
         assert np.array_equal(got.view(np.uint64), codes[ids]), order
     got = B.lookup_byteslice_rows(col, torch.from_numpy(np.sort(ids))).cpu().numpy()
     assert np.array_equal(got.view(np.uint64), codes[np.sort(ids)])
+    for order in ("auto", "keep"):  # int32 codes (sorted gather under "auto")
+        got = B.lookup_byteslice_rows(col, torch.from_numpy(ids), out_dtype=torch.int32,
+                                      order=order).cpu().numpy()
+        assert np.array_equal(got, codes[ids].astype(np.int32)), order
     vals, od, vcodes, lens = _ppe_column(1.1, 16, n, 9)
     vcol = B.build_vbs(vcodes, lens)
     K = vcol.max_len
