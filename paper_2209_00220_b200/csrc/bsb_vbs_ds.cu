@@ -1,5 +1,4 @@
-// bsb_vbs_ds.cu -- PP-VBS scan in deep-row space (SLICED layout with the
-// deep rows' first byte, deep[0]).
+// bsb_vbs_ds.cu -- PP-VBS scan in deep-row space (SLICED layout).
 //
 // The reference's Alg. 3 (vbs.py:222-289) classifies each row by its own
 // bytes only, so the rows split cleanly by code length:
@@ -7,8 +6,10 @@
 //     gt = byte > lit, eq_final = byte == lit only when the literal has one
 //     byte (a shorter code tied on its own bytes is less, vbs.py:273-275);
 //   * a row with a longer code ("deep") runs levels 1..len entirely on the
-//     deep-row ByteSlice column: level-1 byte from deep[0], byte j from
-//     deep[j-1], existence of byte j+1 from rexist[j] (byte 2 always exists).
+//     deep-row ByteSlice column: level-1 byte from deep[0] (or settled by the
+//     column's zone map when all deep rows share their first byte), byte j
+//     from deep[j-1], existence of byte j+1 from rexist[j] (byte 2 always
+//     exists).
 // Row space therefore needs no level-1 tie masks and no pext into deep-row
 // order: phase 1 (lane = row block) computes the shallow rows' result and the
 // block's deep-row offset; phase 2 (lane = deep block of the super-tile) runs
@@ -21,15 +22,14 @@
 // row can match (e.g. a BETWEEN whose legs share their first byte with a
 // multi-byte lo literal, or EQ with a multi-byte literal), so phase 1 reads
 // only the M_2 words -- no first-slice bytes at all.
-// The L1 variant prefetches the next super-tile's first-slice bytes into L2
-// (cp.async.bulk.prefetch) instead of holding them in registers across
-// phases 2-3.  (Measured and dropped: L2 prefetch of the next super-tile's
-// deep levels, requesting level j+1 together with level j, 5-6 CTAs/SM at
-// 40-48 registers, and cp.async staging of deep levels 1-4 into shared
-// memory one super-tile ahead -- none moved the time by more than the
-// run-to-run noise: the kernel is issue-bound, not load-latency-bound.)
-// Unmasked scans only; masked scans (conjunction chains) use the SLICED
-// kernel, which skips the loads of masked-out blocks.
+// The next super-tile's directory, M_2 words and level-1 deep sectors are
+// requested across phases; the L1 variant prefetches the next super-tile's
+// first-slice bytes into L2 (cp.async.bulk.prefetch) instead of holding them
+// in registers.  MASKED (conjunction chains): see the kernel.
+// Measured and dropped: L2 prefetch of deep levels, level j+1
+// requested with level j, cp.async staging of deep levels in shared memory,
+// 5-6 CTAs/SM, extra compare bodies (0x00 / adjacent literal bytes) -- the
+// kernel is issue-bound and sensitive to code layout, not latency-bound.
 #include <cstdlib>
 #include <cstring>
 
