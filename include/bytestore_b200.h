@@ -103,9 +103,9 @@ typedef struct bsb_byteslice {
  *             per deep block: bit i = deep row 32k+i has byte j+1.  Scanned with
  *             the ByteSlice SWAR compare, one lane per deep block.
  *             deep[0] (optional, SLICED only) holds byte 1 of every deep row
- *             in the same deep-block layout; with it (or with a uniform
- *             deep1_min == deep1_max zone map, which makes it unnecessary)
- *             scans run entirely in deep-row space for the deep rows.
+ *             in the same deep-block layout; with it (or with the
+ *             deep1_shared zone map, which makes it unnecessary) scans run
+ *             entirely in deep-row space for the deep rows.
  * deep allocations are padded by >= 64 bytes.  Index 0 of exist/block_dir/
  * rexist is unused (level 1 is bs1); index 0 of deep is unused except as
  * above. */
@@ -124,11 +124,12 @@ typedef struct bsb_vbs {
   const int64_t* block_dir[BSB_MAX_LEVELS];
   int64_t deep_len[BSB_MAX_LEVELS];
   const uint32_t* rexist[BSB_MAX_LEVELS];
-  /* Range of the first byte over the deep rows (a zone map; SLICED with
-   * deep[0]).  deep1_min == deep1_max lets scans settle level 1 of every deep
-   * row without reading deep[0]; deep1_min > deep1_max = unknown. */
-  int32_t deep1_min;
-  int32_t deep1_max;
+  /* Zone map of the deep rows' first byte (SLICED): 1 + the byte when every
+   * deep row starts with the same byte, which lets scans settle level 1 of
+   * the deep rows without reading deep[0]; 0 = not shared / unknown (the
+   * zero-initialised default). */
+  int32_t deep1_shared;
+  int32_t reserved;
 } bsb_vbs;
 
 /* One column reference for bsb_conj_scan (engine.py:322-332). */
@@ -146,7 +147,7 @@ const char* bsb_version(void);
  * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
  * scans only), "ds_serial" (warp-cooperative pdep up to this many blocks per
  * tile), "ds_tiles" (tiles per super-tile, 0 = auto), "ds_unroll" (0/1),
- * "ds_zonemap" (0/1: settle level 1 from deep1_min/max).  Unknown key:
+ * "ds_zonemap" (0/1: settle level 1 from deep1_shared).  Unknown key:
  * BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);

@@ -45,7 +45,7 @@ class BsbVbs(ctypes.Structure):
                 ("deep_mode", c_int32), ("bs1", c_void_p), ("deep", c_void_p * MAX_LEVELS),
                 ("exist", c_void_p * MAX_LEVELS), ("block_dir", c_void_p * MAX_LEVELS),
                 ("deep_len", c_int64 * MAX_LEVELS), ("rexist", c_void_p * MAX_LEVELS),
-                ("deep1_min", c_int32), ("deep1_max", c_int32)]
+                ("deep1_shared", c_int32), ("reserved", c_int32)]
 
 
 class BsbDecode(ctypes.Structure):

@@ -338,7 +338,7 @@ int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const L
                     const uint32_t* mask, uint32_t* out, unsigned long long* count,
                     cudaStream_t s);
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
-                int deep1_min, int deep1_max, const Leg& A, const Leg& B, bool between,
+                int deep1_shared, const Leg& A, const Leg& B, bool between,
                 const uint32_t* mask, uint32_t* out, unsigned long long* count,
                 cudaStream_t s);
 }
@@ -398,10 +398,9 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
                     : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
     case BSB_DEEP_SLICED:
       if (K >= 2 && bsb::ds_enabled(mask != nullptr) &&
-          (col->deep[0] || (col->deep1_min == col->deep1_max && bsb::ds_zonemap_enabled())))
-        return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], col->deep1_min,
-                           col->deep1_max, a.A, a.B, pred->op == BSB_BETWEEN, mask, out_words,
-                           a.count, s);
+          (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled())))
+        return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], col->deep1_shared,
+                           a.A, a.B, pred->op == BSB_BETWEEN, mask, out_words, a.count, s);
       return vbs_sliced_scan(a.vbs, a.n_rows, K >= 2 ? col->deep_len[1] : 0, a.A, a.B,
                              pred->op == BSB_BETWEEN, mask, out_words, a.count, s);
     default: return BSB_EINVAL;

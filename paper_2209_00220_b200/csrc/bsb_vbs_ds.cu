@@ -458,7 +458,7 @@ static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 
 // Scan of a SLICED column that carries deep[0] (K >= 2), optionally masked.
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
-                int deep1_min, int deep1_max, const Leg& A, const Leg& B, bool between,
+                int deep1_shared, const Leg& A, const Leg& B, bool between,
                 const uint32_t* mask, uint32_t* out, unsigned long long* count,
                 cudaStream_t s) {
   DsArgs a;
@@ -477,8 +477,8 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.mask = mask;
   a.out = out;
   a.count = count;
-  if (deep1_min == deep1_max && deep1_min >= 0 && deep1_min < 256 && tune(4)) {
-    const uint32_t x = (uint32_t)deep1_min;
+  if (deep1_shared >= 1 && deep1_shared <= 256 && tune(4)) {
+    const uint32_t x = (uint32_t)(deep1_shared - 1);
     a.d1 = 1;
     a.d1gA = x > A.byte[0] ? kFull : 0u;
     a.d1eA = x == A.byte[0] ? kFull : 0u;

@@ -53,7 +53,8 @@ class VbsColumn:
         d.max_len = self.max_len
         d.deep_mode = self.deep_mode
         d.bs1 = self.bs1.data_ptr()
-        d.deep1_min, d.deep1_max = self.deep1_range
+        lo, hi = self.deep1_range
+        d.deep1_shared = lo + 1 if lo == hi else 0  # zone map: shared first byte + 1
         if self.deep and self.deep[0] is not None:  # SLICED: deep rows' first byte
             d.deep[0] = self.deep[0].data_ptr()
             d.deep_len[0] = self.deep[0].numel() - DEEP_PAD

@@ -318,7 +318,7 @@ def test_vbs_sliced_deep_space_scan_vs_oracle():
             use = lens > k
             codes[use] |= byts[use, k] << np.uint64(8 * k)
         col = B.build_vbs(codes, lens, deep_mode="sliced")
-        assert col.deep[0] is not None
+        assert col.deep[0] is not None and col._desc.deep1_shared == 0
         ocol = O.vbs_build(codes, lens)
 
         def lit():
@@ -373,7 +373,7 @@ def test_vbs_sliced_zone_map_uniform_first_byte(x):
     top = (lens.astype(np.uint64) - np.uint64(1)) * np.uint64(8)
     codes[deep] = (codes[deep] & ~(np.uint64(0xFF) << top[deep])) | (np.uint64(x) << top[deep])
     col = B.build_vbs(codes, lens, deep_mode="sliced")
-    assert col.deep1_range == (x, x)
+    assert col.deep1_range == (x, x) and col._desc.deep1_shared == x + 1
     assert col.deep[0] is None  # the zone map makes the level-1 plane unnecessary
     ocol = O.vbs_build(codes, lens)
     mw = O.bools_to_words(rng.random(n) < 0.5)
