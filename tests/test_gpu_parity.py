@@ -686,3 +686,51 @@ def test_device_bitvector_ops():
         assert da.count() == a.count()
         assert np.array_equal(da.to_indices(), a.to_indices())
         assert np.array_equal(da.row_ids(5).cpu().numpy(), a.to_indices() + 5)
+
+
+def test_row_range_shards_concatenate_to_the_full_scan():
+    """SURVEY.md §8(e) on one GPU: each tile-aligned row-range shard built and
+    scanned on its own (global dictionary, as every rank does) -- ByteSlice
+    and PP-VBS through the deep-row-space kernel, with and without masks --
+    concatenates to the full column's words, and the shard counts' exclusive
+    prefix gives each shard's first global match."""
+    from paper_2209_00220_b200.sharded import shard_range
+    n = (1 << 20) + 777
+    vals, od, codes, lens = _ppe_column(1.2, 18, n, 5)
+    of = O.OracleDict.from_values(vals, "fixed")
+    ranks = of.encode_rows(vals)
+    w = max(1, int(ranks.max()).bit_length())
+    full_v = B.build_vbs(codes, lens)
+    full_b = B.build_byteslice(ranks, w)
+    srt = np.sort(vals)
+    mw = O.bools_to_words(np.random.default_rng(1).random(n) < 0.4)
+    for p in (0.001, 0.1, 0.5):
+        lo, hi = int(srt[int((1 - p - min(p, .25)) * n)]), int(srt[int((1 - min(p, .25)) * n)])
+        pv = od.encode_literal("BETWEEN", lo, hi)
+        rb = of.encode_literal("BETWEEN", lo, hi)
+        for masked in (False, True):
+            m_full = B.ResultBitVector(n, mw) if masked else None
+            want_v, _ = B.scan_vbs(full_v, rp(list(pv)), m_full)
+            want_b, _ = B.scan_byteslice(full_b, rp(list(rb)), m_full)
+            assert np.array_equal(want_v.words, want_b.words)
+            for world in (2, 3, 8):
+                parts, counts = [], []
+                for rank in range(world):
+                    r0, r1 = shard_range(n, world, rank)
+                    if r1 <= r0:
+                        continue
+                    col = B.build_vbs(codes[r0:r1], lens[r0:r1])
+                    m = (B.ResultBitVector(r1 - r0, O.bools_to_words(
+                        O.words_to_bools(mw, n)[r0:r1])) if masked else None)
+                    bv, _ = B.scan_vbs(col, rp(list(pv)), m)
+                    parts.append(O.words_to_bools(bv.words, r1 - r0))
+                    counts.append(bv.count())
+                got = np.concatenate(parts)
+                assert np.array_equal(got, O.words_to_bools(want_v.words, n)), (p, world)
+                assert sum(counts) == want_v.count()
+                offs = np.concatenate([[0], np.cumsum(counts)[:-1]])
+                first = np.flatnonzero(got)
+                r0s = [shard_range(n, world, r)[0] for r in range(len(counts))]
+                for k, c in enumerate(counts):
+                    if c:
+                        assert first[offs[k]] >= r0s[k]
