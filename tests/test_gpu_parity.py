@@ -734,3 +734,47 @@ def test_row_range_shards_concatenate_to_the_full_scan():
                 for k, c in enumerate(counts):
                     if c:
                         assert first[offs[k]] >= r0s[k]
+
+
+@pytest.mark.parametrize("tiles", [0, 1, 4])
+def test_vbs_sliced_all_rows_deep(tiles):
+    """Every code has >= 2 bytes: a 1-tile super-tile spans up to 33 deep
+    blocks (the deep-block pass runs twice), and forced 4-tile super-tiles up
+    to 129; unaligned deep-row bases; every op, BETWEEN, masks."""
+    rng = np.random.default_rng(31 + tiles)
+    lib = B._lib.load()
+    n, K = 70_003, 4
+    lens = rng.integers(2, K + 1, size=n).astype(np.uint8)
+    byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+    byts[:, 0] |= np.uint64(1)
+    byts[:, 1] &= np.uint64(3)  # few distinct second bytes: many ties
+    codes = np.zeros(n, np.uint64)
+    for k in range(8):
+        use = lens > k
+        codes[use] |= byts[use, k] << np.uint64(8 * k)
+    col = B.build_vbs(codes, lens, deep_mode="sliced")
+    ocol = O.vbs_build(codes, lens)
+    mw = O.bools_to_words(rng.random(n) < 0.3)
+    assert lib.bsb_tune(b"ds_tiles", tiles) == 0
+    try:
+        for r in rng.integers(0, n, size=5):
+            c, ll = int(codes[r]), int(lens[r])
+            for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                p = O.pred_compare(op, c, ll)
+                for m_o in (None, mw):
+                    want, _ = O.vbs_scan(ocol, p, m_o)
+                    bv, _ = B.scan_vbs(col, rp(list(p)),
+                                       None if m_o is None else B.ResultBitVector(n, m_o))
+                    assert np.array_equal(bv.words, want), (tiles, op)
+            r2 = int(rng.integers(0, n))
+            a, b = sorted([(int(codes[r]) << (8 * (K - ll)), c, ll),
+                           (int(codes[r2]) << (8 * (K - int(lens[r2]))), int(codes[r2]),
+                            int(lens[r2]))])
+            p = O.pred_between(a[1], a[2], b[1], b[2])
+            for m_o in (None, mw):
+                want, _ = O.vbs_scan(ocol, p, m_o)
+                bv, _ = B.scan_vbs(col, rp(list(p)),
+                                   None if m_o is None else B.ResultBitVector(n, m_o))
+                assert np.array_equal(bv.words, want), (tiles, "BETWEEN")
+    finally:
+        lib.bsb_tune(b"ds_tiles", 0)
