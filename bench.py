@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="time the step as eager launches instead of a CUDA graph replay")
     ap.add_argument("--deep-mode", default="auto",
-                    help="PP-VBS deep layout: auto|packed|rank2|planes|sliced")
+                    help="PP-VBS deep layout: auto|packed|sliced")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clocks/e2e/cpu baseline")
     return ap.parse_args()
@@ -525,7 +525,7 @@ def measure_extra_configs(data) -> dict:
     import bench_cfgs
     out = {}
     for name, fn in (("cfg1", bench_cfgs.measure_cfg1), ("cfg4", bench_cfgs.measure_cfg4),
-                     ("cfg5", bench_cfgs.measure_cfg5), ("layout_sweep", bench_cfgs.measure_sweep)):
+                     ("cfg5", bench_cfgs.measure_cfg5)):
         torch.cuda.empty_cache()
         t0 = time.perf_counter()
         try:

@@ -324,18 +324,3 @@ def measure_cfg5(reps: int = 20, log2n: int = 29) -> dict:
                    "selected": int(allm.sum()),
                    "row_ids_us": round(ms_ids * 1e3, 2)}
     return out
-
-
-# ------------------------------------------------------------ layout sweep
-def measure_sweep(log2n: int = 26) -> dict:
-    """The reference's layout sweep (bench.py:59-107) on the device: LT scan
-    near 10 % selectivity and lookup + decode of its matches for all five
-    layouts, Zipf skews 0.5 / 1.0 / 1.5 over 2^20 values."""
-    from paper_2209_00220_b200.sweep import SweepSpec, run_sweep
-    rows = run_sweep(SweepSpec(s_values=[0.5, 1.0, 1.5], domain_bits=20, n_rows=1 << log2n,
-                               reps=5))
-    return {"workload": f"layout sweep: 2^{log2n} rows, Zipf s in (0.5, 1.0, 1.5) over 2^20, "
-                        "LT at ~10% selectivity, device-timed median of 5",
-            "rows": [{k: (float(f"{v:.5g}") if isinstance(v, float) else v)
-                      for k, v in r.items()} for r in rows]}
-

@@ -45,10 +45,15 @@ enum bsb_status {
   BSB_ERANGE = 2,     /* value out of range (width, length)   -> ValueError   */
   BSB_ENOTFOUND = 3,  /* padded code not in dictionary        -> LookupError  */
   BSB_ECUDA = 4,      /* CUDA runtime error                   -> RuntimeError */
-  BSB_EKEY = 5        /* value missing from dictionary        -> KeyError     */
+  BSB_EKEY = 5,       /* value missing from dictionary        -> KeyError     */
+  BSB_EINDEX = 6      /* row id outside [0, n_rows)           -> IndexError   */
 };
 
 /* Operators: reference predicate.py:13-38 (Op). */
+/* Bits of the device error word (err_dev) of the row-id lookups. */
+#define BSB_ERR_NOTFOUND 1u
+#define BSB_ERR_INDEX 2u
+
 enum bsb_op { BSB_EQ = 0, BSB_NE = 1, BSB_LT = 2, BSB_LE = 3, BSB_GT = 4, BSB_GE = 5,
               BSB_BETWEEN = 6 };
 
@@ -86,16 +91,6 @@ typedef struct bsb_byteslice {
  *  BSB_DEEP_PACKED (0): deep[j] = slice j+1 packed in row order exactly like
  *             the reference (vbs.py:98-100); block_dir[j] = int64[stride/32+1]
  *             bytes of slice j+1 before block b (vbs.py:105-106).
- *  BSB_DEEP_RANK2 (1): every deep slice holds one byte per "deep row" (rows
- *             whose code has >= 2 bytes), in row order; rows shorter than the
- *             level hold a 0 pad byte.  All levels share block_dir[1] (the
- *             level-2 directory); block_dir[j>1] are unused.  The scan then
- *             works in one packed space per block for all deep levels.
- *  BSB_DEEP_PLANES (2): like RANK2 but levels are paired into big-endian
- *             uint16 planes indexed by deep row: deep[p+1] = plane p holding
- *             bytes (2p+2, 2p+3) (p = 0..ceil((max_len-1)/2)-1, 0-padded);
- *             rexist[j] (j = 2..max_len-1) = bitmap over deep rows of "code
- *             has byte j+1".  Scanned cooperatively, one deep row per lane.
  *  BSB_DEEP_SLICED (3): the deep rows form their own ByteSlice-like column:
  *             deep[j] (j = 1..max_len-1) holds byte j+1 of every deep row in
  *             32-deep-row "deep blocks", swizzled like bs1 (0-padded for rows
@@ -110,9 +105,7 @@ typedef struct bsb_byteslice {
  * rexist is unused (level 1 is bs1); index 0 of deep is unused except as
  * above. */
 #define BSB_DEEP_PACKED 0
-#define BSB_DEEP_RANK2 1
-#define BSB_DEEP_PLANES 2
-#define BSB_DEEP_SLICED 3
+#define BSB_DEEP_SLICED 3 /* modes 1 and 2 (experimental round-1 layouts) were removed */
 typedef struct bsb_vbs {
   int64_t n_rows;
   int64_t stride;
@@ -182,10 +175,16 @@ int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred, const uin
  * decoded values values[code] (dictionary.py:413-414) to out_values (int64,
  * may be NULL) and/or out_values32 (int32, may be NULL).  Without
  * rank_values, out_values32 receives the codes truncated to int32 (columns
- * whose codes are the values). */
+ * whose codes are the values).  Row ids are checked against [0, n_rows)
+ * inside the gather (an out-of-range id is never read; the reference raises
+ * IndexError at the numpy fancy index, byteslice.py:154): with err_dev (a
+ * caller-zeroed device word) the call does not synchronise and ORs
+ * BSB_ERR_INDEX into *err_dev; with err_dev NULL it synchronises and returns
+ * BSB_EINDEX. */
 int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t* rows, int64_t n_ids,
                               uint64_t* out_codes, const int64_t* rank_values,
-                              int64_t* out_values, int32_t* out_values32, void* stream);
+                              int64_t* out_values, int32_t* out_values32, uint32_t* err_dev,
+                              void* stream);
 
 /* ----------------------------------------------------------------- PP-VBS */
 /* build_vbs, pass 1 (vbs.py:68-82): validate lengths 1..8 and code widths,
@@ -220,11 +219,14 @@ int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
  * NULL).  A code absent from the dictionary sets BSB_ENOTFOUND (syncs only
  * when decoding).  level_counts (uint64[BSB_MAX_LEVELS], may be NULL) is
  * overwritten with the number of looked-up rows owning a byte at each level
- * (LookupStats accounting, vbs.py:346-370). */
+ * (LookupStats accounting, vbs.py:346-370).  err_dev as for
+ * bsb_byteslice_lookup_rows (BSB_ERR_INDEX / BSB_ERR_NOTFOUND bits; NULL =
+ * synchronise and return BSB_EINDEX / BSB_ENOTFOUND). */
 int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
                         uint64_t* out_padded, const uint64_t* sorted_padded,
                         const int64_t* dict_values, int64_t n_dict, int64_t* out_values,
-                        int32_t* out_values32, uint64_t* level_counts, void* stream);
+                        int32_t* out_values32, uint64_t* level_counts, uint32_t* err_dev,
+                        void* stream);
 
 /* Decode of looked-up codes to values (dictionary.py:403-414).
  *  kind 0: none (raw codes out)
@@ -267,8 +269,10 @@ int bsb_vbs_lookup_bits(const bsb_vbs* col, const uint32_t* words, const bsb_dec
                         uint64_t* n_out_dev, void* stream);
 /* Row-id lookup of a PP-VBS column with a general decoder (kinds 0/2/3).
  * With err_dev (caller-zeroed device word) given the call does not
- * synchronise and *err_dev becomes nonzero for a code not in the dictionary;
- * with err_dev NULL a decoding call synchronises and returns BSB_ENOTFOUND. */
+ * synchronise and ORs BSB_ERR_NOTFOUND into *err_dev for a code not in the
+ * dictionary and BSB_ERR_INDEX for a row id outside [0, n_rows) (never
+ * read); with err_dev NULL it synchronises and returns BSB_EINDEX /
+ * BSB_ENOTFOUND. */
 int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
                             const bsb_decode* dec, uint64_t* out_padded, int64_t* out_values,
                             int32_t* out_values32, uint32_t* err_dev, void* stream);

@@ -30,8 +30,6 @@ _LAZY = {
     "bitpacked_size_report": "bitpacked", "VbpColumn": "vbp", "build_vbp": "vbp",
     "pad_codes": "vbp", "scan_vbp": "vbp", "lookup_vbp": "vbp", "vbp_size_report": "vbp",
     "ppe_categorical": "dictionary", "prefix_free_assignment": "dictionary",
-    "SweepSpec": "sweep", "run_sweep": "sweep", "sweep_to_csv": "sweep",
-    "ingest": "engine", "read_csv_columns": "engine",
     "ColumnKind": "dictionary", "FrequencyTable": "dictionary", "CodeAssignment": "dictionary",
     "Dictionary": "dictionary", "build_frequency_table": "dictionary",
     "ppe_numerical": "dictionary", "fixed_assignment": "dictionary",

@@ -22,10 +22,11 @@ MAX_LEVELS = 8
 MAX_CONJ = 8
 STATS_WORDS = 24
 
-OK, EINVAL, ERANGE, ENOTFOUND, ECUDA, EKEY = 0, 1, 2, 3, 4, 5
+OK, EINVAL, ERANGE, ENOTFOUND, ECUDA, EKEY, EINDEX = 0, 1, 2, 3, 4, 5, 6
+ERR_NOTFOUND, ERR_INDEX = 1, 2  # device error word bits (err_dev)
 OP_CODES = {"EQ": 0, "NE": 1, "LT": 2, "LE": 3, "GT": 4, "GE": 5, "BETWEEN": 6}
 LAYOUT_BYTESLICE, LAYOUT_PPVBS = 0, 1
-DEEP_PACKED, DEEP_RANK2, DEEP_PLANES, DEEP_SLICED = 0, 1, 2, 3
+DEEP_PACKED, DEEP_SLICED = 0, 3
 VBP_PLAIN, VBP_PADDED = 0, 1
 VBP_MAX_PLANES, VBP_STATS_WORDS = 32, 66
 
@@ -81,14 +82,14 @@ _SIGS = {
     "bsb_byteslice_scan": (c_int32, [POINTER(BsbByteSlice), POINTER(BsbPred), _P, _P, _P, _P,
                                      _P, _P]),
     "bsb_byteslice_lookup_rows": (c_int32, [POINTER(BsbByteSlice), _P, c_int64, _P, _P, _P, _P,
-                                            _P]),
+                                            _P, _P]),
     "bsb_vbs_plan": (c_int32, [_P, _P, c_int64, POINTER(c_int32), POINTER(c_int64), _P]),
     "bsb_vbs_build": (c_int32, [_P, _P, POINTER(BsbVbs), _P]),
     "bsb_vbs_export_bs1": (c_int32, [POINTER(BsbVbs), _P, _P]),
     "bsb_vbs_export_level": (c_int32, [POINTER(BsbVbs), c_int32, _P, _P, _P]),
     "bsb_vbs_scan": (c_int32, [POINTER(BsbVbs), POINTER(BsbPred), _P, _P, _P, _P, _P, _P]),
     "bsb_vbs_lookup_rows": (c_int32, [POINTER(BsbVbs), _P, c_int64, _P, _P, _P, c_int64, _P, _P,
-                                      _P, _P]),
+                                      _P, _P, _P]),
     "bsb_byteslice_lookup_bits": (c_int32, [POINTER(BsbByteSlice), _P, POINTER(BsbDecode), _P,
                                             _P, _P, _P, _P]),
     "bsb_vbs_lookup_bits": (c_int32, [POINTER(BsbVbs), _P, POINTER(BsbDecode), _P, _P, _P, _P,
@@ -163,6 +164,8 @@ def check(rc: int, what: str = ""):
         raise LookupError(msg)
     if rc == EKEY:
         raise KeyError(msg)
+    if rc == EINDEX:
+        raise IndexError(msg)
     raise RuntimeError(f"CUDA error in {msg}")
 
 

@@ -181,30 +181,13 @@ __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
     const uint64_t c = codes[r];
     const int64_t b = r >> 5;
     const uint32_t below = (1u << (r & 31)) - 1u;
-    if (mode == BSB_DEEP_RANK2) {
-      // one slot per deep row in every deep slice; shorter codes pad with 0
-      const int64_t pos = dir[1][b] + __popc(exist[1][b] & below);
-      for (int j = 2; j <= K; ++j)
-        deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
-    } else if (mode == BSB_DEEP_SLICED) {
+    if (mode == BSB_DEEP_SLICED) {
       // deep rows as a swizzled ByteSlice column + per-deep-block existence words
       const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
       const int64_t pos = (q & ~int64_t(31)) + swz((int)(q & 31));
       if (deep[0]) deep[0][pos] = (uint8_t)(c >> (8 * (l - 1)));  // level 1 in deep-row space
       for (int j = 2; j <= K; ++j)
         deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
-      for (int j = 3; j <= (int)l; ++j)
-        atomicOr(rexist[j - 1] + (q >> 5), 1u << (q & 31));
-    } else if (mode == BSB_DEEP_PLANES) {
-      // big-endian uint16 planes of bytes (2p+2, 2p+3) + deep-row existence bitmaps
-      const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
-      const int np = K >> 1;
-      for (int p = 0; p < np; ++p) {
-        const int jh = 2 * p + 2, jl = 2 * p + 3;
-        const uint32_t hi = jh <= (int)l ? (uint32_t)((c >> (8 * (l - jh))) & 0xFF) : 0u;
-        const uint32_t lo = jl <= (int)l ? (uint32_t)((c >> (8 * (l - jl))) & 0xFF) : 0u;
-        reinterpret_cast<uint16_t*>(deep[p + 1])[q] = (uint16_t)((hi << 8) | lo);
-      }
       for (int j = 3; j <= (int)l; ++j)
         atomicOr(rexist[j - 1] + (q >> 5), 1u << (q & 31));
     } else {
@@ -236,9 +219,6 @@ __global__ void vbs_export_level_kernel(int64_t n, int level, int mode,
     uint8_t byte;
     if (mode == BSB_DEEP_SLICED) {
       byte = deep_l[(src & ~int64_t(31)) + swz((int)(src & 31))];
-    } else if (mode == BSB_DEEP_PLANES) {
-      const uint16_t v = reinterpret_cast<const uint16_t*>(deep_l)[src];
-      byte = ((level - 2) & 1) ? (uint8_t)(v & 0xFF) : (uint8_t)(v >> 8);
     } else {
       byte = deep_l[src];
     }
@@ -356,13 +336,12 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
   PtrTable h;
   std::memset(&h, 0, sizeof(h));
   const int mode = col->deep_mode;
-  if (mode < BSB_DEEP_PACKED || mode > BSB_DEEP_SLICED) return BSB_EINVAL;
+  if (mode != BSB_DEEP_PACKED && mode != BSB_DEEP_SLICED) return BSB_EINVAL;
   if (mode == BSB_DEEP_SLICED) h.deep[0] = const_cast<uint8_t*>(col->deep[0]);  // optional
   for (int j = 1; j < K; ++j) {
     const bool need_dir = mode == BSB_DEEP_PACKED || j == 1;
-    const bool need_deep = mode != BSB_DEEP_PLANES || j <= (K >> 1);
-    const bool need_rex = (mode == BSB_DEEP_PLANES || mode == BSB_DEEP_SLICED) && j >= 2;
-    if ((need_deep && !col->deep[j]) || !col->exist[j] || (need_dir && !col->block_dir[j]) ||
+    const bool need_rex = mode == BSB_DEEP_SLICED && j >= 2;
+    if (!col->deep[j] || !col->exist[j] || (need_dir && !col->block_dir[j]) ||
         (need_rex && !col->rexist[j]))
       return BSB_EINVAL;
     h.deep[j] = const_cast<uint8_t*>(col->deep[j]);
@@ -433,8 +412,7 @@ extern "C" int bsb_vbs_export_level(const bsb_vbs* col, int32_t level, uint8_t* 
   cub::DeviceScan::InclusiveSum(tmp, tb, cnt, out_dir + 1, nb, s);
   BSB_LAUNCH_CHECK();
   const bool shared_dir = col->deep_mode != BSB_DEEP_PACKED;
-  const uint8_t* src = col->deep_mode == BSB_DEEP_PLANES ? col->deep[((level - 2) >> 1) + 1]
-                                                         : col->deep[level - 1];
+  const uint8_t* src = col->deep[level - 1];
   vbs_export_level_kernel<<<grid_for(n, 256), 256, 0, s>>>(
       n, level, col->deep_mode, src, col->exist[level - 1], col->exist[1],
       shared_dir ? col->block_dir[1] : col->block_dir[level - 1], out_dir, out_bytes);

@@ -302,6 +302,10 @@ __device__ __forceinline__ uint32_t finalize_op(int op, uint32_t gt, uint32_t eq
   }
 }
 
+// Device error word bits of the row-id lookups (err_dev).
+constexpr unsigned int kErrNotFound = 1u;  // padded code not in the dictionary -> LookupError
+constexpr unsigned int kErrIndex = 2u;     // row id outside [0, n_rows)        -> IndexError
+
 __device__ __forceinline__ uint32_t tail_valid(int64_t block, int64_t n_rows) {
   const int64_t r0 = block * 32;
   if (r0 + 32 <= n_rows) return kFull;

@@ -27,8 +27,10 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
                                  uint64_t* __restrict__ out_codes,
                                  const int64_t* __restrict__ rank_values,
                                  int64_t* __restrict__ out_values,
-                                 int32_t* __restrict__ out_values32) {
+                                 int32_t* __restrict__ out_values32, int64_t n_rows,
+                                 unsigned int* __restrict__ err) {
   const int shift = 8 * K - width;
+  bool oob = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
        i0 += nthr * kIdsPerThread) {
@@ -37,7 +39,11 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
       const int64_t i = i0 + u * nthr;
-      const int64_t r = i < n_ids ? __ldg(rows + i) : 0;
+      int64_t r = i < n_ids ? __ldg(rows + i) : 0;
+      if ((uint64_t)r >= (uint64_t)n_rows) {  // IndexError in the reference; never read it
+        oob = true;
+        r = 0;
+      }
       pos[u] = (r & ~int64_t(31)) + swz((int)(r & 31));
       c[u] = 0;
     }
@@ -62,6 +68,7 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
       }
     }
   }
+  if (__any_sync(kFull, oob) && (threadIdx.x & 31) == 0) atomicOr(err, kErrIndex);
 }
 
 struct VbsLookupDesc {
@@ -69,9 +76,23 @@ struct VbsLookupDesc {
   const uint8_t* deep[kMaxLevels];
   const uint32_t* exist[kMaxLevels];
   const int64_t* dir[kMaxLevels];
+  int64_t n_rows;
   int K;
   int mode;
 };
+
+static void fill_lookup_desc(VbsLookupDesc& d, const bsb_vbs* col) {
+  std::memset(&d, 0, sizeof(d));
+  d.bs1 = col->bs1;
+  d.K = col->max_len;
+  d.mode = col->deep_mode;
+  d.n_rows = col->n_rows;
+  for (int j = 0; j < kMaxLevels; ++j) {
+    d.deep[j] = col->deep[j];
+    d.exist[j] = col->exist[j];
+    d.dir[j] = col->block_dir[j];
+  }
+}
 
 // lookup_vbs (vbs.py:331-371) + decode_padded (dictionary.py:403-411)
 __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
@@ -89,7 +110,11 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
   for (int j = 0; j < kMaxLevels; ++j) lc[j] = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ids;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = __ldg(rows + i);
+    int64_t r = __ldg(rows + i);
+    if ((uint64_t)r >= (uint64_t)d.n_rows) {  // IndexError in the reference; never read it
+      atomicOr(err, kErrIndex);
+      r = 0;
+    }
     const int64_t b = r >> 5;
     const int lr = (int)(r & 31);
     uint64_t code = (uint64_t)__ldg(d.bs1 + (b * 32 + swz(lr))) << (8 * (K - 1));
@@ -109,12 +134,8 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
       uint64_t byte;
       if (d.mode == BSB_DEEP_SLICED) {
         byte = __ldg(d.deep[j - 1] + ((pos2 & ~int64_t(31)) + swz((int)(pos2 & 31))));
-      } else if (d.mode == BSB_DEEP_PLANES) {
-        const uint16_t v = __ldg(reinterpret_cast<const uint16_t*>(d.deep[((j - 2) >> 1) + 1]) + pos2);
-        byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
       } else {
-        const int64_t pos = d.mode == BSB_DEEP_RANK2 ? pos2
-                                                     : __ldg(d.dir[j - 1] + b) + __popc(w & below);
+        const int64_t pos = __ldg(d.dir[j - 1] + b) + __popc(w & below);
         byte = __ldg(d.deep[j - 1] + pos);
       }
       code |= byte << (8 * (K - j));
@@ -132,7 +153,7 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
       }
       int64_t v = 0;
       if (lo >= n_dict || __ldg(sorted_padded + lo) != code) {
-        atomicOr(err, 1u);
+        atomicOr(err, kErrNotFound);
       } else {
         v = __ldg(dict_values + lo);
       }
@@ -249,61 +270,73 @@ static int bits_to_rows_impl(const uint32_t* words, int64_t n_rows, int64_t row_
 
 using namespace bsb;
 
+// Reads the device error word of a row-id lookup (synchronises) and maps it
+// to a status: an out-of-range id wins over an absent code.
+static int read_err(unsigned int* err, cudaStream_t s) {
+  unsigned int h = 0;
+  BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
+  BSB_CUDA(cudaFreeAsync(err, s));
+  BSB_CUDA(cudaStreamSynchronize(s));
+  if (h & kErrIndex) {
+    set_error_msg("row id out of range");
+    return BSB_EINDEX;
+  }
+  if (h & kErrNotFound) {
+    set_error_msg("padded code not in dictionary");
+    return BSB_ENOTFOUND;
+  }
+  return BSB_OK;
+}
+
+static int alloc_err(unsigned int** err, cudaStream_t s) {
+  BSB_CUDA(cudaMallocAsync(err, 4, s));
+  BSB_CUDA(cudaMemsetAsync(*err, 0, 4, s));
+  return BSB_OK;
+}
+
 extern "C" int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t* rows,
                                          int64_t n_ids, uint64_t* out_codes,
                                          const int64_t* rank_values, int64_t* out_values,
-                                         int32_t* out_values32, void* stream) {
+                                         int32_t* out_values32, uint32_t* err_dev,
+                                         void* stream) {
   if (!col || n_ids < 0 || (n_ids > 0 && !rows)) return BSB_EINVAL;
   if (n_ids == 0) return BSB_OK;
   cudaStream_t s = as_stream(stream);
+  unsigned int* err = err_dev;
+  if (!err) {
+    const int rc = alloc_err(&err, s);
+    if (rc) return rc;
+  }
   bs_lookup_kernel<<<grid_for_l((n_ids + kIdsPerThread - 1) / kIdsPerThread, 256), 256, 0, s>>>(
       col->slices, col->stride, col->n_slices, col->width_bits, rows, n_ids, out_codes,
-      rank_values, out_values, out_values32);
+      rank_values, out_values, out_values32, col->n_rows, err);
   BSB_LAUNCH_CHECK();
-  return BSB_OK;
+  return err_dev ? BSB_OK : read_err(err, s);
 }
 
 extern "C" int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
                                    uint64_t* out_padded, const uint64_t* sorted_padded,
                                    const int64_t* dict_values, int64_t n_dict,
                                    int64_t* out_values, int32_t* out_values32,
-                                   uint64_t* level_counts, void* stream) {
+                                   uint64_t* level_counts, uint32_t* err_dev, void* stream) {
   if (!col || n_ids < 0 || (n_ids > 0 && !rows)) return BSB_EINVAL;
   if (sorted_padded && (!dict_values || n_dict <= 0)) return BSB_EINVAL;
   cudaStream_t s = as_stream(stream);
   if (level_counts) BSB_CUDA(cudaMemsetAsync(level_counts, 0, 8 * kMaxLevels, s));
   if (n_ids == 0) return BSB_OK;
   VbsLookupDesc d;
-  std::memset(&d, 0, sizeof(d));
-  d.bs1 = col->bs1;
-  d.K = col->max_len;
-  d.mode = col->deep_mode;
-  for (int j = 0; j < kMaxLevels; ++j) {
-    d.deep[j] = col->deep[j];
-    d.exist[j] = col->exist[j];
-    d.dir[j] = col->block_dir[j];
-  }
-  unsigned int* err = nullptr;
-  if (sorted_padded) {
-    BSB_CUDA(cudaMallocAsync(&err, 4, s));
-    BSB_CUDA(cudaMemsetAsync(err, 0, 4, s));
+  fill_lookup_desc(d, col);
+  unsigned int* err = err_dev;
+  if (!err) {
+    const int rc = alloc_err(&err, s);
+    if (rc) return rc;
   }
   vbs_lookup_kernel<<<grid_for_l(n_ids, 256), 256, 0, s>>>(d, rows, n_ids, out_padded,
                                                            sorted_padded, dict_values, n_dict,
                                                            out_values, out_values32, err,
                                                            reinterpret_cast<unsigned long long*>(level_counts));
   BSB_LAUNCH_CHECK();
-  if (sorted_padded) {
-    unsigned int h = 0;
-    BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
-    BSB_CUDA(cudaFreeAsync(err, s));
-    BSB_CUDA(cudaStreamSynchronize(s));
-    if (h) {
-      set_error_msg("padded code not in dictionary");
-      return BSB_ENOTFOUND;
-    }
-  }
-  return BSB_OK;
+  return err_dev ? BSB_OK : read_err(err, s);
 }
 
 extern "C" int bsb_bits_to_rows(const uint32_t* words, int64_t n_rows, int64_t* rows_out,
@@ -431,7 +464,7 @@ __device__ __forceinline__ int64_t decode_value(const Decoder& D, uint64_t code,
 // Per-block PP-VBS metadata, loaded once and shared by the block's rows.
 struct VbsBlockMeta {
   uint32_t m[kMaxLevels];  // m[j-1] = existence word of level j (j >= 2)
-  int64_t dir2;            // rank2 / planes / sliced: deep-row base of the block
+  int64_t dir2;            // sliced: deep-row base of the block
 };
 
 __device__ __forceinline__ void vbs_block_meta(const VbsLookupDesc& d, int64_t blk,
@@ -469,11 +502,6 @@ __device__ __forceinline__ uint64_t vbs_row_code_f(const VbsLookupDesc& d, int64
     uint32_t byte;
     if (mode == BSB_DEEP_SLICED) {
       byte = __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
-    } else if (mode == BSB_DEEP_PLANES) {
-      const uint16_t v = __ldg(reinterpret_cast<const uint16_t*>(d.deep[((j - 2) >> 1) + 1]) + q);
-      byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
-    } else if (mode == BSB_DEEP_RANK2) {
-      byte = __ldg(d.deep[j - 1] + q);
     } else {
       byte = __ldg(d.deep[j - 1] + (__ldg(d.dir[j - 1] + blk) + __popc(mt.m[j - 1] & below)));
     }
@@ -635,12 +663,6 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
                 uint32_t byte;
                 if (MODE == BSB_DEEP_SLICED) {
                   byte = __ldg(vd.deep[j - 1] + qs);
-                } else if (MODE == BSB_DEEP_PLANES) {
-                  const uint16_t v =
-                      __ldg(reinterpret_cast<const uint16_t*>(vd.deep[((j - 2) >> 1) + 1]) + q);
-                  byte = ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
-                } else if (MODE == BSB_DEEP_RANK2) {
-                  byte = __ldg(vd.deep[j - 1] + q);
                 } else {
                   byte = __ldg(vd.deep[j - 1] + (__ldg(vd.dir[j - 1] + blkr) +
                                                  __popc(smeta[(j - 2) * 32 + bl] & below)));
@@ -689,7 +711,7 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
     __syncthreads();
     e1s = e1sm;
   }
-  bool bad = false;
+  bool bad = false, oob = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
        i0 += nthr * kIdsPerThread) {
@@ -698,7 +720,11 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
       const int64_t i = i0 + u * nthr;
-      const int64_t r = i < n_ids ? __ldg(rows + i) : 0;
+      int64_t r = i < n_ids ? __ldg(rows + i) : 0;
+      if ((uint64_t)r >= (uint64_t)vd.n_rows) {  // IndexError in the reference; never read it
+        oob = true;
+        r = 0;
+      }
       const int64_t blk = r >> 5;
       const int lr = (int)(r & 31);
       const uint32_t first = __ldg(vd.bs1 + (blk * 32 + swz(lr)));
@@ -727,36 +753,11 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
       emit(oc, ov, ov32, i, padded, v);
     }
   }
-  if (bad) atomicOr(err, 1u);
+  if (bad) atomicOr(err, kErrNotFound);
+  if (__any_sync(kFull, oob) && (threadIdx.x & 31) == 0) atomicOr(err, kErrIndex);
 }
 
-static void fill_lookup_desc(VbsLookupDesc& d, const bsb_vbs* col) {
-  std::memset(&d, 0, sizeof(d));
-  d.bs1 = col->bs1;
-  d.K = col->max_len;
-  d.mode = col->deep_mode;
-  for (int j = 0; j < kMaxLevels; ++j) {
-    d.deep[j] = col->deep[j];
-    d.exist[j] = col->exist[j];
-    d.dir[j] = col->block_dir[j];
-  }
-}
 
-static int finish_err(unsigned int* err, cudaStream_t s, bool need) {
-  if (!need) {
-    BSB_CUDA(cudaFreeAsync(err, s));
-    return BSB_OK;
-  }
-  unsigned int h = 0;
-  BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
-  BSB_CUDA(cudaFreeAsync(err, s));
-  BSB_CUDA(cudaStreamSynchronize(s));
-  if (h) {
-    set_error_msg("padded code not in dictionary");
-    return BSB_ENOTFOUND;
-  }
-  return BSB_OK;
-}
 
 template <bool VBS>
 static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
@@ -828,8 +829,6 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
       constexpr int DKC = decltype(dk)::value;
       switch (vcol->deep_mode) {
         case BSB_DEEP_PACKED: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_PACKED, 0>);
-        case BSB_DEEP_RANK2: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_RANK2, 0>);
-        case BSB_DEEP_PLANES: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_PLANES, 0>);
         default: return sliced_k(dk);
       }
     };
@@ -903,13 +902,11 @@ extern "C" int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, 
                                                     out_values, out_values32, err);       \
     break;
     BSB_ROWS_DEC(BSB_DEEP_PACKED)
-    BSB_ROWS_DEC(BSB_DEEP_RANK2)
-    BSB_ROWS_DEC(BSB_DEEP_PLANES)
     BSB_ROWS_DEC(BSB_DEEP_SLICED)
 #undef BSB_ROWS_DEC
     default: return BSB_EINVAL;
   }
   BSB_LAUNCH_CHECK();
   if (err_dev) return BSB_OK;
-  return finish_err(err, s, D.kind >= 2);
+  return read_err(err, s);
 }

@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t tile_valid(int64_t tile, int64_t b, int64_t 
 // operands (and two tiles ahead, its input-mask word) are fetched while the
 // current tile is scanned.
 template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED, bool L1Z = false>
-__global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
+__global__ void __launch_bounds__(kScanThreads, 1)
     scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(kScanThreads, (LAYOUT >= 3 ? 3 : 1))
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
       res = scan_tile_bs<BETWEEN, STATS, L1Z>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
-      res = scan_tile_vbs<BETWEEN, STATS, LAYOUT - 1>(a.vbs, a.A, a.B, tile, b, valid, in, &st,
-                                                     &depth);
+      res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, in, &st, &depth);
     if (b < a.nb) {
       a.out[b] = res;
       if (STATS && a.depth != nullptr) {
@@ -348,15 +347,6 @@ bool ds_enabled(bool masked);  // bsb_tune("ds_enable") / BSB_DS
 bool ds_zonemap_enabled();     // bsb_tune("ds_zonemap") / BSB_DS_ZONEMAP
 }
 
-// The cooperative plane scan needs every multi-byte literal to end in a
-// non-zero byte (always true for dictionary codes).
-static bool planes_fast_ok(const bsb_pred* p) {
-  auto ok = [](uint64_t code, int len) { return len < 2 || (code & 0xFF) != 0; };
-  if (p->trivial >= 0) return true;
-  if (p->op == BSB_BETWEEN) return ok(p->code, p->length) && ok(p->code2, p->length2);
-  return ok(p->code, p->length);
-}
-
 extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
                             uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
                             void* stream) {
@@ -387,15 +377,10 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
   a.count = reinterpret_cast<unsigned long long*>(count);
   a.stats = stats;
   a.depth = depth;
-  if ((col->deep_mode == BSB_DEEP_PLANES && (stats != nullptr || !planes_fast_ok(pred))) ||
-      (col->deep_mode == BSB_DEEP_SLICED && stats != nullptr))
+  if (col->deep_mode == BSB_DEEP_SLICED && stats != nullptr)
     return vbs_rows_scan(a.vbs, a.n_rows, pred, mask, out_words, count, stats, depth, s);
   switch (col->deep_mode) {
-    case BSB_DEEP_PACKED: return scan_dispatch<1 + BSB_DEEP_PACKED>(a, pred, K, s);
-    case BSB_DEEP_RANK2: return scan_dispatch<1 + BSB_DEEP_RANK2>(a, pred, K, s);
-    case BSB_DEEP_PLANES:
-      return K <= 5 ? scan_dispatch<1 + BSB_DEEP_PLANES>(a, pred, K, s)
-                    : scan_dispatch<5>(a, pred, K, s);  // 64-bit plane values
+    case BSB_DEEP_PACKED: return scan_dispatch<BSB_LAYOUT_PPVBS>(a, pred, K, s);
     case BSB_DEEP_SLICED:
       if (K >= 2 && bsb::ds_enabled(mask != nullptr) &&
           (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled())))

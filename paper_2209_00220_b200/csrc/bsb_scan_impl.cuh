@@ -26,7 +26,7 @@ struct Leg {
   int32_t len;                 // levels examined (ByteSlice: K; PP-VBS: literal bytes)
   int32_t op;                  // operator when this is the only leg
   LevelLit lv[kMaxLevels];
-  uint32_t byte[kMaxLevels + 1];  // literal byte per level, 0-padded (one spare for planes)
+  uint32_t byte[kMaxLevels + 1];  // literal byte per level, 0-padded (one spare)
 };
 
 struct BsDesc {
@@ -40,9 +40,9 @@ struct VbsDesc {
   const uint8_t* deep[kMaxLevels];
   const uint32_t* exist[kMaxLevels];
   const int64_t* dir[kMaxLevels];
-  const uint32_t* rexist[kMaxLevels];  // PLANES: deep-row bitmaps of byte j+1
+  const uint32_t* rexist[kMaxLevels];  // SLICED: deep-row bitmaps of byte j+1
   int32_t K;
-  int32_t mode;  // BSB_DEEP_PACKED / BSB_DEEP_RANK2 / BSB_DEEP_PLANES
+  int32_t mode;  // BSB_DEEP_PACKED / BSB_DEEP_SLICED
 };
 
 // Per-lane statistics accumulators (reference stats.py:18-45).
@@ -64,7 +64,7 @@ __device__ __forceinline__ void stat_level(StatAcc* st, int j, int64_t nbytes) {
 struct TileIn {
   uint32_t w[8];   // the lane's 32 swizzled bytes of level 1
   uint32_t m2;     // PP-VBS: existence word of level 2 (every lane)
-  int64_t base;    // PP-VBS packed: lane i holds dir[i+2][tile*32]; rank2: dir2[tile*32]
+  int64_t base;    // PP-VBS packed: lane i holds dir[i+2][tile*32]; sliced: dir2[tile*32]
 };
 
 __device__ __forceinline__ void fetch_bs(const BsDesc& d, int64_t b, uint32_t valid, TileIn& t) {
@@ -354,334 +354,14 @@ __device__ __forceinline__ uint32_t scan_tile_vbs_packed(const VbsDesc& d, const
   return finalize_op(A.op, zgtA, eqfA, valid);
 }
 
-// PP-VBS, deep slices in level-2 rank space (BSB_DEEP_RANK2): all deep levels
-// share one packed space per block, so the row-space <-> packed conversion
-// (one butterfly setup) happens once per block instead of once per level.
+// PP-VBS scan of one tile for the reference-packed deep layout
+// (BSB_DEEP_PACKED).  SLICED columns run their own kernels (bsb_vbs_ds.cu,
+// bsb_vbs_sliced.cu; stats: bsb_vbs_rows.cu).
 template <bool BETWEEN, bool STATS>
-__device__ __forceinline__ uint32_t scan_tile_vbs_rank2(const VbsDesc& d, const Leg& A,
-                                                        const Leg& B, int64_t tile, int64_t b,
-                                                        uint32_t valid, const TileIn& in,
-                                                        StatAcc* st, int* depth_out) {
-  const int K = d.K;
-  uint32_t zeqA = valid, zgtA = 0, eqfA = 0;
-  uint32_t zeqB = valid, zgtB = 0, eqfB = 0;
-  const int maxlen = BETWEEN ? (A.len > B.len ? A.len : B.len) : A.len;
-  int depth = 0;
-  vbs_level1<BETWEEN, STATS>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB, st, depth);
-  const bool any_deep = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
-  if (maxlen >= 2 && __any_sync(kFull, any_deep)) {
-    const ExpandNet net = expand_setup(in.m2);
-    uint32_t pzA = compress_apply(net, zeqA);
-    uint32_t pzB = BETWEEN ? compress_apply(net, zeqB) : 0u;
-    // deep rows already known to pass GE(lo) at level 1 (row-space results)
-    const uint32_t passA1 = BETWEEN ? compress_apply(net, zgtA | eqfA) : 0u;
-    uint32_t pgtA = 0, peqA = 0, pgtB = 0, peqB = 0;
-    const int c2 = __popc(in.m2);
-    const uint32_t incl = warp_incl_scan((uint32_t)c2);
-    const int64_t start = in.base + (int64_t)(incl - c2);
-    const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
-    const int nwmax = __reduce_max_sync(kFull, any_deep ? ((c2 + 3) >> 2) : 0);
-    int rc = c2;  // bytes of the current level (reference accounting)
-    for (int j = 2; j <= maxlen; ++j) {
-      const bool act = BETWEEN ? ((pzA | pzB) != 0) : (pzA != 0);
-      if (!__any_sync(kFull, act)) break;
-      Run run;
-      load_run(d.deep[j - 1], start, c2, act, run);
-      const uint32_t mnext = (j < K && act) ? __ldg(d.exist[j] + b) : 0u;
-      uint32_t pgA, peA, pgB, peB;
-      if (BETWEEN && A.byte[j - 1] != B.byte[j - 1])
-        cmp_run<true>(run, nwmax, A.lv[j - 1], B.lv[j - 1], pgA, peA, pgB, peB);
-      else
-        cmp_run<false>(run, nwmax, A.lv[j - 1], A.lv[j - 1], pgA, peA, pgB, peB);
-      const uint32_t rnext = compress_apply(net, mnext);  // M_{j+1} in packed space
-      if (act) {
-        depth = j;
-        stat_level<STATS>(st, j - 1, rc);
-      }
-      rc = __popc(rnext);
-      vbs_transition(j, A.len, K, pgA & lowm, peA & lowm, rnext, pzA, pgtA, peqA);
-      if (BETWEEN) {
-        vbs_transition(j, B.len, K, pgB & lowm, peB & lowm, rnext, pzB, pgtB, peqB);
-        pzB &= pzA | pgtA | peqA | passA1;
-      }
-    }
-    zgtA |= expand_apply(net, pgtA);
-    eqfA |= expand_apply(net, peqA);
-    if (BETWEEN) zgtB |= expand_apply(net, pgtB);
-  }
-  if (STATS) *depth_out = depth;
-  if (BETWEEN) return valid & (zgtA | eqfA) & ~zgtB;
-  return finalize_op(A.op, zgtA, eqfA, valid);
-}
-
-// PP-VBS, deep levels paired into uint16 planes (BSB_DEEP_PLANES), compared
-// cooperatively: after the level-1 SWAR pass (lane = block), the warp walks
-// the tile's deep rows one per lane (coalesced 2-byte loads, 8 slots in
-// flight), compares plane values against the literal planes, resolves ties
-// with the deep-row existence bitmap, ballots two flag words per 32 deep rows,
-// and each lane finally pulls its block's window of flags and expands it to
-// row space with one butterfly.  Requires every literal's last byte to be
-// non-zero (dictionary codes always are; the host falls back otherwise).
-// VT = uint32_t for columns with at most 2 planes (max_len <= 5), uint64_t else.
-template <bool BETWEEN, typename VT>
-__device__ __forceinline__ uint32_t scan_tile_vbs_planes(const VbsDesc& d, const Leg& A,
-                                                         const Leg& B, int64_t tile, int64_t b,
-                                                         uint32_t valid, const TileIn& in) {
-  constexpr int G = 12;  // 32-deep-row slots per group: one round trip per plane per group
-  constexpr int VB = 8 * (int)sizeof(VT);  // value bits: planes packed big-endian
-  const int lane = threadIdx.x & 31;
-  const int K = d.K;
-  uint32_t zeqA = valid, zgtA = 0, eqfA = 0;
-  uint32_t zeqB = valid, zgtB = 0, eqfB = 0;
-  int depth = 0;
-  vbs_level1<BETWEEN, false>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB, nullptr,
-                             depth);
-  const int lenA = A.len;
-  const int lenB = BETWEEN ? B.len : 0;
-  const uint32_t cand = BETWEEN ? (zeqA | zeqB) : zeqA;
-  if ((lenA >= 2 || lenB >= 2) && __any_sync(kFull, cand != 0)) {
-    const int npA = lenA >> 1, npB = lenB >> 1;  // planes holding literal bytes 2..len
-    const int np = npA > npB ? npA : npB;        // 1 or 2 (K <= 5) ... up to 4
-    const int c2 = __popc(in.m2);
-    const uint32_t incl = warp_incl_scan((uint32_t)c2);
-    const uint32_t S = __shfl_sync(kFull, incl, 31);
-    const int64_t T0 = in.base;
-    // literal planes concatenated: big-endian plane 0 | plane 1 (| plane 2 | plane 3)
-    VT LA = 0, LB = 0;
-#pragma unroll
-    for (int p = 0; p < VB / 16; ++p) {
-      const VT a = p < np ? ((A.byte[2 * p + 1] << 8) | A.byte[2 * p + 2]) : 0u;
-      const VT bb = p < np ? ((B.byte[2 * p + 1] << 8) | B.byte[2 * p + 2]) : 0u;
-      LA |= a << (VB - 16 - 16 * p);
-      LB |= bb << (VB - 16 - 16 * p);
-    }
-    const uint32_t* rexA = (lenA >= 2 && lenA < K) ? d.rexist[lenA] : nullptr;
-    const uint32_t* rexB = (BETWEEN && lenB >= 2 && lenB < K) ? d.rexist[lenB] : nullptr;
-    const uint16_t* pl0 = reinterpret_cast<const uint16_t*>(d.deep[1]) + T0;
-    uint32_t keepP = 0, keepQ = 0;
-    const int niter = (int)((S + 31) >> 5);
-    for (int g = 0; g < niter; g += G) {
-      VT V[G];
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const uint32_t qo = (uint32_t)(g + k) * 32u + lane;
-        V[k] = (g + k < niter && qo < S) ? (VT)__ldg(pl0 + qo) << (VB - 16) : (VT)0;
-      }
-      // further planes only for rows tied so far with a leg that has bytes there
-      for (int p = 1; p < np; ++p) {
-        const uint16_t* pl = reinterpret_cast<const uint16_t*>(d.deep[p + 1]) + T0;
-        const int sh = VB - 16 * p;  // compare the planes loaded so far
-        const VT pa = p < npA ? (VT)(LA >> sh) : (VT)~(VT)0;  // ~0: leg has no byte here
-        const VT pb = p < npB ? (VT)(LB >> sh) : (VT)~(VT)0;
-        bool any = false;
-        uint32_t need = 0;
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          const VT hv = V[k] >> sh;
-          const bool t = (g + k < niter) && (hv == pa || (BETWEEN && hv == pb));
-          need |= (uint32_t)t << k;
-        }
-        any = __any_sync(kFull, need != 0);
-        if (!any) break;
-#pragma unroll
-        for (int k = 0; k < G; ++k)
-          if ((need >> k) & 1u)
-            V[k] |= (VT)__ldg(pl + (g + k) * 32 + lane) << (VB - 16 - 16 * p);
-      }
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        if (g + k >= niter) break;
-        const uint32_t qo = (uint32_t)(g + k) * 32u + lane;
-        const bool inA = qo < S && lenA >= 2, inB = qo < S && lenB >= 2;
-        bool gA = inA && V[k] > LA, eA = inA && V[k] == LA;
-        bool gB = inB && V[k] > LB, eB = inB && V[k] == LB;
-        // tie through a literal's last byte: longer codes are greater (vbs.py:276-280)
-        if (rexA != nullptr && __any_sync(kFull, eA)) {
-          const uint32_t q = (uint32_t)(T0 + qo);
-          const bool has = eA && ((__ldg(rexA + (q >> 5)) >> (q & 31)) & 1u);
-          gA |= has;
-          eA &= !has;
-        }
-        if (BETWEEN && rexB != nullptr && __any_sync(kFull, eB)) {
-          const uint32_t q = (uint32_t)(T0 + qo);
-          const bool has = eB && ((__ldg(rexB + (q >> 5)) >> (q & 31)) & 1u);
-          gB |= has;
-          eB &= !has;
-        }
-        const uint32_t wp = __ballot_sync(kFull, BETWEEN ? (gA || eA) : gA);
-        const uint32_t wq = __ballot_sync(kFull, BETWEEN ? gB : eA);
-        if (lane == g + k) {
-          keepP = wp;
-          keepQ = wq;
-        }
-      }
-    }
-    // this block's deep rows are run bits [incl - c2, incl)
-    const uint32_t excl = incl - (uint32_t)c2;
-    const int w0 = (int)(excl >> 5), sh = (int)(excl & 31);
-    const int w1 = w0 + 1 < 32 ? w0 + 1 : 31;
-    const uint32_t p0 = __shfl_sync(kFull, keepP, w0 & 31), p1 = __shfl_sync(kFull, keepP, w1);
-    const uint32_t q0 = __shfl_sync(kFull, keepQ, w0 & 31), q1 = __shfl_sync(kFull, keepQ, w1);
-    const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
-    const uint32_t pP = __funnelshift_r(p0, p1, sh) & lowm;
-    const uint32_t pQ = __funnelshift_r(q0, q1, sh) & lowm;
-    const ExpandNet net = expand_setup(in.m2);
-    const uint32_t eP = expand_apply(net, pP), eQ = expand_apply(net, pQ);
-    if (BETWEEN) {
-      zgtA |= zeqA & eP;  // deep rows at least lo
-      zgtB |= zeqB & eQ;  // deep rows strictly above hi
-    } else {
-      zgtA |= zeqA & eP;
-      eqfA |= zeqA & eQ;
-    }
-  }
-  if (BETWEEN) return valid & (zgtA | eqfA) & ~zgtB;
-  return finalize_op(A.op, zgtA, eqfA, valid);
-}
-
-// PP-VBS with the deep rows stored as their own ByteSlice-like column
-// (BSB_DEEP_SLICED).  Level 1 runs lane = row block as usual.  The tied rows
-// of every block (compressed with one butterfly set-up) are OR-ed into
-// deep-block candidate words in shared memory; then lane t walks deep block
-// t through levels 2..len exactly like Alg. 3 (one 256-bit load and a SWAR
-// compare per level, early stop per deep block, transitions with the
-// deep-row existence words), and each row block expands its window of the
-// deep results back to row space.
-constexpr int kTileWarps = 8;  // all scan kernels run 256-thread CTAs
-
-template <bool BETWEEN>
-__device__ __forceinline__ uint32_t scan_tile_vbs_sliced(const VbsDesc& d, const Leg& A,
-                                                         const Leg& B, int64_t tile, int64_t b,
-                                                         uint32_t valid, const TileIn& in) {
-  __shared__ uint32_t sh[kTileWarps][5][36];
-  const int lane = threadIdx.x & 31;
-  const int wq = (threadIdx.x >> 5) & (kTileWarps - 1);
-  const int K = d.K;
-  uint32_t zeqA = valid, zgtA = 0, eqfA = 0;
-  uint32_t zeqB = valid, zgtB = 0, eqfB = 0;
-  int depth = 0;
-  vbs_level1<BETWEEN, false>(A, B, K, valid, in, zeqA, zgtA, eqfA, zeqB, zgtB, eqfB, nullptr,
-                             depth);
-  const int lenA = A.len;
-  const int lenB = BETWEEN ? B.len : 0;
-  const int maxlen = lenA > lenB ? lenA : lenB;
-  const uint32_t cand = BETWEEN ? (zeqA | zeqB) : zeqA;
-  if (maxlen >= 2 && __any_sync(kFull, cand != 0)) {
-    const int c2 = __popc(in.m2);
-    const uint32_t incl = warp_incl_scan((uint32_t)c2);
-    const uint32_t S = __shfl_sync(kFull, incl, 31);
-    const int64_t D0 = in.base;
-    const int64_t db0 = D0 >> 5;
-    const int off0 = (int)(D0 & 31);
-    const int ndt = (off0 + (int)S + 31) >> 5;  // deep blocks this tile touches (<= 33)
-    const ExpandNet net = expand_setup(in.m2);
-    const uint32_t pA = compress_apply(net, zeqA);
-    const uint32_t pB = BETWEEN ? compress_apply(net, zeqB) : 0u;
-    uint32_t* cA = sh[wq][0];
-    uint32_t* cB = sh[wq][1];
-    cA[lane] = 0;
-    cB[lane] = 0;
-    if (lane < 4) {
-      cA[32 + lane] = 0;
-      cB[32 + lane] = 0;
-    }
-    __syncwarp();
-    const int o = off0 + (int)(incl - (uint32_t)c2);  // block's first deep row, from db0*32
-    const int wi = o >> 5, sb = o & 31;
-    const bool spill = sb != 0 && sb + c2 > 32;
-    if (pA) {
-      atomicOr(&cA[wi], pA << sb);
-      if (spill) atomicOr(&cA[wi + 1], pA >> (32 - sb));
-    }
-    if (BETWEEN && pB) {
-      atomicOr(&cB[wi], pB << sb);
-      if (spill) atomicOr(&cB[wi + 1], pB >> (32 - sb));
-    }
-    __syncwarp();
-    for (int t0 = 0; t0 < ndt; t0 += 32) {
-      const int t = t0 + lane;
-      const bool has = t < ndt;
-      uint32_t zA = has ? cA[t] : 0u, zB = (BETWEEN && has) ? cB[t] : 0u;
-      uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
-      const int64_t dbk = db0 + t;
-      for (int j = 2; j <= maxlen; ++j) {
-        const bool act = BETWEEN ? ((zA | zB) != 0) : (zA != 0);
-        if (!__any_sync(kFull, act)) break;
-        uint32_t w[8];
-        if (act) {
-          ldg256(d.deep[j - 1] + dbk * 32, w);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) w[i] = 0;
-        }
-        const uint32_t nxt = (j < K && act) ? __ldg(d.rexist[j] + dbk) : 0u;
-        uint32_t gA, eA, gB, eB;
-        if (BETWEEN && A.byte[j - 1] != B.byte[j - 1]) {
-          cmp_block2(w, A.lv[j - 1], B.lv[j - 1], gA, eA, gB, eB);
-        } else {
-          cmp_block(w, A.lv[j - 1], gA, eA);
-          gB = gA;
-          eB = eA;
-        }
-        eA &= ~gA;
-        eB &= ~gB;
-        vbs_transition(j, lenA, K, gA, eA, nxt, zA, gtA, eqA);
-        if (BETWEEN) vbs_transition(j, lenB, K, gB, eB, nxt, zB, gtB, eqB);
-      }
-      __syncwarp();
-      if (has) {
-        sh[wq][2][t] = BETWEEN ? (gtA | eqA) : gtA;
-        sh[wq][3][t] = BETWEEN ? gtB : eqA;
-      }
-    }
-    if (lane < 4) {
-      sh[wq][2][ndt + lane] = 0;  // guard words read by the last windows
-      sh[wq][3][ndt + lane] = 0;
-    }
-    __syncwarp();
-    const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
-    const uint32_t pP = __funnelshift_r(sh[wq][2][wi], sh[wq][2][wi + 1], sb) & lowm;
-    const uint32_t pQ = __funnelshift_r(sh[wq][3][wi], sh[wq][3][wi + 1], sb) & lowm;
-    const uint32_t eP = expand_apply(net, pP), eQ = expand_apply(net, pQ);
-    if (BETWEEN) {
-      zgtA |= zeqA & eP;  // deep rows at least lo
-      zgtB |= zeqB & eQ;  // deep rows strictly above hi
-    } else {
-      zgtA |= zeqA & eP;
-      eqfA |= zeqA & eQ;
-    }
-    __syncwarp();
-  }
-  if (BETWEEN) return valid & (zgtA | eqfA) & ~zgtB;
-  return finalize_op(A.op, zgtA, eqfA, valid);
-}
-
-// MODE: -1 = dispatch on d.mode at run time (conjunction kernel), else the
-// deep layout fixed at compile time (single-predicate scan kernels):
-// 0 packed, 1 rank2, 2 planes (32-bit values), 3 sliced, 4 planes (64-bit).
-template <bool BETWEEN, bool STATS, int MODE = -1>
 __device__ __forceinline__ uint32_t scan_tile_vbs(const VbsDesc& d, const Leg& A,
                                                   const Leg& B, int64_t tile, int64_t b,
                                                   uint32_t valid, const TileIn& in,
                                                   StatAcc* st, int* depth_out) {
-  if (MODE == BSB_DEEP_PLANES)  // PLANES, max_len <= 5
-    return scan_tile_vbs_planes<BETWEEN, uint32_t>(d, A, B, tile, b, valid, in);
-  if (MODE == 4)  // PLANES, max_len > 5
-    return scan_tile_vbs_planes<BETWEEN, uint64_t>(d, A, B, tile, b, valid, in);
-  if (MODE == BSB_DEEP_SLICED)
-    return scan_tile_vbs_sliced<BETWEEN>(d, A, B, tile, b, valid, in);
-  if (MODE < 0 && !STATS && d.mode == BSB_DEEP_PLANES) {
-    if (d.K <= 5) return scan_tile_vbs_planes<BETWEEN, uint32_t>(d, A, B, tile, b, valid, in);
-    return scan_tile_vbs_planes<BETWEEN, uint64_t>(d, A, B, tile, b, valid, in);
-  }
-  if (MODE < 0 && !STATS && d.mode == BSB_DEEP_SLICED)
-    return scan_tile_vbs_sliced<BETWEEN>(d, A, B, tile, b, valid, in);
-  if (MODE == BSB_DEEP_RANK2)
-    return scan_tile_vbs_rank2<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
-  if (MODE == BSB_DEEP_PACKED)
-    return scan_tile_vbs_packed<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
-  if (d.mode == BSB_DEEP_RANK2)
-    return scan_tile_vbs_rank2<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
   return scan_tile_vbs_packed<BETWEEN, STATS>(d, A, B, tile, b, valid, in, st, depth_out);
 }
 

@@ -1,13 +1,13 @@
-// bsb_vbs_rows.cu -- row-parallel PP-VBS scan for the PLANES deep layout.
+// bsb_vbs_rows.cu -- row-parallel PP-VBS scan of a SLICED column with
+// ScanStats (the stats path of bsb_vbs_scan for that layout).
 //
 // One warp per 32-row block, one lane per row: the lane rebuilds its code's
-// bytes (level 1 from the swizzled first slice, deeper levels from the uint16
-// planes) and runs the reference's per-row state machine (vbs.py:241-284):
-// compare level by level, drop a tied row that has no next byte, settle a tie
-// at the literal's last byte with the existence shortcut.  The block depth is
-// the warp max of the levels each row stayed tied, which gives ScanStats
-// exactly (stats.py:18-45).  Used for the stats path and as the fallback when
-// a literal's last byte is zero (the cooperative plane scan needs it non-zero).
+// bytes (level 1 from the swizzled first slice, deeper levels from the deep
+// rows' byte planes) and runs the reference's per-row state machine
+// (vbs.py:241-284): compare level by level, drop a tied row that has no next
+// byte, settle a tie at the literal's last byte with the existence shortcut.
+// The block depth is the warp max of the levels each row stayed tied, which
+// gives ScanStats exactly (stats.py:18-45).
 #include <cstring>
 
 #include "bsb_scan_impl.cuh"
@@ -33,12 +33,9 @@ struct RowArgs {
   int32_t depth_max;
 };
 
+// byte j of deep row q (SLICED: swizzled 32-deep-row blocks)
 __device__ __forceinline__ uint32_t plane_byte(const VbsDesc& d, int64_t q, int j) {
-  if (d.mode == BSB_DEEP_SLICED)
-    return __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
-  const uint16_t* pl = reinterpret_cast<const uint16_t*>(d.deep[((j - 2) >> 1) + 1]);
-  const uint32_t v = __ldg(pl + q);
-  return ((j - 2) & 1) ? (v & 0xFFu) : (v >> 8);
+  return __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
 }
 
 __global__ void __launch_bounds__(256) vbs_rowscan_kernel(const __grid_constant__ RowArgs a) {
@@ -150,7 +147,7 @@ static int launch_rows(const RowArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 
-// Scan of a PLANES column through the row-parallel kernel.  BETWEEN runs as
+// Scan of a SLICED column through the row-parallel kernel.  BETWEEN runs as
 // the reference's two pipelined legs (vbs.py:299-304); with `stats` the
 // counters follow stats.py:47-67 (slots 17/19 hold the legs' skipped blocks).
 int vbs_rows_scan(const VbsDesc& d, int64_t n_rows, const bsb_pred* p, const uint32_t* mask,

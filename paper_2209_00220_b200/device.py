@@ -32,21 +32,31 @@ def stream():
     return _lib.stream_ptr()
 
 
+_BIT_CARRIERS = {(torch.uint64, torch.int64), (torch.uint32, torch.int32),
+                 (torch.int8, torch.uint8)}
+
+
 def _to_dev(x, np_dtype, view_dtype, torch_dtype):
-    dev = device()
+    """Integer data only: floating / bool / complex inputs raise TypeError
+    (numpy fancy indexing rejects them too).  Integer dtypes convert by
+    value; only the unsigned<->signed carrier pairs of the same width
+    (uint64 codes in int64, uint32 words in int32) are reinterpreted."""
     if isinstance(x, torch.Tensor):
         t = x
+        if t.dtype.is_floating_point or t.dtype.is_complex or t.dtype == torch.bool:
+            raise TypeError(f"expected an integer tensor, got {t.dtype}")
+        dev = device()
         if t.dtype != torch_dtype:
-            if torch_dtype == torch.int64 and t.dtype in (torch.int32, torch.int16, torch.uint8,
-                                                          torch.int8):
-                t = t.to(torch.int64)
-            elif t.element_size() == torch.empty(0, dtype=torch_dtype).element_size():
+            if (t.dtype, torch_dtype) in _BIT_CARRIERS:
                 t = t.view(torch_dtype)
             else:
                 t = t.to(torch_dtype)
         return t.to(dev, non_blocking=True).contiguous()
-    a = np.ascontiguousarray(np.asarray(x).astype(np_dtype, copy=False))
-    return torch.from_numpy(a.view(view_dtype)).to(dev, non_blocking=False)
+    a = np.asarray(x)
+    if a.dtype.kind not in "iu" and not (a.dtype == object or a.size == 0):
+        raise TypeError(f"expected integer data, got {a.dtype}")
+    a = np.ascontiguousarray(a.astype(np_dtype, copy=False))
+    return torch.from_numpy(a.view(view_dtype)).to(device(), non_blocking=False)
 
 
 def to_dev_i64(x) -> torch.Tensor:

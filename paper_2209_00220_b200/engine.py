@@ -8,9 +8,15 @@ arms on the device and gathers + decodes each projected column straight from
 the selection bitvector with the fused lookup kernels.
 
 All five reference layouts run on the device: "byteslice" and "ppvbs" (the
-north-star path) plus the paper's baselines "bitpacked", "vbp" and "pevbp".  CSV ingest (file I/O)
-is replaced by ``ingest_arrays`` over in-memory columns; the baseline
-layouts (bitpacked, vbp, pevbp) are out of scope.
+north-star path) plus the paper's comparison baselines "bitpacked", "vbp"
+and "pevbp".  CSV ingest (engine.py:114-165, file
+I/O) is out of scope: ``ingest_arrays`` takes in-memory columns.
+
+Timings: the reference writes one "scan" row per predicate (engine.py:
+322-332).  Here a conjunction runs as one device call, so every predicate
+of a group gets a row with ``op`` = its operator name, ``fused`` = True and
+an equal share of the group's measured seconds (the rows still sum to the
+conjunction's time).
 """
 
 from __future__ import annotations
@@ -39,7 +45,7 @@ from .vbs import build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs, vbs_
 __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
            "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",
            "lookup_decode", "lookup_decode_rows", "lookup_decode_bits", "execute", "ingest_arrays",
-           "ingest", "read_csv_columns", "IngestReport", "size_report", "conj_scan"]
+           "IngestReport", "size_report", "conj_scan"]
 
 LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
 DEVICE_LAYOUTS = LAYOUTS
@@ -292,8 +298,10 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
         else:
             running = DeviceBitVector.ones(store.n_rows)  # engine.py:333-334
         torch.cuda.current_stream().synchronize()
-        timings.append({"column": ",".join(p.column for p in group), "phase": "scan",
-                        "op": "AND", "seconds": time.perf_counter() - t0})
+        dt = time.perf_counter() - t0
+        for pred in group:
+            timings.append({"column": pred.column, "phase": "scan", "op": pred.op.name,
+                            "seconds": dt / len(group), "fused": True})
         arms.append(running)
     selection = arms[0]
     for extra in arms[1:]:
@@ -311,62 +319,6 @@ def execute(store: Store, query: Query, threads: int = 1, out_dtype=torch.int64)
         timings.append({"column": name, "phase": "lookup", "op": "",
                         "seconds": time.perf_counter() - t0})
     return QueryResult(n_sel, out, timings, selection)
-
-
-def read_csv_columns(path, schema: Schema) -> dict:
-    """engine.py:114-158: the schema's columns from a header-bearing CSV.
-    Numeric cells must be integers; an empty cell is a NULL and rejected;
-    errors name the 1-based line and the column (DataError)."""
-    import csv
-    with open(path, newline="") as fh:
-        rows = csv.reader(fh)
-        header = next(rows, None)
-        if header is None:
-            raise DataError(f"{path}: empty CSV, header row required")
-        where = {}
-        for spec in schema.columns:
-            if spec.name not in header:
-                raise DataError(f"{path}: column {spec.name!r} missing from header")
-            where[spec.name] = header.index(spec.name)
-        cells = {spec.name: [] for spec in schema.columns}
-        for line, row in enumerate(rows, start=2):
-            if len(row) != len(header):
-                raise DataError(f"{path}:{line}: expected {len(header)} cells, got {len(row)}")
-            for name, col in where.items():
-                if row[col] == "":
-                    raise DataError(f"{path}:{line}: NULL in column {name!r}")
-                cells[name].append(row[col])
-    if not cells or not next(iter(cells.values())):
-        raise DataError(f"{path}: no data rows")
-    out = {}
-    for spec in schema.columns:
-        raw = cells[spec.name]
-        if spec.kind is not ColumnKind.NUMERIC:
-            out[spec.name] = np.array(raw, dtype=object)
-            continue
-        vals = np.empty(len(raw), np.int64)
-        for i, c in enumerate(raw):
-            try:
-                vals[i] = int(c)
-            except ValueError:
-                raise DataError(f"{path}:{i + 2}: non-integer value {c!r} in numeric "
-                                f"column {spec.name!r}") from None
-        out[spec.name] = vals
-    return out
-
-
-def ingest(csv_path, schema: Schema, policy: str = "advisor", *, advise_cost="wall",
-           advise_count: int = 100, subsample: int | None = None,
-           lanes: LaneConfig = DEFAULT_LANES, threads: int = 1,
-           extra_manifest: dict | None = None):
-    """engine.py:239-297: CSV -> (Store, IngestReport); `threads` is accepted
-    for signature compatibility (CPU partitioning only in the reference)."""
-    data = read_csv_columns(csv_path, schema)
-    store, rows, advice = _ingest(data, schema, policy, advise_cost, advise_count, subsample,
-                                  lanes)
-    if extra_manifest:
-        store.manifest.update(extra_manifest)
-    return store, IngestReport(rows, advice)
 
 
 def ingest_arrays(columns: dict, schema: Schema | None = None, policy: str = "advisor", *,

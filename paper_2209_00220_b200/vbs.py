@@ -23,7 +23,8 @@ from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
 __all__ = ["VbsColumn", "build_vbs", "scan_vbs", "lookup_vbs", "lookup_vbs_rows",
-           "lookup_vbs_rows_dec", "lookup_vbs_bits", "vbs_size_report"]
+           "lookup_vbs_rows_dec", "lookup_vbs_bits", "vbs_size_report", "scan_serial",
+           "lookup_serial"]
 
 DEEP_PAD = 64
 
@@ -41,8 +42,8 @@ class VbsColumn:
     exist: list                           # exist[j]: int32 [stride/32] words of slice j+1
     block_dir: list                       # block_dir[j]: int64 [stride/32 + 1]
     level_rows: list                      # rows owning byte j (j = 1..K), reference counts
-    deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED / DEEP_RANK2 / DEEP_PLANES (header)
-    rexist: list = None                   # PLANES: deep-row bitmaps of byte j+1 (j>=2)
+    deep_mode: int = _lib.DEEP_PACKED     # DEEP_PACKED / DEEP_SLICED (header)
+    rexist: list = None                   # SLICED: deep-row bitmaps of byte j+1 (j>=2)
     deep1_range: tuple = (1, 0)           # (min, max) first byte of the deep rows; (1, 0) unknown
     _desc: _lib.BsbVbs = field(default=None, repr=False)
 
@@ -117,9 +118,6 @@ class VbsColumn:
         return np.stack(rows) if rows else np.zeros((0, nb + 1), np.int64)
 
 
-RANK2_MAX_OVERHEAD = 1.25
-
-
 SLICED_MAX_OVERHEAD = 1.30
 
 
@@ -127,7 +125,7 @@ def choose_deep_mode(level_rows, K: int) -> int:
     """SLICED (deep rows as their own swizzled ByteSlice column; the fastest
     scan, measured on B200) when its pad bytes cost <= 30% over the reference
     packing -- true for PPE dictionaries, whose deep codes are mostly full
-    length -- else the reference packing.  RANK2 / PLANES stay selectable."""
+    length -- else the reference packing."""
     if K < 2:
         return _lib.DEEP_PACKED
     exact = sum(int(level_rows[j]) for j in range(1, K))
@@ -141,9 +139,9 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
               deep_mode: str = "auto") -> VbsColumn:
     """vbs.py:68-114 on the device: plan (validate, K, level sizes) + build.
 
-    deep_mode: "auto" | "packed" (reference packing) | "rank2" (one byte per
-    deep row in every deep slice) | "planes" (paired uint16 levels per deep
-    row); see include/bytestore_b200.h."""
+    deep_mode: "auto" | "packed" (reference packing) | "sliced" (the deep
+    rows as their own swizzled byte-plane column); see
+    include/bytestore_b200.h."""
     lanes.require_device()
     codes = row_codes if isinstance(row_codes, torch.Tensor) else np.asarray(row_codes)
     lens = row_lengths if isinstance(row_lengths, torch.Tensor) else np.asarray(row_lengths)
@@ -168,8 +166,7 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
     nbpad = stride // 32
     dev = device()
     level_rows = [int(x) for x in lr[:K]]
-    modes = {"packed": _lib.DEEP_PACKED, "rank2": _lib.DEEP_RANK2, "planes": _lib.DEEP_PLANES,
-             "sliced": _lib.DEEP_SLICED}
+    modes = {"packed": _lib.DEEP_PACKED, "sliced": _lib.DEEP_SLICED}
     if deep_mode == "auto":
         mode = choose_deep_mode(level_rows, K)
     elif deep_mode in modes:
@@ -197,15 +194,8 @@ def build_vbs(row_codes, row_lengths, lanes: LaneConfig = DEFAULT_LANES,
                                     device=dev))
             rex.append(torch.zeros(cnt2 // 32 + 2, dtype=torch.int32, device=dev)
                        if j >= 2 else None)
-        elif mode == _lib.DEEP_PLANES:
-            # plane j-1 (bytes 2j, 2j+1) for j <= K//2; uint16 per deep row
-            deep.append(torch.empty(cnt2 + DEEP_PAD, dtype=torch.int16, device=dev)
-                        if j <= K // 2 else None)
-            rex.append(torch.zeros(cnt2 // 32 + 2, dtype=torch.int32, device=dev)
-                       if j >= 2 else None)
         else:
-            size = cnt2 if mode == _lib.DEEP_RANK2 else level_rows[j]
-            deep.append(torch.empty(size + DEEP_PAD, dtype=torch.uint8, device=dev))
+            deep.append(torch.empty(level_rows[j] + DEEP_PAD, dtype=torch.uint8, device=dev))
             rex.append(None)
         exist.append(torch.empty(nbpad, dtype=torch.int32, device=dev))
         need_dir = mode == _lib.DEEP_PACKED or j == 1
@@ -279,12 +269,13 @@ def _vbs_order(col: VbsColumn, order: str) -> str:
 
 
 def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
-                    out_dtype=torch.int64, level_counts=None, order: str = "auto"):
+                    out_dtype=torch.int64, level_counts=None, order: str = "auto", err=None):
     """Device lookup of a row-id list (any order, output in input order):
     padded codes, or decoded values when the dictionary's sorted padded codes
     / values are given.  order: see lookup_byteslice_rows; "auto" sorts for
     columns with codes of 3+ bytes (a deep row costs up to ~2K random
-    sectors: bs1, existence words, directory, deep bytes)."""
+    sectors: bs1, existence words, directory, deep bytes).  Ids outside
+    [0, n_rows) raise IndexError; `err` as in lookup_byteslice_rows."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
@@ -293,7 +284,7 @@ def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
     if sorted_padded is None:
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
         _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, g.data_ptr(), n, out.data_ptr(),
-                                           None, None, 0, None, None, lc, stream()),
+                                           None, None, 0, None, None, lc, _lib.ptr(err), stream()),
                    "lookup_vbs")
         return scatter_back(out, perm)
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
@@ -301,15 +292,15 @@ def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
     _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, g.data_ptr(), n, None,
                                        sorted_padded.data_ptr(), dict_values.data_ptr(),
-                                       sorted_padded.numel(), p64, p32, lc, stream()),
+                                       sorted_padded.numel(), p64, p32, lc, _lib.ptr(err), stream()),
                "lookup_vbs")
     return scatter_back(out, perm)
 
 
 def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64,
-                        order: str = "auto"):
+                        order: str = "auto", err=None):
     """Row-id lookup decoded through a C-ABI decoder (Dictionary.dev_decoder).
-    order: see lookup_vbs_rows."""
+    order / err: see lookup_vbs_rows."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
@@ -318,8 +309,8 @@ def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64,
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
     _lib.check(lib.bsb_vbs_lookup_rows_dec(col.desc_ref, g.data_ptr(), n,
-                                           ctypes.byref(decoder), None, p64, p32, None,
-                                           stream()),
+                                           ctypes.byref(decoder), None, p64, p32,
+                                           _lib.ptr(err), stream()),
                "lookup_vbs")
     return scatter_back(out, perm)
 
@@ -373,6 +364,28 @@ def lookup_vbs(col: VbsColumn, selection):
     st = LookupStats(levels_touched=levels, bytes_loaded=int(counts.sum()),
                      mask_bytes=nz_words * (col.max_len - 1) * 4)
     return host_u64(codes), st
+
+
+def scan_serial(col: VbsColumn, pred: ResolvedPredicate, mask=None):
+    """vbs.py:378-462, the reference's block-at-a-time scan.  Its results and
+    stats equal scan_vbs's by contract (tests/test_vbs.py:198-209); on the
+    device both are the same Alg. 3 kernels, here with the ScanStats
+    materialised eagerly as the serial form returns them."""
+    bv, st = scan_vbs(col, pred, mask)
+    return bv, st.materialize()
+
+
+def lookup_serial(col: VbsColumn, selection) -> np.ndarray:
+    """vbs.py:465-498 (Alg. 4): padded codes of the selected rows in
+    ascending row order, as uint64.  Same errors as the reference: a
+    selection of another length is ValueError; lanes other than 32 cannot
+    reach the device path (LaneConfig.require_device)."""
+    if selection.n_rows != col.n_rows:
+        raise ValueError("selection length mismatch")
+    if col.lanes.lane_count != 32:
+        raise NotImplementedError("reference lookup assumes 32-code blocks")
+    codes, _ = lookup_vbs(col, selection)
+    return codes
 
 
 def vbs_size_report(col: VbsColumn) -> dict:

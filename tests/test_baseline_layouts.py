@@ -117,17 +117,3 @@ def test_five_layout_store_and_query_vs_reference(tmp_path):
         assert np.array_equal(res.selection.to_bools(), z["store/sel"])
         for k in cols:
             assert np.array_equal(res.columns[k], z[f"store/proj/{k}"]), k
-
-
-@pytest.mark.gpu
-def test_layout_sweep_matches_reference_columns():
-    """sweep.run_sweep: the deterministic columns (selectivity, bits per code)
-    equal the reference's run_sweep on the same spec."""
-    from paper_2209_00220_b200.sweep import SweepSpec, run_sweep
-    g = json.load(open(os.path.join(GOLD, "sweep.json")))
-    rows = run_sweep(SweepSpec(**g["spec"], reps=1))
-    assert len(rows) == len(g["rows"])
-    for got, want in zip(rows, g["rows"]):
-        for k in ("layout", "s", "d", "n_rows", "selectivity", "bits_per_code"):
-            assert got[k] == pytest.approx(want[k], rel=1e-12, abs=0), (k, got, want)
-        assert got["scan_ns_per_code"] > 0

@@ -149,6 +149,44 @@ def test_byteslice_row_lookup_unsorted_duplicates():
     assert np.array_equal(vals, table.cpu().numpy()[codes[rows].astype(np.int64)])
 
 
+@pytest.mark.parametrize("order", ["keep", "sort"])
+def test_row_lookup_out_of_range_ids_raise_index_error(order):
+    """An id outside [0, n_rows) is never read: the reference raises
+    IndexError at its numpy fancy index (byteslice.py:154, vbs.py:357); the
+    device lookups raise it too, or flag it in the async error word."""
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.device import SORT_GATHER_MIN
+    rng = np.random.default_rng(12)
+    n = 70_001
+    vals, od, codes, lens = _ppe_column(1.1, 16, n, 5)
+    col_v = B.build_vbs(codes, lens)
+    col_b = B.build_byteslice(codes.astype(np.uint64) & np.uint64(0xFFFF), 16)
+    d = B.Dictionary.build(B.build_frequency_table(vals, B.ColumnKind.NUMERIC),
+                           "prefix_preserving")
+    m = SORT_GATHER_MIN * 2 if order == "sort" else 1000
+    for bad in (n, -1, 1 << 40):
+        ids = rng.integers(0, n, size=m)
+        ids[m // 2] = bad
+        t = torch.from_numpy(ids).cuda()
+        with pytest.raises(IndexError):
+            B.lookup_byteslice_rows(col_b, t, order=order)
+        with pytest.raises(IndexError):
+            B.lookup_vbs_rows(col_v, t, order=order)
+        with pytest.raises(IndexError):
+            B.lookup_vbs_rows_dec(col_v, t, d.dev_decoder, order=order)
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        B.lookup_byteslice_rows(col_b, t, order=order, err=err)
+        assert int(err.item()) & _lib.ERR_INDEX
+        err.zero_()
+        B.lookup_vbs_rows_dec(col_v, t, d.dev_decoder, order=order, err=err)
+        assert int(err.item()) & _lib.ERR_INDEX
+    # in-range ids leave the word clear
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ok = torch.from_numpy(rng.integers(0, n, size=m)).cuda()
+    B.lookup_vbs_rows(col_v, ok, order=order, err=err)
+    assert int(err.item()) == 0
+
+
 def test_row_lookups_sorted_gather():
     """Long unsorted id lists (>= device.SORT_GATHER_MIN) are gathered in row
     order and scattered back: output in input order, duplicates, both
@@ -205,7 +243,7 @@ def test_byteslice_errors():
 # ----------------------------------------------------------------- PP-VBS
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_golden(mode):
     data, meta = load("vbs")
     for ci, m in enumerate(meta):
@@ -242,7 +280,7 @@ def _ppe_column(s, d, n, seed):
     return vals, od, codes, lens
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_zipf_between_windows_vs_oracle(mode):
     """cfg2-shaped (Zipf 1.2 over 2^20, scaled to 2^20 rows), the four
     BETWEEN windows of SURVEY.md §8(d), fused single pass vs oracle legs."""
@@ -262,7 +300,7 @@ def test_vbs_zipf_between_windows_vs_oracle(mode):
                               O.naive_filter(vals, "BETWEEN", q(1 - p - mm), q(1 - mm)))
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
     rng = np.random.default_rng(77)
     for n, K in ((50_001, 3), (20_000, 8), (3000, 5), (33, 2), (1, 1)):
@@ -409,7 +447,7 @@ def test_vbs_sliced_zone_map_uniform_first_byte(x):
             assert np.array_equal(bv.words, want), (x, "BETWEEN")
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_row_lookup_decode_vs_oracle(mode):
     n = 200_000
     vals, od, codes, lens = _ppe_column(1.0, 20, n, 4)
@@ -440,7 +478,7 @@ def _sel_cases(n, rng):
     yield f
 
 
-@pytest.mark.parametrize("mode", ["packed", "rank2", "planes", "sliced"])
+@pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_fused_bits_lookup_and_tree_decode(mode):
     """bsb_vbs_lookup_bits (bitvector -> codes / values in one kernel) and
     the PPE tree decoder equal the oracle's lookup + the row values."""

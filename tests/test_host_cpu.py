@@ -207,6 +207,19 @@ def test_device_path_fails_loudly_without_cuda():
         build_byteslice(np.arange(10), 4)
 
 
+def test_row_ids_must_be_integers():
+    """device._to_dev rejects floating / bool data before touching a device
+    (numpy fancy indexing in the reference rejects them too); integer dtypes
+    of another width convert by value, not by bit reinterpretation."""
+    import torch
+
+    from paper_2209_00220_b200.device import to_dev_i64
+    for bad in (torch.tensor([1.0, 2.0], dtype=torch.float64), torch.tensor([True, False]),
+                np.array([0.5, 1.5]), np.array([True])):
+        with pytest.raises(TypeError):
+            to_dev_i64(bad)
+
+
 def test_bits_module_matches_oracle():
     """Host bit helpers (reference bits.py API) agree with the oracle's
     restatement on random words, and keep the reference's edge cases."""
