@@ -1,19 +1,25 @@
 #!/usr/bin/env python
-"""ByteStore hot-path benchmark on B200 (BASELINE.json configs[1]).
+"""ByteStore hot-path benchmark on B200.
 
-Workload (one "step"): the cfg2 skewed column -- 2^28 rows of int values from
-a 2^20-value dictionary with Zipf(1.2) frequencies (seed 42), encoded both as
-PP-VBS (reference prefix-preserving codes, K=5) and as ByteSlice (w=20) --
-scanned with the four BETWEEN windows of SURVEY.md §8(d) (selectivity 0.1%,
-1%, 10%, 50%) on each layout: 8 scans, each producing a packed bitvector and
-a match count.  Metric: scan Gcodes/s (codes scanned / s, whole job).
+Default workload (BASELINE.json configs[4], the config its metric is quoted
+on at 1/2/4/8 B200): cfg5 -- a 4-column x 2^32-row table (2 uniform int32
+columns as ByteSlice, 2 Zipf(1.1)/2^24 columns as PP-VBS), stored as 8 fixed
+2^29-row segments per column and row-range sharded over the GPUs (strong
+scaling: total work fixed).  One step = u0 < q(.1), u1 >= q(.5), z0 BETWEEN
+q(.8) AND q(.95), z1 <= q(.6) and their 4-way AND over the rank's segments,
+plus the AND's global row-id compaction, then one NCCL all_gather of the
+per-rank counts.  Metric: codes scanned per second, whole job.  See
+bench_cfg5.py; every segment's result words are checked against a device
+filter of the raw values before timing.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload cfg5|cfg2]
 
-Under torchrun (N > 1) every rank holds its own 2^28-row shard (weak
-scaling) and the per-step match counts are combined with one NCCL all_gather.
-`--impl reference` times the CPU oracle port of the reference algorithm on
-the host cores (rank 0 only).
+At N = 1 the line also carries configs.cfg2 (2^28-row Zipf(1.2) column, the
+four BETWEEN windows on PP-VBS and ByteSlice -- the round-1 headline),
+configs.cfg3 (lookups), configs.cfg1 and configs.cfg4.  `--impl reference`
+times the CPU oracle port of the reference algorithm on the host cores on a
+bounded sample of the same workload (rank 0 only).
 """
 
 from __future__ import annotations
@@ -39,9 +45,16 @@ METRIC = "scan Gcodes/s (PP-VBS + ByteSlice BETWEEN scans, cfg2)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="default: 30 (cfg5) / 400 (cfg2)")
+    ap.add_argument("--warmup", type=int, default=None, help="default: 5 (cfg5) / 20 (cfg2)")
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", choices=("cfg5", "cfg2"), default="cfg5",
+                    help="cfg5 (default): 4 x 2^32-row table row-range sharded over the "
+                         "GPUs; cfg2: the 2^28-row Zipf column, 8 BETWEEN scans per GPU")
+    ap.add_argument("--seg-log2", type=int, default=29,
+                    help="cfg5 segment rows (8 segments per column; 29 = 2^32 rows)")
+    ap.add_argument("--cfg5-streams", type=int, default=5, choices=(1, 2, 3, 4, 5))
     ap.add_argument("--rows-log2", type=int, default=28)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -232,6 +245,93 @@ def cpu_baseline(n_full, m, threads, reps=3):
                           "sample": "same sample, one pass on 1 thread"}}
 
 
+def cfg5_reference_setup(m: int):
+    """Host-only cfg5 sample for the oracle port: the first m rows of chunk 0
+    of every column (the reference generators, the same seeds as the GPU
+    arm).  Dictionaries come from the expected 2^32-row Zipf counts
+    rint(pmf * 2^32) (a host bincount of 2^32 draws would take ~15 min);
+    u0/u1 quantiles are the sample's nearest ranks."""
+    import oracle as O
+    import bench_cfg5 as C
+    cols, preds = {}, {}
+    pmf = O.zipf_pmf(C.ZIPF_S, 1 << C.ZIPF_BITS)
+    w = np.rint(pmf * float(1 << 32)).astype(np.int64)
+    uniq = np.flatnonzero(w).astype(np.int64)
+    w = w[uniq]
+    cum = np.cumsum(w)
+    ntot = int(cum[-1])
+
+    def qz(x):
+        return int(uniq[np.searchsorted(cum, min(ntot - 1, int(x * ntot)), side="right")])
+    for ci, (nm, kind) in enumerate(C.COLS):
+        if kind == "uniform":
+            v = C.gen_host(ci, kind, 0, m).astype(np.int64)
+            codes = (v + (1 << 31)).astype(np.uint64)
+            cols[nm] = ("bs", O.bs_build(codes, 32))
+            srt = np.sort(codes)
+            x = 0.10 if nm == "u0" else 0.50
+            q = int(srt[min(m - 1, int(x * m))])
+            preds[nm] = O.pred_compare("LT" if nm == "u0" else "GE", q, 4)
+        else:
+            v = O.gen_zipf(C.ZIPF_S, C.ZIPF_BITS, m, C.chunk_seed(ci, 0))
+            d = O.OracleDict(uniq, w, "prefix_preserving")
+            cols[nm] = ("vbs", O.vbs_build(*d.row_codes(d.encode_rows(v))))
+            preds[nm] = (d.encode_literal("BETWEEN", qz(0.80), qz(0.95)) if nm == "z0"
+                         else d.encode_literal("LE", qz(0.60)))
+    return cols, preds, m
+
+
+def cfg5_reference_pass(setup, threads: int) -> float:
+    import oracle as O
+    cols, preds, m = setup
+
+    def one(nm, mask):
+        kind, c = cols[nm]
+        if kind == "bs":
+            return O.bs_scan(c, 32, m, preds[nm], mask, threads=threads)[0]
+        return O.vbs_scan(c, preds[nm], mask, threads=threads)[0]
+    t0 = time.perf_counter()
+    for nm in ("u0", "u1", "z0", "z1"):
+        one(nm, None)
+    run = None
+    for nm in ("u0", "u1", "z0", "z1"):
+        run = one(nm, run)
+    O.words_to_rows(run, m)
+    return time.perf_counter() - t0
+
+
+def run_reference_cfg5(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    probe = cfg5_reference_setup(1 << 18)
+    cfg5_reference_pass(probe, threads)
+    per_row = cfg5_reference_pass(probe, threads) / (1 << 18)
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    m = max(1 << 14, min(int(budget / per_row) // 1024 * 1024, 1 << 24))
+    setup = probe if m == (1 << 18) else cfg5_reference_setup(m)
+    for _ in range(args.warmup):
+        cfg5_reference_pass(setup, threads)
+    total = sum(cfg5_reference_pass(setup, threads) for _ in range(args.steps))
+    value = 8 * m * args.steps / total / 1e9
+    sample = (f"first {m} rows of chunk 0 of each of the 4 cfg5 columns, the 5 queries "
+              f"(AND pipelined) per step, numpy oracle port on {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC5, "value": round(value, 6), "unit": "Gcodes/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "cfg5: 4 columns x 2^32 rows (u0,u1 uniform int32 ByteSlice "
+                               "w=32; z0,z1 Zipf(1.1)/2^24 PP-VBS), 5 queries per step",
+                   "rows": m, "rows_total": 8 << 29,
+                   "sample": "bounded per-step sample (CPU)"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gcodes/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": "Gcodes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -283,6 +383,329 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if args.workload == "cfg5":
+            out = run_cfg5(args, world, rank, local)
+        else:
+            out = run_cfg2(args, world, rank, local)
+        if rank == 0 and out is not None:
+            print(json.dumps(out), flush=True)
+    finally:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+METRIC5 = ("scan Gcodes/s (cfg5: 4 columns x 2^32 rows row-range sharded; u0<q10, u1>=q50, "
+           "z0 BETWEEN q80,q95, z1<=q60 and their 4-way AND + global row ids)")
+KERNEL5 = {"u0": "scan_kernel<ByteSlice> (LT, w=32)",
+           "u1": "scan_kernel<ByteSlice> (GE, w=32)",
+           "z0": "vbs_ds_kernel<BETWEEN> (PP-VBS SLICED, deep-row space)",
+           "z1": "vbs_ds_kernel (PP-VBS SLICED, LE)",
+           "and4": "bsb_conj_scan chain (ByteSlice + masked ByteSlice + 2 masked vbs_ds_kernel)"}
+
+
+def run_cfg5(args, world, rank, local):
+    """cfg5 headline (bench_cfg5.py): strong scaling over row-range shards."""
+    import torch
+    import torch.distributed as dist
+
+    import bench_cfg5 as C
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.roofline import hbm_peak
+
+    _lib.load()
+    seg_rows = 1 << args.seg_log2
+    t0 = time.perf_counter()
+    tab = C.Cfg5Table(world, rank, seg_rows)
+    t_table = time.perf_counter() - t0
+    step = C.Cfg5Step(tab, 1)
+    step.run_query("and4", torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    cap = int(step.counts[C.QUERIES.index("and4")].sum().item())
+    step.ids = torch.empty(max(cap, 1), dtype=torch.int64, device="cuda")
+    t0 = time.perf_counter()
+    sel = C.check_parity(tab, step)          # raises on any mismatch
+    t_parity = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ab = C.alg_bytes(tab)
+    t_alg = time.perf_counter() - t0
+    cpu = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_cpu_baseline:
+        thr = os.cpu_count() or 1
+        cs = C.cpu_sample(tab, 1 << 22, thr)
+        cpu = {"value": round(cs["all"], 6), "unit": "Gcodes/s", "cores": thr, "kind": "port",
+               "sample": f"first {cs['rows']} rows of segment 0 of each column (global "
+                         f"dictionaries and quantiles of the full table): the 5 cfg5 queries "
+                         f"(AND pipelined) with the numpy oracle on {thr} threads, median "
+                         f"after 1 warm-up",
+               "threads_1": {"value": round(cs["one"], 6), "unit": "Gcodes/s", "cores": 1}}
+    tab.free_raw()
+    # ---- the step as one CUDA graph (C ABI calls + two tiny torch reductions)
+    nst = args.cfg5_streams
+    streams = [torch.cuda.Stream() for _ in range(nst)]
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        capst = streams[0]
+        capst.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(graph, stream=capst):
+            for st in streams[1:]:
+                st.wait_stream(capst)
+            step.local(streams)
+        torch.cuda.current_stream().wait_stream(capst)
+
+    gath = torch.zeros(world, len(C.QUERIES), dtype=torch.int64, device="cuda")
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            cur = torch.cuda.current_stream()
+            for st in streams:
+                st.wait_stream(cur)
+            step.local(streams)
+            cur.wait_stream(streams[0])
+        if world > 1:
+            dist.all_gather_into_tensor(gath, step.totals)
+        else:
+            gath[0].copy_(step.totals)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        one_step()
+    ev1.record()
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if not args.profile else None
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    # the timed steps reproduce the checked counts; global counts and offsets
+    got = gath.cpu().numpy()
+    for qi, q in enumerate(C.QUERIES):
+        if int(got[rank, qi]) != sel[q]:
+            raise AssertionError(f"cfg5 {q}: timed count {got[rank, qi]} != checked {sel[q]}")
+    glob = {q: int(got[:, qi].sum()) for qi, q in enumerate(C.QUERIES)}
+    id_offset = int(got[:rank, C.QUERIES.index("and4")].sum())
+    # ---- per-kernel (per C ABI call) durations for the roofline
+    kt = C.kernel_times(step)
+    S = len(tab.segs)
+    peak, peak_src = hbm_peak(ROOT)
+    queries = {}
+    for q in C.QUERIES:
+        gbs = ab[q] / S / (kt[q] * 1e-3) / 1e9
+        queries[q] = {"kernel": KERNEL5[q], "us_per_segment": round(kt[q] * 1e3, 2),
+                      "alg_bytes_per_code": round(ab[q] / (S * seg_rows), 4),
+                      "alg_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                      "selected_global": glob[q],
+                      "predicate": tab.literals.get(q, "u0 AND u1 AND z0 AND z1")}
+    dom = max(C.QUERIES, key=lambda q: kt[q])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic_cfg5.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except (OSError, ValueError):
+            traffic = None
+    ms_step = total_ms / args.steps
+    codes_per_step = 8 * tab.n_total
+    value = codes_per_step / (ms_step * 1e-3) / 1e9
+    whole = sum(ab.values())
+    t5 = torch.tensor([float(whole)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t5)
+    step_frac = float(t5.item()) / (ms_step * 1e-3) / 1e9 / (peak * world)
+    e2e = None
+    if not args.profile:
+        e2e = measure_e2e_cfg5(tab, args.e2e_steps, world)
+    if rank != 0:
+        return None
+    dq = queries[dom]
+    out = {
+        "metric": METRIC5, "value": round(value, 3), "unit": "Gcodes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded numpy PCG64 draws with the reference generators; "
+                "8 fixed chunks per column, identical at every N)",
+        "config": {"workload": "cfg5: 4 columns x 2^32 rows (u0,u1 uniform int32 ByteSlice "
+                               "w=32; z0,z1 Zipf(1.1)/2^24 PP-VBS with global dictionaries), "
+                               "row-range sharded; 5 queries per step",
+                   "rows_total": tab.n_total, "segments": C.N_CHUNKS, "segment_rows": seg_rows,
+                   "segments_per_gpu": S, "codes_per_step": codes_per_step,
+                   "parallelism": f"row-range shards x{world}" if world > 1 else "single GPU",
+                   "collectives_per_step": "1 NCCL all_gather of 5 int64 counts per rank"
+                                           if world > 1 else "none (N=1)",
+                   "l2": f"inputs larger than L2 ({tab.col_bytes() / 1e9:.1f} GB of encoded "
+                         f"columns per GPU)",
+                   "launch": (f"CUDA graph of the rank's C ABI calls on {nst} forked streams"
+                              if graph is not None else "eager C ABI calls")},
+        "roofline": {"bound": "hbm", "kernel": dq["kernel"], "query": dom,
+                     "achieved": dq["alg_gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": dq["frac"], "peak_source": peak_src, "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic_cfg5.json (ncu dram read+write "
+                                       "per launch)" if traffic else None,
+                     "alg_bytes_per_launch": int(ab[dom] / S),
+                     "us_per_launch": dq["us_per_segment"],
+                     "whole_step_frac": round(step_frac, 4)},
+        "queries": queries,
+        "parity": {"checked": "every segment's bitvector of every query == packed device "
+                              "filter of its raw values; AND global row ids == filter rows + "
+                              "segment start; counts", "segments_checked": S,
+                   "selected_rank0": sel, "and4_id_offset_rank0": id_offset},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": None,
+        "clocks": clk,
+        "build_s": {"table": round(t_table, 2), "gen": round(tab.t_gen, 2),
+                    "dictionaries": round(tab.t_dict, 2), "layouts": round(tab.t_build, 2),
+                    "parity": round(t_parity, 2), "alg_bytes": round(t_alg, 2)},
+    }
+    # kernels of the rank's step: one per single scan, 4 per AND chain, 3 for
+    # each segment's compaction (tile popcount, CUB scan, emit)
+    out["gpu_launches"] = int(args.steps * S * (4 + 4 + 3))
+    if world == 1 and not args.profile and not args.no_extra:
+        del graph, step, tab
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        out["configs"] = measure_configs_after_cfg5(args, world, rank, local)
+    return out
+
+
+def measure_configs_after_cfg5(args, world, rank, local) -> dict:
+    """cfg2 (8 BETWEEN scans, the round-1 headline), cfg3 lookups, cfg1, cfg4."""
+    import torch
+    out = {}
+    a2 = argparse.Namespace(**vars(args))
+    a2.steps, a2.warmup, a2.workload = 100, 10, "cfg2"
+    t0 = time.perf_counter()
+    try:
+        out["cfg2"] = run_cfg2(a2, world, rank, local, emit_extras=False)
+    except Exception as exc:  # noqa: BLE001 - recorded, not swallowed
+        out["cfg2"] = {"error": f"{type(exc).__name__}: {exc}"}
+    out["cfg2"]["wall_s"] = round(time.perf_counter() - t0, 1)
+    torch.cuda.empty_cache()
+    if not args.no_lookup:
+        t0 = time.perf_counter()
+        try:
+            out["cfg3"] = measure_lookups(max(3, args.lookup_steps), 28)
+        except Exception as exc:  # noqa: BLE001
+            out["cfg3"] = {"error": f"{type(exc).__name__}: {exc}"}
+        if isinstance(out["cfg3"], dict):
+            out["cfg3"]["wall_s"] = round(time.perf_counter() - t0, 1)
+    torch.cuda.empty_cache()
+    out.update(measure_extra_configs(None))
+    return out
+
+
+def measure_e2e_cfg5(tab, steps, world) -> dict:
+    """The 5 cfg5 queries end to end through the public API on the rank's
+    first segment of every column with the encoded columns in pinned HOST
+    memory: every step uploads the 4 segment columns, runs the scans, the
+    conjunction and the row-id compaction, and reads back every result
+    bitvector, the counts and the AND's global row ids."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_00220_b200.byteslice import ByteSliceColumn, scan_byteslice
+    from paper_2209_00220_b200.engine import conj_scan
+    from paper_2209_00220_b200.vbs import VbsColumn, scan_vbs
+
+    names = ("u0", "u1", "z0", "z1")
+    pairs, dcols = [], {}
+    for nm in names:
+        c = tab.cols[nm][0]
+        if tab.layout[nm] == "byteslice":
+            h = c.planes.cpu().pin_memory()
+            d = torch.empty_like(c.planes)
+            pairs.append((h, d))
+            dcols[nm] = ByteSliceColumn(c.n_rows, c.width_bits, c.lanes, c.stride, d)
+            continue
+        K = c.max_len
+
+        def cp(t):
+            if t is None:
+                return None
+            h = t.cpu().pin_memory()
+            d = torch.empty_like(t)
+            pairs.append((h, d))
+            return d
+        bs1 = cp(c.bs1)
+        deep = [cp(t) for t in c.deep]
+        exist = [None] + [cp(c.exist[j]) for j in range(1, K)]
+        bdir = [None] + [cp(c.block_dir[j]) for j in range(1, K)]
+        rex = None if c.rexist is None else [cp(t) for t in c.rexist]
+        dcols[nm] = VbsColumn(c.n_rows, K, c.lanes, c.stride, bs1, deep, exist, bdir,
+                              c.level_rows, c.deep_mode, rex, c.deep1_range)
+    h2d = sum(h.numel() * h.element_size() for h, _ in pairs)
+    n = tab.seg_rows
+    nw = n // 32
+    res_h = [torch.empty(nw, dtype=torch.int32).pin_memory() for _ in range(5)]
+    cnt_h = torch.empty(5, dtype=torch.int64).pin_memory()
+    ids_h = [None]
+    r0 = tab.seg_starts[0]
+
+    def step():
+        for h, d in pairs:
+            d.copy_(h, non_blocking=True)
+        bvs = []
+        for nm in names:
+            fn = scan_vbs if tab.layout[nm] == "ppvbs" else scan_byteslice
+            bvs.append(fn(dcols[nm], tab.preds[nm])[0])
+        andb = conj_scan([(tab.layout[nm], dcols[nm]) for nm in names],
+                         [tab.preds[nm] for nm in names])
+        bvs.append(andb)
+        for i, b in enumerate(bvs):
+            res_h[i].copy_(b.dwords, non_blocking=True)
+            cnt_h[i:i + 1].copy_(b.count_device(), non_blocking=True)
+        ids = andb.row_ids(row_offset=r0)        # syncs for the count (public API)
+        ids_h[0] = ids.cpu()
+        return ids.numel()
+
+    nsel = step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    d2h = 5 * nw * 4 + 5 * 8 + 8 * nsel
+    return {"value": round(world * 8 * n / (ms * 1e-3) / 1e9, 3), "unit": "Gcodes/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "what": "public API (scan_byteslice / scan_vbs / engine.conj_scan / row_ids) on "
+                    "each rank's first segment (2^29 rows) of the 4 columns: encoded columns "
+                    "uploaded from pinned host memory every step, 5 result bitvectors + counts "
+                    "+ the AND's global row ids read back every step"}
+
+
+def run_cfg2(args, world, rank, local, emit_extras=True):
+    """The cfg2 step (configs[1]): 8 BETWEEN scans of the 2^28-row Zipf(1.2)
+    column on PP-VBS and ByteSlice.  Returns rank 0's JSON dict."""
+    import torch
+    import torch.distributed as dist
 
     from paper_2209_00220_b200 import _lib
     from paper_2209_00220_b200.byteslice import scan_byteslice
@@ -454,11 +877,11 @@ def run_b200(args):
     if rank == 0:
         e2e = None if args.profile else measure_e2e(data, scans, args.e2e_steps, n, world)
         lookups = None
-        if not args.profile and not args.no_lookup:
+        if emit_extras and not args.profile and not args.no_lookup:
             torch.cuda.empty_cache()
             lookups = measure_lookups(max(3, args.lookup_steps), args.rows_log2)
         extra = None
-        if not args.profile and not args.no_extra:
+        if emit_extras and not args.profile and not args.no_extra:
             extra = measure_extra_configs(data)
         cpu = None
         if world == 1 and not args.profile and not args.no_cpu_baseline:
@@ -510,22 +933,18 @@ def run_b200(args):
             "build_s": {"gen_zipf": round(data["t_gen"], 3),
                         "encode_and_layouts": round(data["t_encode"], 3)},
         }
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
     return out
 
 
 def measure_extra_configs(data) -> dict:
-    """SURVEY.md §8(d) cfg1 / cfg4 / cfg5 (bench_cfgs.py); a failure is
-    reported in the line instead of hiding the headline."""
+    """SURVEY.md §8(d) cfg1 / cfg4 (bench_cfgs.py); a failure is reported in
+    the line instead of hiding the headline.  (cfg5 is bench.py's own
+    workload, bench_cfg5.py.)"""
     import torch
 
     import bench_cfgs
     out = {}
-    for name, fn in (("cfg1", bench_cfgs.measure_cfg1), ("cfg4", bench_cfgs.measure_cfg4),
-                     ("cfg5", bench_cfgs.measure_cfg5)):
+    for name, fn in (("cfg1", bench_cfgs.measure_cfg1), ("cfg4", bench_cfgs.measure_cfg4)):
         torch.cuda.empty_cache()
         t0 = time.perf_counter()
         try:
@@ -791,8 +1210,12 @@ def measure_e2e(data, scans, steps, n, world):
 
 def main():
     args = parse()
+    if args.steps is None:
+        args.steps = 30 if args.workload == "cfg5" else 400
+    if args.warmup is None:
+        args.warmup = 5 if args.workload == "cfg5" else 20
     if args.impl == "reference":
-        run_reference(args)
+        (run_reference_cfg5 if args.workload == "cfg5" else run_reference)(args)
     else:
         run_b200(args)
 

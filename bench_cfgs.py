@@ -1,6 +1,6 @@
-"""Secondary measurements for bench.py: SURVEY.md §8(d) cfg1, cfg4 and cfg5
-(one GPU's shard).  Each returns a JSON-able dict that bench.py attaches to
-its line under "configs"; every timed number is device time from CUDA events
+"""Secondary measurements for bench.py: SURVEY.md §8(d) cfg1 and cfg4.
+Each returns a JSON-able dict that bench.py attaches to its line under
+"configs"; every timed number is device time from CUDA events
 on the launching stream, after warm-up, and every workload is checked against
 a host numpy filter of the same raw values before it is timed.
 
@@ -9,9 +9,7 @@ a host numpy filter of the same raw values before it is timed.
   cfg4  16 columns x 2^27 rows through the advisor (GPU wall-clock AUC), then
         the 4-predicate conjunction as ONE fused device pass + 3 projections
         decoded on the device + SUM(u32)
-  cfg5  one GPU's shard of the 8-GPU scan: 4 columns x 2^29 rows (2 uniform
-        int32 ByteSlice w=32, 2 Zipf(1.1)/2^24 PP-VBS), each predicate alone
-        and the 4-way AND, plus the global row-id compaction
+(cfg5, the 2^32-row sharded table, is bench.py's headline: bench_cfg5.py.)
 """
 
 from __future__ import annotations
@@ -238,89 +236,3 @@ def measure_cfg4(reps: int = 20, log2n: int = 27, advise_count: int = 100) -> di
         "lookups": {nm: {"us": round(t * 1e3, 2), "mrows_s": round(want_count / t / 1e3, 1),
                          "layout": store.columns[nm].layout} for nm, t in ms_look.items()},
     }
-
-
-# --------------------------------------------------------------------- cfg5
-def measure_cfg5(reps: int = 20, log2n: int = 29) -> dict:
-    import torch
-
-    from paper_2209_00220_b200 import ColumnKind, Dictionary, FrequencyTable, ZipfSpec
-    from paper_2209_00220_b200.byteslice import build_byteslice, scan_byteslice
-    from paper_2209_00220_b200.datagen import gen_zipf_device, zipf_pmf
-    from paper_2209_00220_b200.engine import conj_scan
-    from paper_2209_00220_b200.predicate import Op, Predicate, ResolvedPredicate
-    from paper_2209_00220_b200.roofline import hbm_peak
-    from paper_2209_00220_b200.vbs import build_vbs, scan_vbs
-
-    n, chunk = 1 << log2n, 0   # shard 0 of the 8 fixed 2^29-row chunks
-    t0 = time.perf_counter()
-    raw, cols, preds = {}, {}, {}
-    for ci, nm in enumerate(("u0", "u1")):
-        v = np.random.default_rng(500 + 10 * ci + chunk).integers(-(1 << 31), 1 << 31, n,
-                                                                 dtype=np.int32)
-        raw[nm] = v
-        codes = torch.from_numpy(v).cuda().to(torch.int64) + (1 << 31)  # bias identity
-        cols[nm] = ("byteslice", build_byteslice(codes, 32), None)
-        srt = torch.sort(codes).values
-        qv = {x: int(srt[min(n - 1, int(x * n))].item()) - (1 << 31) for x in (0.10, 0.50)}
-        del codes, srt
-        if nm == "u0":
-            preds[nm] = (ResolvedPredicate.compare(Op.LT, qv[0.10] + (1 << 31), 4),
-                         lambda v, t=qv[0.10]: v < t)
-        else:
-            preds[nm] = (ResolvedPredicate.compare(Op.GE, qv[0.50] + (1 << 31), 4),
-                         lambda v, t=qv[0.50]: v >= t)
-    # Zipf(1.1)/2^24 columns; dictionary from the expected global weights
-    pmf = zipf_pmf(1.1, 1 << 24)
-    wts = np.maximum(np.rint(pmf * float(1 << 32)).astype(np.int64), 1)
-    dom = np.arange(1 << 24, dtype=np.int64)
-    d = Dictionary.build(FrequencyTable(dom, wts, ColumnKind.NUMERIC), "prefix_preserving")
-    qz = lambda x: _q(dom, wts, int(wts.sum()), x)  # noqa: E731
-    for ci, nm in ((2, "z0"), (3, "z1")):
-        vals = gen_zipf_device(ZipfSpec(1.1, 24, n, 500 + 10 * ci + chunk))
-        raw[nm] = vals.to(torch.int32).cpu().numpy()
-        c, l = d.row_codes_device(vals)  # every value is in the dictionary: rank == value
-        col = build_vbs(c, l)
-        del c, l, vals
-        cols[nm] = ("ppvbs", col, [col.mask_words(j) for j in range(2, col.max_len + 1)])
-    lo, hi = qz(0.80), qz(0.95)
-    preds["z0"] = (d.encode_literal(Predicate("z0", Op.BETWEEN, lo, hi)),
-                   lambda v: (v >= lo) & (v <= hi))
-    q60 = qz(0.60)
-    preds["z1"] = (d.encode_literal(Predicate("z1", Op.LE, q60)), lambda v: v <= q60)
-    t_gen = time.perf_counter() - t0
-    peak, _ = hbm_peak()
-    out = {"workload": "cfg5 shard: 4 columns x 2^29 rows (one of 8 fixed chunks; u0,u1 "
-                       "int32 bias-identity ByteSlice w=32; z0,z1 Zipf(1.1)/2^24 PP-VBS with the "
-                       "dictionary of the expected 2^32-row weights)",
-           "rows": n, "gen_s": round(t_gen, 2), "columns": {}}
-    allm = np.ones(n, bool)
-    for nm in ("u0", "u1", "z0", "z1"):
-        lay, col, ex = cols[nm]
-        rp, hf = preds[nm]
-        hm = hf(raw[nm])
-        allm &= hm
-        fn = scan_vbs if lay == "ppvbs" else scan_byteslice
-        bv, _ = fn(col, rp)
-        assert bv.count() == int(hm.sum()), f"cfg5 {nm} count"
-        ms = _time(lambda: fn(col, rp), reps)
-        ab = _alg_bytes([(lay, col, ex)], [rp])
-        out["columns"][nm] = {"layout": lay, "us": round(ms * 1e3, 2),
-                              "gcodes_s": round(n / ms / 1e6, 1),
-                              "alg_bytes_per_code": round(ab / n, 4),
-                              "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4),
-                              "selected": int(hm.sum())}
-    order = ("u0", "u1", "z0", "z1")
-    pairs = [(cols[k][0], cols[k][1]) for k in order]
-    rps = [preds[k][0] for k in order]
-    sel = conj_scan(pairs, rps)
-    assert sel.count() == int(allm.sum()), "cfg5 AND count"
-    ms = _time(lambda: conj_scan(pairs, rps), reps)
-    ab = _alg_bytes([cols[k] for k in order], rps)
-    ms_ids = _time(lambda: sel.row_ids(row_offset=chunk * n), reps)
-    out["and4"] = {"us": round(ms * 1e3, 2), "gcodes_s": round(4 * n / ms / 1e6, 1),
-                   "alg_bytes_per_code": round(ab / n, 4),
-                   "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 4),
-                   "selected": int(allm.sum()),
-                   "row_ids_us": round(ms_ids * 1e3, 2)}
-    return out

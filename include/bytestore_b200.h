@@ -302,6 +302,13 @@ int bsb_bits_to_rows(const uint32_t* words, int64_t n_rows, int64_t* rows_out,
  * count is written to the device scalar n_out_dev. */
 int bsb_bits_to_rows_async(const uint32_t* words, int64_t n_rows, int64_t row_offset,
                            int64_t* rows_out, uint64_t* n_out_dev, void* stream);
+/* Compaction of one row-range segment into a shared id array without a host
+ * sync: ids row_offset + i of the set bits are written to
+ * rows_out[*base_dev ...], base_dev a device int64 (e.g. the exclusive prefix
+ * of the earlier segments' counts). */
+int bsb_bits_to_rows_at(const uint32_t* words, int64_t n_rows, int64_t row_offset,
+                        const int64_t* base_dev, int64_t* rows_out, uint64_t* n_out_dev,
+                        void* stream);
 /* & | ~ and popcount (bitvector.py:84-125).  op: 0 = and, 1 = or, 2 = not
  * (b ignored), 3 = andnot (a & ~b).  Tail bits cleared. */
 int bsb_bits_combine(int32_t op, const uint32_t* a, const uint32_t* b, uint32_t* out,

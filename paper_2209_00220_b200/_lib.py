@@ -100,6 +100,7 @@ _SIGS = {
     "bsb_scatter": (c_int32, [_P, _P, c_int64, c_int32, _P, _P]),
     "bsb_bits_to_rows": (c_int32, [_P, c_int64, _P, POINTER(c_int64), _P]),
     "bsb_bits_to_rows_async": (c_int32, [_P, c_int64, c_int64, _P, _P, _P]),
+    "bsb_bits_to_rows_at": (c_int32, [_P, c_int64, c_int64, _P, _P, _P, _P]),
     "bsb_bits_combine": (c_int32, [c_int32, _P, _P, _P, c_int64, _P]),
     "bsb_bits_popcount": (c_int32, [_P, c_int64, _P, _P]),
     "bsb_conj_scan": (c_int32, [c_int32, POINTER(BsbColumnRef), POINTER(BsbPred), _P, _P, _P,

@@ -188,7 +188,9 @@ __global__ void tile_popc_kernel(const uint32_t* __restrict__ words, int64_t nb,
 
 __global__ void tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
                                  const int64_t* __restrict__ tile_incl, int64_t row_offset,
+                                 const int64_t* __restrict__ base_dev,
                                  int64_t* __restrict__ rows_out) {
+  if (base_dev) rows_out += __ldg(base_dev);  // compaction into a shared id array
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -236,7 +238,7 @@ __global__ void popcount_kernel(const uint32_t* __restrict__ w, int64_t nb,
 }
 
 static int bits_to_rows_impl(const uint32_t* words, int64_t n_rows, int64_t row_offset,
-                             int64_t* rows_out, uint64_t* n_out_dev, int64_t* n_out_host,
+                             const int64_t* base_dev, int64_t* rows_out, uint64_t* n_out_dev, int64_t* n_out_host,
                              cudaStream_t s) {
   const int64_t nb = (n_rows + 31) / 32;
   const int64_t ntiles = (nb + 31) / 32;
@@ -253,7 +255,8 @@ static int bits_to_rows_impl(const uint32_t* words, int64_t n_rows, int64_t row_
   cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, tc, incl, ntiles, s);
   BSB_LAUNCH_CHECK();
   if (rows_out) {
-    tile_emit_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, incl, row_offset, rows_out);
+    tile_emit_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, incl, row_offset, base_dev,
+                                          rows_out);
     BSB_LAUNCH_CHECK();
   }
   if (n_out_dev)
@@ -342,13 +345,21 @@ extern "C" int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int6
 extern "C" int bsb_bits_to_rows(const uint32_t* words, int64_t n_rows, int64_t* rows_out,
                                 int64_t* n_out_host, void* stream) {
   if (!words || n_rows <= 0 || !n_out_host) return BSB_EINVAL;
-  return bits_to_rows_impl(words, n_rows, 0, rows_out, nullptr, n_out_host, as_stream(stream));
+  return bits_to_rows_impl(words, n_rows, 0, nullptr, rows_out, nullptr, n_out_host,
+                           as_stream(stream));
 }
 
 extern "C" int bsb_bits_to_rows_async(const uint32_t* words, int64_t n_rows, int64_t row_offset,
                                       int64_t* rows_out, uint64_t* n_out_dev, void* stream) {
   if (!words || n_rows <= 0) return BSB_EINVAL;
-  return bits_to_rows_impl(words, n_rows, row_offset, rows_out, n_out_dev, nullptr,
+  return bits_to_rows_impl(words, n_rows, row_offset, nullptr, rows_out, n_out_dev, nullptr,
+                           as_stream(stream));
+}
+extern "C" int bsb_bits_to_rows_at(const uint32_t* words, int64_t n_rows, int64_t row_offset,
+                                   const int64_t* base_dev, int64_t* rows_out,
+                                   uint64_t* n_out_dev, void* stream) {
+  if (!words || n_rows <= 0 || !base_dev || !rows_out) return BSB_EINVAL;
+  return bits_to_rows_impl(words, n_rows, row_offset, base_dev, rows_out, n_out_dev, nullptr,
                            as_stream(stream));
 }
 

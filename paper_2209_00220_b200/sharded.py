@@ -23,9 +23,15 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "ShardResult", "exchange_counts", "sharded_scan",
-           "global_row_ids", "merge_frequency_tables", "gather_row_ids", "global_sum"]
+           "global_row_ids", "merge_frequency_tables", "gather_row_ids", "global_sum",
+           "owned_segments", "compact_segments", "global_nearest_rank_u32",
+           "exclusive_offsets"]
 
 TILE_ROWS = 1024
+# A table larger than one kernel's comfortable row range is stored as fixed
+# row-range segments (row groups) of this many rows; a rank owns a contiguous
+# run of segments, so every segment boundary is also a tile boundary.
+SEGMENT_ROWS = 1 << 29
 
 
 def shard_range(n_total: int, world: int, rank: int, align: int = TILE_ROWS):
@@ -38,6 +44,72 @@ def shard_range(n_total: int, world: int, rank: int, align: int = TILE_ROWS):
     r0 = min(n_total, rank * per)
     r1 = min(n_total, r0 + per)
     return r0, r1
+
+
+def owned_segments(n_segments: int, world: int, rank: int) -> range:
+    """Contiguous segments [lo, hi) of rank: the row-range partition at
+    segment granularity (SPEC.md:284 -- any block-aligned partition
+    concatenates bit-exactly).  Every rank owns at least one segment."""
+    if world < 1 or not 0 <= rank < world or n_segments < world:
+        raise ValueError("need 0 <= rank < world <= n_segments")
+    return range(n_segments * rank // world, n_segments * (rank + 1) // world)
+
+
+def exclusive_offsets(counts: torch.Tensor) -> torch.Tensor:
+    """Exclusive prefix sum of int64 counts, on their device (no host sync)."""
+    c = counts.reshape(-1).to(torch.int64)
+    return torch.cumsum(c, 0) - c
+
+
+def compact_segments(seg_words, seg_rows, seg_starts, seg_counts: torch.Tensor,
+                     out: torch.Tensor, stream_ptr=None) -> None:
+    """Global int64 row ids of several segments' matches, compacted into
+    `out` in ascending row order without a host sync: segment s's ids
+    (seg_starts[s] + local row) land at the exclusive prefix of seg_counts
+    (device int64, one per segment) -- bitvector.py:71-72 per segment.
+    `out` must hold the rank's total count."""
+    from . import _lib
+    from .device import stream as cur_stream
+    lib = _lib.load()
+    base = exclusive_offsets(seg_counts)
+    sp = cur_stream() if stream_ptr is None else stream_ptr
+    for s, (w, n, r0) in enumerate(zip(seg_words, seg_rows, seg_starts)):
+        _lib.check(lib.bsb_bits_to_rows_at(w.data_ptr(), int(n), int(r0),
+                                           base[s:].data_ptr(), out.data_ptr(), None, sp),
+                   "compact_segments")
+    return base
+
+
+def global_nearest_rank_u32(chunks, fractions, n_total: int, group=None):
+    """Exact nearest-rank quantiles sorted(v)[min(n-1, floor(x*n))] (the
+    advisor's literal rule, advisor.py:56-59) of uint32 values spread over
+    ranks and chunks (int64 tensors holding 0..2^32-1), by a two-level radix
+    select: a 2^16-bin histogram of the high halves, all-reduced, picks each
+    quantile's bin; a second histogram of the low halves inside that bin
+    picks the value.  Two small all_reduces per quantile, no sort."""
+    dev = chunks[0].device
+    dist_on = dist.is_available() and dist.is_initialized()
+
+    def hist(fn):
+        h = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
+        for c in chunks:
+            for p in torch.split(c, 1 << 27):
+                v = fn(p)
+                if v.numel():
+                    h += torch.bincount(v, minlength=1 << 16)
+        if dist_on:
+            dist.all_reduce(h, group=group)
+        return h
+
+    hi = torch.cumsum(hist(lambda p: p >> 16), 0).cpu().numpy()
+    out = []
+    for x in fractions:
+        k = min(n_total - 1, int(x * n_total))
+        b = int(np.searchsorted(hi, k, side="right"))
+        k2 = k - (int(hi[b - 1]) if b else 0)
+        lo = torch.cumsum(hist(lambda p, b=b: (p[(p >> 16) == b] & 0xFFFF)), 0).cpu().numpy()
+        out.append((b << 16) | int(np.searchsorted(lo, k2, side="right")))
+    return out
 
 
 @dataclass
