@@ -78,7 +78,7 @@ class Cfg5Table:
     """This rank's segments of the cfg5 table, built on the device."""
 
     def __init__(self, world: int, rank: int, seg_rows: int = 1 << 29, group=None,
-                 keep_raw: bool = True, log=print):
+                 keep_raw: bool = True, log=print, only_segments=None):
         import torch
         import torch.distributed as dist
 
@@ -94,6 +94,9 @@ class Cfg5Table:
         self.seg_rows = seg_rows
         self.n_total = N_CHUNKS * seg_rows
         self.segs = list(owned_segments(N_CHUNKS, world, rank))
+        if only_segments is not None:  # diagnostics: a subset (dictionaries from it alone)
+            self.segs = [s for s in self.segs if s in only_segments]
+            self.n_total = len(self.segs) * seg_rows
         self.seg_starts = [s * seg_rows for s in self.segs]
         dev = torch.device("cuda", torch.cuda.current_device())
         dist_on = world > 1
