@@ -54,13 +54,19 @@ static int grid_for(int64_t items, int threads, int cap = 148 * 16) {
 
 // ------------------------------------------------------------- ByteSlice
 
+// Warp per 32-row block: lane r validates and aligns row r's code
+// (byteslice.py:52-73), then every plane's block is written in the
+// bit-plane layout (bsb_common.cuh, "BP32") with 8 ballots.
 template <typename CodeT>
 __global__ void bs_build_kernel(const CodeT* __restrict__ codes, int64_t n, int width, int K,
                                 uint8_t* __restrict__ slices, int64_t stride,
                                 unsigned int* __restrict__ err) {
   const int shift = 8 * K - width;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < stride;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < stride / 32; b += nwarps) {
+    const int64_t r = b * 32 + lane;
     uint64_t c = 0;
     if (r < n) {
       const CodeT v = codes[r];
@@ -71,18 +77,23 @@ __global__ void bs_build_kernel(const CodeT* __restrict__ codes, int64_t n, int 
         if (width < 64 && (c >> width) != 0) atomicOr(err, 1u);
       }
     }
-    const uint64_t a = c << shift;
-    const int64_t pos = (r & ~int64_t(31)) + swz((int)(r & 31));
-    for (int j = 0; j < K; ++j) slices[(int64_t)j * stride + pos] = (uint8_t)(a >> (8 * (K - 1 - j)));
+    const uint64_t a = shift >= 64 ? 0 : (c << shift);
+    for (int j = 0; j < K; ++j)
+      bp_store_block(slices + (int64_t)j * stride + b * 32,
+                     (uint32_t)(a >> (8 * (K - 1 - j))) & 0xFFu, lane);
   }
 }
 
+// Reference planes (row order, byteslice.py:68): out[j][r]
 __global__ void bs_export_kernel(const uint8_t* __restrict__ slices, int64_t stride, int K,
                                  int64_t npad, uint8_t* __restrict__ out) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npad;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t pos = (r & ~int64_t(31)) + swz((int)(r & 31));
-    for (int j = 0; j < K; ++j) out[(int64_t)j * npad + r] = slices[(int64_t)j * stride + pos];
+    for (int j = 0; j < K; ++j) {
+      uint32_t w[8];
+      ldg256(slices + (int64_t)j * stride + (r >> 5) * 32, w);
+      out[(int64_t)j * npad + r] = (uint8_t)bp_byte(w, (int)(r & 31));
+    }
   }
 }
 
@@ -97,7 +108,7 @@ static int bs_build_impl(const CodeT* codes, int64_t n, int32_t width, uint8_t* 
   BSB_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
   BSB_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
   bs_build_kernel<CodeT><<<grid_for(stride, 256), 256, 0, s>>>(codes, n, width, K, slices,
-                                                               stride, err);
+                                                               stride, err);  // warp per block
   BSB_LAUNCH_CHECK();
   unsigned int h = 0;
   BSB_CUDA(cudaMemcpyAsync(&h, err, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -159,7 +170,7 @@ __global__ void vbs_exist_kernel(const uint64_t* __restrict__ codes,
       l = lens[r];
       c = codes[r];
     }
-    bs1[b * 32 + swz(lane)] = l ? (uint8_t)(c >> (8 * (l - 1))) : (uint8_t)0;
+    bp_store_block(bs1 + b * 32, l ? (uint32_t)(c >> (8 * (l - 1))) & 0xFFu : 0u, lane);
     for (int j = 2; j <= K; ++j) {
       const uint32_t bal = __ballot_sync(kFull, l >= (unsigned)j);
       if (lane == 0) {
@@ -170,10 +181,14 @@ __global__ void vbs_exist_kernel(const uint64_t* __restrict__ codes,
   }
 }
 
+// Deep rows in row order: SLICED gathers each deep row's (code, length) at
+// its deep-row index q (the rank of the row among rows with >= 2 bytes, from
+// the level-2 directory); PACKED writes the reference packing (vbs.py:98-100).
 __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
                                    const uint8_t* __restrict__ lens, int64_t n, int K, int mode,
                                    uint8_t* const* deep, const uint32_t* const* exist,
-                                   const int64_t* const* dir, uint32_t* const* rexist) {
+                                   const int64_t* const* dir, uint64_t* __restrict__ dcode,
+                                   uint8_t* __restrict__ dlen) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const unsigned l = lens[r];
@@ -182,19 +197,41 @@ __global__ void vbs_scatter_kernel(const uint64_t* __restrict__ codes,
     const int64_t b = r >> 5;
     const uint32_t below = (1u << (r & 31)) - 1u;
     if (mode == BSB_DEEP_SLICED) {
-      // deep rows as a swizzled ByteSlice column + per-deep-block existence words
       const int64_t q = dir[1][b] + __popc(exist[1][b] & below);
-      const int64_t pos = (q & ~int64_t(31)) + swz((int)(q & 31));
-      if (deep[0]) deep[0][pos] = (uint8_t)(c >> (8 * (l - 1)));  // level 1 in deep-row space
-      for (int j = 2; j <= K; ++j)
-        deep[j - 1][pos] = j <= (int)l ? (uint8_t)(c >> (8 * (l - j))) : (uint8_t)0;
-      for (int j = 3; j <= (int)l; ++j)
-        atomicOr(rexist[j - 1] + (q >> 5), 1u << (q & 31));
+      dcode[q] = c;
+      dlen[q] = (uint8_t)l;
     } else {
       for (int j = 2; j <= (int)l; ++j) {
         const uint32_t w = exist[j - 1][b];
         const int64_t pos = dir[j - 1][b] + __popc(w & below);
         deep[j - 1][pos] = (uint8_t)(c >> (8 * (l - j)));
+      }
+    }
+  }
+}
+
+// SLICED deep planes, warp per 32-deep-row block: byte j of every deep row
+// (0 where the code is shorter) in the bit-plane layout, byte 1 in deep[0]
+// when allocated, and rexist[j] = "deep row has byte j+1" (j >= 2).
+__global__ void vbs_deep_planes_kernel(const uint64_t* __restrict__ dcode,
+                                       const uint8_t* __restrict__ dlen, int64_t cnt2, int K,
+                                       uint8_t* const* deep, uint32_t* const* rexist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ndb = (cnt2 + 31) / 32;
+  for (int64_t db = warp; db < ndb; db += nwarps) {
+    const int64_t q = db * 32 + lane;
+    const unsigned l = q < cnt2 ? dlen[q] : 0u;
+    const uint64_t c = q < cnt2 ? dcode[q] : 0ull;
+    if (deep[0])
+      bp_store_block(deep[0] + db * 32, l ? (uint32_t)(c >> (8 * (l - 1))) & 0xFFu : 0u, lane);
+    for (int j = 2; j <= K; ++j) {
+      const uint32_t byte = j <= (int)l ? (uint32_t)(c >> (8 * (l - j))) & 0xFFu : 0u;
+      bp_store_block(deep[j - 1] + db * 32, byte, lane);
+      if (j < K) {
+        const uint32_t bal = __ballot_sync(kFull, (int)l >= j + 1);
+        if (lane == 0) rexist[j][db] = bal;
       }
     }
   }
@@ -218,7 +255,9 @@ __global__ void vbs_export_level_kernel(int64_t n, int level, int mode,
                                                 : dir_src[b] + __popc(w & below);
     uint8_t byte;
     if (mode == BSB_DEEP_SLICED) {
-      byte = deep_l[(src & ~int64_t(31)) + swz((int)(src & 31))];
+      uint32_t v[8];
+      ldg256(deep_l + (src >> 5) * 32, v);
+      byte = (uint8_t)bp_byte(v, (int)(src & 31));
     } else {
       byte = deep_l[src];
     }
@@ -237,7 +276,11 @@ __global__ void vbs_export_kernel(const uint8_t* __restrict__ bs1, int64_t npad,
                                   uint8_t* __restrict__ out) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npad;
        r += (int64_t)gridDim.x * blockDim.x)
-    out[r] = bs1[(r & ~int64_t(31)) + swz((int)(r & 31))];
+  {
+    uint32_t v[8];
+    ldg256(bs1 + (r >> 5) * 32, v);
+    out[r] = (uint8_t)bp_byte(v, (int)(r & 31));
+  }
 }
 
 struct PtrTable {
@@ -373,11 +416,33 @@ extern "C" int bsb_vbs_build(const uint64_t* codes, const uint8_t* lens, const b
     BSB_CUDA(cudaFreeAsync(tmp, s));
   }
   if (K > 1) {
+    uint64_t* dcode = nullptr;
+    uint8_t* dlen = nullptr;
+    int64_t cnt2 = 0;
+    if (mode == BSB_DEEP_SLICED) {
+      // deep-row count = level-2 directory total
+      BSB_CUDA(cudaMemcpyAsync(&cnt2, h.dir[1] + nbpad, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               s));
+      BSB_CUDA(cudaStreamSynchronize(s));
+      if (cnt2 > 0) {
+        BSB_CUDA(cudaMallocAsync(&dcode, (size_t)cnt2 * 8, s));
+        BSB_CUDA(cudaMallocAsync(&dlen, (size_t)cnt2, s));
+      }
+      for (int j = 2; j < K; ++j)
+        BSB_CUDA(cudaMemsetAsync(h.rexist[j], 0, (size_t)((cnt2 + 31) / 32) * 4, s));
+    }
     vbs_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(codes, lens, n, K, mode, dt->deep,
                                                          (const uint32_t* const*)dt->exist,
-                                                         (const int64_t* const*)dt->dir,
-                                                         dt->rexist);
+                                                         (const int64_t* const*)dt->dir, dcode,
+                                                         dlen);
     BSB_LAUNCH_CHECK();
+    if (mode == BSB_DEEP_SLICED && cnt2 > 0) {
+      vbs_deep_planes_kernel<<<grid_for(cnt2, 256), 256, 0, s>>>(dcode, dlen, cnt2, K, dt->deep,
+                                                                 dt->rexist);
+      BSB_LAUNCH_CHECK();
+      BSB_CUDA(cudaFreeAsync(dcode, s));
+      BSB_CUDA(cudaFreeAsync(dlen, s));
+    }
   }
   BSB_CUDA(cudaFreeAsync(counts, s));
   BSB_CUDA(cudaFreeAsync(dt, s));

@@ -62,12 +62,6 @@ int persistent_grid(K kernel, int threads, int64_t work_items_per_cta_iter, int6
   return (int)(want < cap ? want : cap);
 }
 
-// Row swizzle inside one 32-byte block of a byte plane: row r -> byte
-// ((r & 7) << 2) | (r >> 3).  Word i (bytes 4i..4i+3) then holds rows
-// {i, 8+i, 16+i, 24+i}, which lets cmp_block() build lane masks with
-// PRMT + shifted adds and no bit gather.
-__host__ __device__ __forceinline__ int swz(int r) { return ((r & 7) << 2) | (r >> 3); }
-
 // 256-bit read-only streaming load (sm_100: LDG.E.NA.ENL2.256.CONSTANT).
 __device__ __forceinline__ void ldg256(const void* p, uint32_t (&w)[8]) {
   asm volatile(
@@ -77,9 +71,121 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
-// Literal constants for one level of one comparison leg: adding (255 - L)
-// to a byte in a 16-bit lane carries into bit 8 iff byte > L; adding
-// (256 - L) carries iff byte >= L.
+// ---------------------------------------------------------------------------
+// Bit-plane block layout of a byte plane ("BP32").  Every byte plane of the
+// device layouts (ByteSlice slices, the PP-VBS first slice, the SLICED deep
+// planes) stores the 32 bytes of one 32-row block -- exactly one 32-byte DRAM
+// sector, as in the reference's byte slices -- as 8 uint32 words:
+//   word k (k = 0..7) = bit (7 - k) of the byte of every row, bit r = row r.
+// The bytes, the sectors a scan touches and the early-stopping decisions are
+// the reference's (byteslice.py:56-106, vbs.py:222-289); only the order of the
+// bits inside a sector differs.  One 256-bit load gives a lane its block's 8
+// words, and a comparison with a literal byte is a carry chain over the bit
+// planes: x >= T  <=>  x + (256 - T) carries out of 8 bits, and with the
+// addend bits a_p as all-zero / all-one masks each carry step is one
+// majority LOP3 for 32 rows at once:  c_{p+1} = maj(x_p, a_p, c_p).
+// Results come out as row-ordered lane masks: no byte split, no gather.
+// (Round 1 stored the bytes row-swizzled and compared them with SWAR carry
+// tricks: ~10 integer instructions per 4 bytes per threshold; the carry
+// chain is 8 per 32 bytes.)
+
+// Addend masks of one threshold: m[p] = bit p of the addend ? ~0 : 0.
+struct PlaneLit {
+  uint32_t m[8];
+};
+// Addend for "x > L" / "x >= L" of a literal byte L: a = 255 - L, carry-in
+// 0 (>) or 1 (>=).
+__host__ inline PlaneLit make_plane_lit(uint32_t byte) {
+  PlaneLit l;
+  const uint32_t a = 255u - (byte & 0xFFu);
+  for (int p = 0; p < 8; ++p) l.m[p] = ((a >> p) & 1u) ? kFull : 0u;
+  return l;
+}
+// Threshold "x >= t" for t in 0..256: addend (256 - t) & 255 with carry-in
+// 1 only for t == 0 (everything).
+struct PlaneThr {
+  PlaneLit a;
+  uint32_t c0;
+};
+__host__ inline PlaneThr make_plane_thr(int t) {
+  PlaneThr r;
+  const uint32_t add = t == 0 ? 255u : (uint32_t)(256 - t) & 0xFFu;
+  for (int p = 0; p < 8; ++p) r.a.m[p] = ((add >> p) & 1u) ? kFull : 0u;
+  r.c0 = t == 0 ? kFull : 0u;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
+  return (a & b) | (c & (a | b));  // one LOP3 (0xE8)
+}
+
+// Carry out of x + a + c0 over the 8 bit planes (LSB plane = word 7).
+__device__ __forceinline__ uint32_t bp_carry(const uint32_t (&w)[8], const PlaneLit& L,
+                                             uint32_t c0) {
+  uint32_t c = c0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) c = maj3(w[7 - p], L.m[p], c);
+  return c;
+}
+
+// One literal byte: gt = [x > L], ge = [x >= L], row-ordered lane masks.
+__device__ __forceinline__ void cmp_block(const uint32_t (&w)[8], const PlaneLit& L,
+                                          uint32_t& gt, uint32_t& ge) {
+  gt = bp_carry(w, L, 0u);
+  ge = bp_carry(w, L, kFull);
+}
+// Two literals at once (fused BETWEEN).
+__device__ __forceinline__ void cmp_block2(const uint32_t (&w)[8], const PlaneLit& A,
+                                           const PlaneLit& B, uint32_t& gtA, uint32_t& geA,
+                                           uint32_t& gtB, uint32_t& geB) {
+  gtA = bp_carry(w, A, 0u);
+  geA = bp_carry(w, A, kFull);
+  gtB = bp_carry(w, B, 0u);
+  geB = bp_carry(w, B, kFull);
+}
+// "x >= t" for a host-prepared threshold.
+__device__ __forceinline__ uint32_t bp_ge(const uint32_t (&w)[8], const PlaneThr& T) {
+  return bp_carry(w, T.a, T.c0);
+}
+
+// Byte of row r from its block's 8 bit-plane words.
+__device__ __forceinline__ uint32_t bp_byte(const uint32_t (&w)[8], int r) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) b = (b << 1) | ((w[k] >> r) & 1u);
+  return b;
+}
+
+// Byte of row r of a bit-plane block in global memory (one 32-byte sector).
+__device__ __forceinline__ uint32_t bp_row_byte(const uint8_t* blk, int r) {
+  uint32_t w[8];
+  ldg256(blk, w);
+  return bp_byte(w, r);
+}
+// ... and of a block staged in shared memory (16-byte aligned).
+__device__ __forceinline__ uint32_t bp_row_byte_smem(const uint8_t* blk, int r) {
+  const uint4 a = reinterpret_cast<const uint4*>(blk)[0];
+  const uint4 b = reinterpret_cast<const uint4*>(blk)[1];
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  return bp_byte(w, r);
+}
+
+// Warp-cooperative write of one block of a plane: lane r holds row r's byte;
+// lanes 0..7 store words 0..7 (one 32-byte sector).
+__device__ __forceinline__ void bp_store_block(uint8_t* blk, uint32_t byte, int lane) {
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t wk = __ballot_sync(kFull, (byte >> (7 - k)) & 1u);
+    if (lane == k) mine = wk;
+  }
+  if (lane < 8) reinterpret_cast<uint32_t*>(blk)[lane] = mine;
+}
+
+// Round-1 byte-split literal constants, still used by the reference-packed
+// deep runs (BSB_DEEP_PACKED, variable-length byte runs per block): adding
+// (255 - L) to a byte in a 16-bit lane carries into bit 8 iff byte > L;
+// adding (256 - L) carries iff byte >= L.
 struct LevelLit {
   uint32_t cgt;
   uint32_t cge;
@@ -89,121 +195,6 @@ __host__ __device__ inline LevelLit make_level_lit(uint32_t byte) {
   l.cgt = (255u - byte) * 0x00010001u;
   l.cge = (256u - byte) * 0x00010001u;
   return l;
-}
-
-// Compare the 32 swizzled bytes of one block against one literal byte:
-// returns (gt, ge) lane masks in row order.
-__device__ __forceinline__ void cmp_block(const uint32_t (&w)[8], LevelLit L, uint32_t& gt,
-                                          uint32_t& ge) {
-  uint32_t g = 0, e = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);  // [b0, 0, b2, 0]
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);  // [b1, 0, b3, 0]
-    const uint32_t gf = __byte_perm(ev + L.cgt, od + L.cgt, 0x7351);  // carry bytes -> 0/1
-    const uint32_t ef = __byte_perm(ev + L.cge, od + L.cge, 0x7351);
-    g += gf << i;  // byte k, bit i  == row 8k + i
-    e += ef << i;
-  }
-  gt = g;
-  ge = e;
-}
-
-// cmp_block for PP-VBS levels: a literal byte 0xFF (PPE's right-most pointer
-// slot, the first byte of every long code in the skewed columns) has nothing
-// above it, so only the >= (here: ==) carries are computed.
-__device__ __forceinline__ void cmp_block_vbs(const uint32_t (&w)[8], LevelLit L, uint32_t& gt,
-                                              uint32_t& ge) {
-  if (L.cgt != 0u) {
-    cmp_block(w, L, gt, ge);
-    return;
-  }
-  uint32_t e = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    e += __byte_perm(ev + L.cge, od + L.cge, 0x7351) << i;
-  }
-  gt = 0u;
-  ge = e;
-}
-
-// Two literals at once (fused BETWEEN), sharing the byte split.
-__device__ __forceinline__ void cmp_block2(const uint32_t (&w)[8], LevelLit A, LevelLit B,
-                                           uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
-                                           uint32_t& geB) {
-  uint32_t ga = 0, ea = 0, gb = 0, eb = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
-    ea += __byte_perm(ev + A.cge, od + A.cge, 0x7351) << i;
-    gb += __byte_perm(ev + B.cgt, od + B.cgt, 0x7351) << i;
-    eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
-  }
-  gtA = ga;
-  geA = ea;
-  gtB = gb;
-  geB = eb;
-}
-
-// Level-1 compares for a lo literal byte 0x00 (the top byte of every small
-// rank): everything is >= it, so only the > carries are computed.  Selected
-// by a kernel template argument, never by a branch inside the compare.
-__device__ __forceinline__ void cmp_block_z(const uint32_t (&w)[8], LevelLit L, uint32_t& gt,
-                                            uint32_t& ge) {
-  uint32_t g = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    g += __byte_perm(ev + L.cgt, od + L.cgt, 0x7351) << i;
-  }
-  gt = g;
-  ge = kFull;
-}
-__device__ __forceinline__ void cmp_block2_z(const uint32_t (&w)[8], LevelLit A, LevelLit B,
-                                             uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
-                                             uint32_t& geB) {
-  uint32_t ga = 0, gb = 0, eb = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
-    gb += __byte_perm(ev + B.cgt, od + B.cgt, 0x7351) << i;
-    eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
-  }
-  gtA = ga;
-  geA = kFull;
-  gtB = gb;
-  geB = eb;
-}
-
-// cmp_block2 for PP-VBS levels: when the hi literal byte is 0xFF only its
-// >= carries are needed (nothing is above 0xFF).
-__device__ __forceinline__ void cmp_block2_vbs(const uint32_t (&w)[8], LevelLit A, LevelLit B,
-                                               uint32_t& gtA, uint32_t& geA, uint32_t& gtB,
-                                               uint32_t& geB) {
-  if (B.cgt != 0u) {
-    cmp_block2(w, A, B, gtA, geA, gtB, geB);
-    return;
-  }
-  uint32_t ga = 0, ea = 0, eb = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    ga += __byte_perm(ev + A.cgt, od + A.cgt, 0x7351) << i;
-    ea += __byte_perm(ev + A.cge, od + A.cge, 0x7351) << i;
-    eb += __byte_perm(ev + B.cge, od + B.cge, 0x7351) << i;
-  }
-  gtA = ga;
-  geA = ea;
-  gtB = 0u;
-  geB = eb;
 }
 
 // Packed-order compare of 4 consecutive bytes (rank 4i..4i+3): 4-bit masks.

@@ -34,7 +34,8 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
        i0 += nthr * kIdsPerThread) {
-    int64_t pos[kIdsPerThread];
+    int64_t blk[kIdsPerThread];
+    int lr[kIdsPerThread];
     uint64_t c[kIdsPerThread];
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
@@ -44,14 +45,23 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
         oob = true;
         r = 0;
       }
-      pos[u] = (r & ~int64_t(31)) + swz((int)(r & 31));
+      blk[u] = r >> 5;
+      lr[u] = (int)(r & 31);
       c[u] = 0;
     }
     for (int j = 0; j < K; ++j) {
+      uint32_t w[kIdsPerThread][8];
 #pragma unroll
-      for (int u = 0; u < kIdsPerThread; ++u)
-        if (i0 + u * nthr < n_ids)
-          c[u] = (c[u] << 8) | __ldg(slices + (int64_t)j * stride + pos[u]);
+      for (int u = 0; u < kIdsPerThread; ++u) {
+        if (i0 + u * nthr < n_ids) {
+          ldg256(slices + (int64_t)j * stride + blk[u] * 32, w[u]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[u][q] = 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kIdsPerThread; ++u) c[u] = (c[u] << 8) | bp_byte(w[u], lr[u]);
     }
 #pragma unroll
     for (int u = 0; u < kIdsPerThread; ++u) {
@@ -117,7 +127,7 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
     }
     const int64_t b = r >> 5;
     const int lr = (int)(r & 31);
-    uint64_t code = (uint64_t)__ldg(d.bs1 + (b * 32 + swz(lr))) << (8 * (K - 1));
+    uint64_t code = (uint64_t)bp_row_byte(d.bs1 + b * 32, lr) << (8 * (K - 1));
     const uint32_t below = (1u << lr) - 1u;
     lc[0] += 1;
     int64_t pos2 = 0;
@@ -133,7 +143,7 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
         if (q == j - 1) lc[q] += 1;
       uint64_t byte;
       if (d.mode == BSB_DEEP_SLICED) {
-        byte = __ldg(d.deep[j - 1] + ((pos2 & ~int64_t(31)) + swz((int)(pos2 & 31))));
+        byte = bp_row_byte(d.deep[j - 1] + (pos2 >> 5) * 32, (int)(pos2 & 31));
       } else {
         const int64_t pos = __ldg(d.dir[j - 1] + b) + __popc(w & below);
         byte = __ldg(d.deep[j - 1] + pos);
@@ -512,7 +522,7 @@ __device__ __forceinline__ uint64_t vbs_row_code_f(const VbsLookupDesc& d, int64
     if (j > len) continue;  // predicated, not a break: the loads issue together
     uint32_t byte;
     if (mode == BSB_DEEP_SLICED) {
-      byte = __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
+      byte = bp_row_byte(d.deep[j - 1] + (q >> 5) * 32, (int)(q & 31));
     } else {
       byte = __ldg(d.deep[j - 1] + (__ldg(d.dir[j - 1] + blk) + __popc(mt.m[j - 1] & below)));
     }
@@ -523,7 +533,7 @@ __device__ __forceinline__ uint64_t vbs_row_code_f(const VbsLookupDesc& d, int64
 
 __device__ __forceinline__ uint64_t vbs_row_code(const VbsLookupDesc& d, int64_t blk, int lr,
                                                  const VbsBlockMeta& mt, int& len) {
-  return vbs_row_code_f(d, blk, lr, mt, __ldg(d.bs1 + (blk * 32 + swz(lr))), len);
+  return vbs_row_code_f(d, blk, lr, mt, bp_row_byte(d.bs1 + blk * 32, lr), len);
 }
 
 __device__ __forceinline__ void emit(uint64_t* oc, int64_t* ov, int32_t* ov32, int64_t pos,
@@ -660,12 +670,10 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           const uint32_t r = on[u] ? idx[k] : 0u;
           const int bl = (int)((r >> 5) & 31);
           const int lr = (int)(r & 31);
-          const int off = bl * 32 + swz(lr);
           if (VBS) {
             len[u] = on[u] ? 1 + (int)((r >> 10) & 7u) : 1;
-            uint64_t cd = stage[off];
+            uint64_t cd = bp_row_byte_smem(stage + bl * 32, lr);
             const int64_t q = MODE == BSB_DEEP_PACKED ? 0 : sdir[bl] + (r >> 13);
-            const int64_t qs = (q & ~int64_t(31)) + swz((int)(q & 31));
             const int64_t blkr = t * 32 + bl;
             const uint32_t below = (1u << lr) - 1u;
 #pragma unroll
@@ -673,7 +681,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
               if (j <= KL && j <= len[u]) {
                 uint32_t byte;
                 if (MODE == BSB_DEEP_SLICED) {
-                  byte = __ldg(vd.deep[j - 1] + qs);
+                  byte = bp_row_byte(vd.deep[j - 1] + (q >> 5) * 32, (int)(q & 31));
                 } else {
                   byte = __ldg(vd.deep[j - 1] + (__ldg(vd.dir[j - 1] + blkr) +
                                                  __popc(smeta[(j - 2) * 32 + bl] & below)));
@@ -687,7 +695,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
             uint64_t cd = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLevels; ++j)
-              if (j < K) cd = (cd << 8) | stage[j * 1024 + off];
+              if (j < K) cd = (cd << 8) | bp_row_byte_smem(stage + j * 1024 + bl * 32, lr);
             code[u] = pad[u] = cd >> shift;
             len[u] = 0;
           }
@@ -738,7 +746,7 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
       }
       const int64_t blk = r >> 5;
       const int lr = (int)(r & 31);
-      const uint32_t first = __ldg(vd.bs1 + (blk * 32 + swz(lr)));
+      const uint32_t first = bp_row_byte(vd.bs1 + blk * 32, lr);
       // a row outside M_2 has a 1-byte code: no deeper existence words,
       // directory entry or deep bytes to fetch
       const uint32_t m2 = vd.K >= 2 ? __ldg(vd.exist[1] + blk) : 0u;

@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t tile_valid(int64_t tile, int64_t b, int64_t 
 // Persistent grid-stride kernel: one warp per tile, the next tile's level-1
 // operands (and two tiles ahead, its input-mask word) are fetched while the
 // current tile is scanned.
-template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED, bool L1Z = false>
+template <int LAYOUT, bool BETWEEN, bool STATS, bool MASKED>
 __global__ void __launch_bounds__(kScanThreads, 1)
     scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     int depth = 0;
     uint32_t res;
     if (LAYOUT == BSB_LAYOUT_BYTESLICE)
-      res = scan_tile_bs<BETWEEN, STATS, L1Z>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
+      res = scan_tile_bs<BETWEEN, STATS>(a.bs, a.A, a.B, b, valid, in, &st, &depth);
     else
       res = scan_tile_vbs<BETWEEN, STATS>(a.vbs, a.A, a.B, tile, b, valid, in, &st, &depth);
     if (b < a.nb) {
@@ -130,6 +130,120 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
   flush_stats<STATS>(a, st);
+}
+
+// ---------------------------------------------------------------------------
+// ByteSlice scan without stats: persistent warps, lane = 32-row block, and a
+// two-stage software pipeline per warp.  While tile Y's level-2 sectors are
+// compared, tile X (the next one) has had its level-1 compare done and its
+// level-2 loads issued, and tile X's successor has its level-1 sectors in
+// flight: the dependent level-2 round trip (byteslice.py:92-95: a block
+// reads slice 2 only while it has tied rows) overlaps a whole tile of work.
+struct BsState {
+  uint32_t valid, zgtA, zeqA, zgtB, zeqB;
+};
+
+template <bool BETWEEN>
+__device__ __forceinline__ void bs_level(const uint32_t (&w)[8], const Leg& A, const Leg& B,
+                                         int j, BsState& s) {
+  if (BETWEEN) {
+    uint32_t gA, eA, gB, eB;
+    cmp_block2(w, A.pl[j], B.pl[j], gA, eA, gB, eB);
+    s.zgtA |= s.zeqA & gA;
+    s.zeqA &= eA & ~gA;
+    s.zgtB |= s.zeqB & gB;
+    s.zeqB &= eB & ~gB & (s.zeqA | s.zgtA);  // hi-leg ties that already fail GE(lo)
+  } else {
+    uint32_t g, e;
+    cmp_block(w, A.pl[j], g, e);
+    s.zgtA |= s.zeqA & g;
+    s.zeqA &= e & ~g;
+  }
+}
+
+template <bool BETWEEN>
+__device__ __forceinline__ bool bs_tied(const BsState& s) {
+  return BETWEEN ? ((s.zeqA | s.zeqB) != 0) : (s.zeqA != 0);
+}
+
+template <bool BETWEEN, bool MASKED>
+__global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_constant__ ScanArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int K = a.bs.K;
+  const int64_t stride = a.bs.stride;
+  const uint8_t* sl = a.bs.slices;
+  unsigned long long cnt = 0;
+  auto valid_of = [&](int64_t tile, uint32_t mword) -> uint32_t {
+    return tile_valid(tile, tile * 32 + lane, a.n_rows) & (MASKED ? mword : kFull);
+  };
+  int64_t tX = warp;
+  uint32_t vN = 0, mN = kFull, wN[8];
+  if (tX < a.ntiles) {
+    if (MASKED) mN = mask_raw<true>(a, tX * 32 + lane);
+    vN = valid_of(tX, mN);
+    if (vN) ldg256(sl + (tX * 32 + lane) * 32, wN);
+    if (MASKED) mN = mask_raw<true>(a, (tX + nwarps) * 32 + lane);
+  }
+  BsState sY;
+  uint32_t w2Y[8];
+  int64_t tY = -1;
+  for (;;) {
+    // ---- stage X: level 1 of tile tX, issue its level-2 loads
+    const bool haveX = tX < a.ntiles;
+    BsState sX;
+    uint32_t w2X[8];
+    if (haveX) {
+      uint32_t w1[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w1[q] = wN[q];
+      sX.valid = vN;
+      const int64_t tn = tX + nwarps;
+      if (tn < a.ntiles) {
+        vN = valid_of(tn, mN);
+        if (vN) ldg256(sl + (tn * 32 + lane) * 32, wN);
+        if (MASKED) mN = mask_raw<true>(a, (tn + nwarps) * 32 + lane);
+      }
+      sX.zgtA = 0;
+      sX.zeqA = sX.valid;
+      sX.zgtB = 0;
+      sX.zeqB = sX.valid;
+      bs_level<BETWEEN>(w1, a.A, a.B, 0, sX);
+      if (K >= 2 && bs_tied<BETWEEN>(sX)) ldg256(sl + stride + (tX * 32 + lane) * 32, w2X);
+    }
+    // ---- stage Y: levels 2..K of tile tY, result word
+    if (tY >= 0) {
+      if (K >= 2 && __any_sync(kFull, bs_tied<BETWEEN>(sY))) {
+        if (bs_tied<BETWEEN>(sY)) bs_level<BETWEEN>(w2Y, a.A, a.B, 1, sY);
+#pragma unroll
+        for (int j = 2; j < kMaxLevels; ++j) {
+          if (j >= K) break;
+          const bool act = bs_tied<BETWEEN>(sY);
+          if (!__any_sync(kFull, act)) break;
+          if (act) {
+            uint32_t w[8];
+            ldg256(sl + (int64_t)j * stride + (tY * 32 + lane) * 32, w);
+            bs_level<BETWEEN>(w, a.A, a.B, j, sY);
+          }
+        }
+      }
+      const uint32_t res = BETWEEN ? sY.valid & (sY.zgtA | sY.zeqA) & ~sY.zgtB
+                                   : finalize_op(a.A.op, sY.zgtA, sY.zeqA, sY.valid);
+      const int64_t b = tY * 32 + lane;
+      if (b < a.nb) a.out[b] = res;
+      cnt += __popc(res);
+    }
+    if (!haveX) break;
+    tY = tX;
+    sY = sX;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w2Y[q] = w2X[q];
+    tX += nwarps;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
 // Trivial predicates (vbs.py:200-208): true -> mask & valid, false -> 0.
@@ -161,7 +275,10 @@ static void fill_leg(Leg& L, int op, uint64_t code, int len, int levels) {
     uint32_t byte = 0;
     if (j < levels) byte = (uint32_t)((code >> (8 * (levels - 1 - j))) & 0xFF);
     L.byte[j] = byte;
-    if (j < kMaxLevels) L.lv[j] = make_level_lit(byte);
+    if (j < kMaxLevels) {
+      L.lv[j] = make_level_lit(byte);
+      L.pl[j] = make_plane_lit(byte);
+    }
   }
 }
 
@@ -217,15 +334,13 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   const bool stats = a.stats != nullptr;
   BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
-    // ByteSlice with a level-1 literal byte 0x00: the variant without the >=
-    // carries of that literal
-    if (LAYOUT == BSB_LAYOUT_BYTESLICE && a.A.byte[0] == 0u) {
+    if (LAYOUT == BSB_LAYOUT_BYTESLICE) {
       if (a.mask) {
-        if (between) return launch_scan(scan_kernel<LAYOUT, true, false, true, true>, a, s);
-        return launch_scan(scan_kernel<LAYOUT, false, false, true, true>, a, s);
+        if (between) return launch_scan(bs_scan_kernel<true, true>, a, s);
+        return launch_scan(bs_scan_kernel<false, true>, a, s);
       }
-      if (between) return launch_scan(scan_kernel<LAYOUT, true, false, false, true>, a, s);
-      return launch_scan(scan_kernel<LAYOUT, false, false, false, true>, a, s);
+      if (between) return launch_scan(bs_scan_kernel<true, false>, a, s);
+      return launch_scan(bs_scan_kernel<false, false>, a, s);
     }
     if (a.mask) {
       if (between) return launch_scan(scan_kernel<LAYOUT, true, false, true>, a, s);

@@ -25,7 +25,8 @@ namespace bsb {
 struct Leg {
   int32_t len;                 // levels examined (ByteSlice: K; PP-VBS: literal bytes)
   int32_t op;                  // operator when this is the only leg
-  LevelLit lv[kMaxLevels];
+  PlaneLit pl[kMaxLevels];     // bit-plane carry masks per level (bit-plane blocks)
+  LevelLit lv[kMaxLevels];     // byte-split constants (reference-packed deep runs)
   uint32_t byte[kMaxLevels + 1];  // literal byte per level, 0-padded (one spare)
 };
 
@@ -93,12 +94,11 @@ __device__ __forceinline__ void fetch_vbs(const VbsDesc& d, int64_t tile, int64_
 }
 
 // ---------------------------------------------------------------- ByteSlice
-// levels >= 2 where every live block has at most this many tied rows compare
-// those rows' bytes one by one instead of the 32-byte SWAR compare
-constexpr int kSparseRows = 4;
-
-// L1Z: the (lo) literal's level-1 byte is 0x00 (host-selected variant).
-template <bool BETWEEN, bool STATS, bool L1Z = false>
+// One tile: lane b compares its block level by level (byteslice.py:86-106):
+// the level-j sector is loaded only while the block still has tied rows,
+// and the warp stops once no lane has one.  Levels are unrolled so every
+// literal mask is a constant-bank operand of its LOP3.
+template <bool BETWEEN, bool STATS>
 __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, const Leg& B,
                                                  int64_t b, uint32_t valid, const TileIn& in,
                                                  StatAcc* st, int* depth_out) {
@@ -107,18 +107,10 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
   // level 1: every lane, branch free (invalid lanes carry zero state)
   {
     uint32_t gA, eA, gB, eB;
-    if (BETWEEN && A.byte[0] != B.byte[0]) {
-      if (L1Z)
-        cmp_block2_z(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
-      else
-        cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+    if (BETWEEN) {
+      cmp_block2(in.w, A.pl[0], B.pl[0], gA, eA, gB, eB);
     } else {
-      if (L1Z)
-        cmp_block_z(in.w, A.lv[0], gA, eA);
-      else
-        cmp_block(in.w, A.lv[0], gA, eA);
-      gB = gA;
-      eB = eA;
+      cmp_block(in.w, A.pl[0], gA, eA);
     }
     if (STATS && valid) {
       depth = 1;
@@ -132,35 +124,11 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
     }
   }
   const uint8_t* base = d.slices + b * 32;
-  for (int j = 1; j < d.K; ++j) {
+#pragma unroll
+  for (int j = 1; j < kMaxLevels; ++j) {
+    if (j >= d.K) break;
     const bool act = BETWEEN ? ((zeqA | zeqB) != 0) : (zeqA != 0);
     if (!__any_sync(kFull, act)) break;
-    const uint32_t cand = BETWEEN ? (zeqA | zeqB) : zeqA;
-    if (BETWEEN && !STATS && !__any_sync(kFull, __popc(cand) > kSparseRows)) {
-      // every live block has only a few tied rows: compare just their bytes
-      if (act) {
-        uint32_t w[8];
-        ldg256(base + (int64_t)j * d.stride, w);
-        const uint32_t la = A.byte[j], lb = B.byte[j];
-        uint32_t gA = 0, eA = 0, gB = 0, eB = 0;
-        for (uint32_t rest = cand; rest; rest &= rest - 1) {
-          const int r = __ffs(rest) - 1;
-          uint32_t x = w[0];
-#pragma unroll
-          for (int q = 1; q < 8; ++q) x = (r & 7) == q ? w[q] : x;
-          const uint32_t by = (x >> ((r >> 3) << 3)) & 0xFFu, bit = 1u << r;
-          gA |= by > la ? bit : 0u;
-          eA |= by == la ? bit : 0u;
-          gB |= by > lb ? bit : 0u;
-          eB |= by == lb ? bit : 0u;
-        }
-        zgtA |= zeqA & gA;
-        zeqA &= eA;
-        zgtB |= zeqB & gB;
-        zeqB &= eB & (zeqA | zgtA);
-      }
-      continue;
-    }
     if (act) {
       uint32_t w[8];
       ldg256(base + (int64_t)j * d.stride, w);
@@ -168,23 +136,14 @@ __device__ __forceinline__ uint32_t scan_tile_bs(const BsDesc& d, const Leg& A, 
       stat_level<STATS>(st, j, 32);
       if (BETWEEN) {
         uint32_t gA, eA, gB, eB;
-        if (A.byte[j] == B.byte[j]) {
-          cmp_block(w, A.lv[j], gA, eA);
-          gB = gA;
-          eB = eA;
-        } else if (L1Z && A.byte[j] == 0u) {
-          // the L1Z variant also covers deeper lo bytes 0x00 (small ranks)
-          cmp_block2_z(w, A.lv[j], B.lv[j], gA, eA, gB, eB);
-        } else {
-          cmp_block2(w, A.lv[j], B.lv[j], gA, eA, gB, eB);
-        }
+        cmp_block2(w, A.pl[j], B.pl[j], gA, eA, gB, eB);
         zgtA |= zeqA & gA;
         zeqA &= eA & ~gA;
         zgtB |= zeqB & gB;
         zeqB &= eB & ~gB & (zeqA | zgtA);
       } else {
         uint32_t g, e;
-        cmp_block(w, A.lv[j], g, e);
+        cmp_block(w, A.pl[j], g, e);
         zgtA |= zeqA & g;
         zeqA &= e & ~g;
       }
@@ -283,9 +242,9 @@ __device__ __forceinline__ void vbs_level1(const Leg& A, const Leg& B, int K, ui
                                            uint32_t& eqfB, StatAcc* st, int& depth) {
   uint32_t gA, eA, gB, eB;
   if (BETWEEN && A.byte[0] != B.byte[0]) {
-    cmp_block2(in.w, A.lv[0], B.lv[0], gA, eA, gB, eB);
+    cmp_block2(in.w, A.pl[0], B.pl[0], gA, eA, gB, eB);
   } else {
-    cmp_block_vbs(in.w, A.lv[0], gA, eA);
+    cmp_block(in.w, A.pl[0], gA, eA);
     gB = gA;
     eB = eA;
   }

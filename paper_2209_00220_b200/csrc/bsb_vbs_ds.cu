@@ -46,10 +46,11 @@ struct DsArgs {
   int64_t nbpad;      // blocks covered by exist[1] / block_dir[1] (stride / 32)
   int serial_blocks;  // warp-cooperative pdep up to this many blocks per tile
   // Row-space level 1 (L1 variant): shallow result = valid & ~M_2 &
-  // ((P & ~Q) ^ inv) with P = [byte >= tP], Q = [byte >= tQ]; cP / cQ are the
-  // carry constants (256 - t) * 0x00010001 (t = 256 -> 0: never), cQ == 0
-  // skips the Q compare.
-  uint32_t cP, cQ, inv;
+  // ((P & ~Q) ^ inv) with P = [byte >= tP], Q = [byte >= tQ] (bit-plane
+  // thresholds, bsb_common.cuh); twoQ == 0 skips the Q compare (tQ = 256).
+  PlaneThr tP, tQ;
+  int twoQ;
+  uint32_t inv;
   // Level 1 of the deep rows when they all share one first byte (zone map):
   // d1 = 1, and the per-leg (gt, eq) masks are constants (kFull or 0).
   int d1;
@@ -65,47 +66,21 @@ __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Threshold compares of the 32 swizzled bytes of a block: P = [byte >= tP],
-// Q = [byte >= tQ] (constants as in DsArgs), lane masks in row order.
-template <bool TWO>
-__device__ __forceinline__ void thr_cmp(const uint32_t (&w)[8], uint32_t cP, uint32_t cQ,
-                                        uint32_t& P, uint32_t& Q) {
-  uint32_t p = 0, q = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t ev = __byte_perm(w[i], 0, 0x4240);
-    const uint32_t od = __byte_perm(w[i], 0, 0x4341);
-    p += __byte_perm(ev + cP, od + cP, 0x7351) << i;
-    if (TWO) q += __byte_perm(ev + cQ, od + cQ, 0x7351) << i;
-  }
-  P = p;
-  Q = TWO ? q : 0u;
-}
-
-// (A literal byte 0x00 shortcut -- gt-only compares -- measured 15-20 %
-// slower: the extra compare bodies cost more than the carries they save.)
-// (gt, eq) of both legs at level index j0 (0-based).  One literal byte 0xFF
-// (PPE's right-most pointer slot) needs only the equality carries; two
-// different bytes take the four-compare form (whose constants already give
-// gt = 0 for 0xFF and ge = all for 0x00).
+// (gt, eq) of both legs at level index j0 (0-based) over a bit-plane block;
+// legs with the same literal byte share one compare.
 template <bool BETWEEN>
 __device__ __forceinline__ void cmp_level(const uint32_t (&w)[8], const Leg& A, const Leg& B,
                                           int j0, uint32_t& gA, uint32_t& eA, uint32_t& gB,
                                           uint32_t& eB) {
-  const LevelLit la = A.lv[j0];
   if (!BETWEEN || A.byte[j0] == B.byte[j0]) {
     uint32_t ge;
-    if (la.cgt == 0u) {
-      cmp_block_vbs(w, la, gA, ge);  // equality only
-    } else {
-      cmp_block(w, la, gA, ge);
-    }
+    cmp_block(w, A.pl[j0], gA, ge);
     eA = ge & ~gA;
     gB = gA;
     eB = eA;
   } else {
     uint32_t geA, geB;
-    cmp_block2(w, la, B.lv[j0], gA, geA, gB, geB);
+    cmp_block2(w, A.pl[j0], B.pl[j0], gA, geA, gB, geB);
     eA = geA & ~gA;
     eB = geB & ~gB;
   }
@@ -287,11 +262,8 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
             for (int i = 0; i < 8; ++i) wN[i] = 0;
           }
         }
-        uint32_t P, Q;
-        if (a.cQ)
-          thr_cmp<true>(w, a.cP, a.cQ, P, Q);
-        else
-          thr_cmp<false>(w, a.cP, 0u, P, Q);
+        const uint32_t P = bp_ge(w, a.tP);
+        const uint32_t Q = a.twoQ ? bp_ge(w, a.tQ) : 0u;
         res = valid & ~m2 & ((P & ~Q) ^ a.inv);
       }
       rs[u] = res;
@@ -454,7 +426,6 @@ static int tune(int i) {
 bool ds_enabled(bool masked) { return masked ? tune(0) == 1 : tune(0) != 0; }
 bool ds_zonemap_enabled() { return tune(4) != 0; }
 
-static uint32_t carry_const(int t) { return (uint32_t)(256 - t) * 0x00010001u; }
 
 // Scan of a SLICED column that carries deep[0] (K >= 2), optionally masked.
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
@@ -516,8 +487,9 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
         break;
     }
   }
-  a.cP = carry_const(tP);
-  a.cQ = carry_const(tQ);
+  a.tP = make_plane_thr(tP);
+  a.tQ = make_plane_thr(tQ);
+  a.twoQ = tQ < 256;
   a.inv = inv;
   const bool l1 = inv != 0 || (tP < 256 && tP < tQ);  // else no shallow row can match
   BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));

@@ -33,9 +33,9 @@ struct RowArgs {
   int32_t depth_max;
 };
 
-// byte j of deep row q (SLICED: swizzled 32-deep-row blocks)
+// byte j of deep row q (SLICED: bit-plane 32-deep-row blocks)
 __device__ __forceinline__ uint32_t plane_byte(const VbsDesc& d, int64_t q, int j) {
-  return __ldg(d.deep[j - 1] + ((q & ~int64_t(31)) + swz((int)(q & 31))));
+  return bp_row_byte(d.deep[j - 1] + (q >> 5) * 32, (int)(q & 31));
 }
 
 __global__ void __launch_bounds__(256) vbs_rowscan_kernel(const __grid_constant__ RowArgs a) {
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) vbs_rowscan_kernel(const __grid_constant_
       const int64_t q = K >= 2 ? __ldg(d.dir[1] + b) + __popc(m[1] & below) : 0;
       t = 1;
       for (int j = 1;; ++j) {
-        const uint32_t cj = j == 1 ? (uint32_t)__ldg(d.bs1 + b * 32 + swz(lane))
+        const uint32_t cj = j == 1 ? bp_row_byte(d.bs1 + b * 32, lane)
                                    : plane_byte(d, q, j);
         const uint32_t lj = a.L.byte[j - 1];
         if (cj != lj) {

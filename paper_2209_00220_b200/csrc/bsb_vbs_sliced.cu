@@ -199,9 +199,9 @@ __global__ void __launch_bounds__(kSlicedThreads, MINB)
           const uint32_t nxt = (j < K && act) ? __ldg(d.rexist[j] + dbk) : 0u;
           uint32_t gA, eA, gB, eB;
           if (BETWEEN && A.byte[j - 1] != B.byte[j - 1]) {
-            cmp_block2_vbs(w, A.lv[j - 1], B.lv[j - 1], gA, eA, gB, eB);
+            cmp_block2(w, A.pl[j - 1], B.pl[j - 1], gA, eA, gB, eB);
           } else {
-            cmp_block_vbs(w, A.lv[j - 1], gA, eA);
+            cmp_block(w, A.pl[j - 1], gA, eA);
             gB = gA;
             eB = eA;
           }
