@@ -48,10 +48,15 @@ def _q(uniq: np.ndarray, counts: np.ndarray, n: int, x: float) -> int:
 
 def _alg_bytes(cols, preds):
     """Pipelined algorithmic bytes of a conjunction: each
-    predicate's own slice/mask terms over the blocks still live."""
+    predicate's own slice/mask terms over the blocks still live, in the order
+    engine.conj_scan evaluates them (engine.conj_order)."""
     from paper_2209_00220_b200.byteslice import scan_byteslice
+    from paper_2209_00220_b200.engine import conj_order
     from paper_2209_00220_b200.roofline import scan_alg_bytes
     from paper_2209_00220_b200.vbs import scan_vbs
+    order = conj_order([c[0] for c in cols])
+    cols = [cols[i] for i in order]
+    preds = [preds[i] for i in order]
     total, running = 0, None
     for (lay, c, ex), p in zip(cols, preds):
         fn = scan_vbs if lay == "ppvbs" else scan_byteslice

@@ -140,8 +140,11 @@ const char* bsb_version(void);
  * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
  * scans only), "ds_serial" (warp-cooperative pdep up to this many blocks per
  * tile), "ds_tiles" (tiles per super-tile, 0 = auto), "ds_unroll" (0/1),
- * "ds_zonemap" (0/1: settle level 1 from deep1_shared).  Unknown key:
- * BSB_EINVAL. */
+ * "ds_zonemap" (0/1: settle level 1 from deep1_shared), "sparse_ppm"
+ * (masked PP-VBS scans inside bsb_conj_scan skip masked-out deep blocks when
+ * the running mask holds at most this many rows per million, and otherwise
+ * scan the column whole and AND the mask into the result words; default
+ * 1000).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

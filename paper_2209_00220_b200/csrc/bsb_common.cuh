@@ -148,12 +148,23 @@ __device__ __forceinline__ uint32_t bp_ge(const uint32_t (&w)[8], const PlaneThr
   return bp_carry(w, T.a, T.c0);
 }
 
-// Byte of row r from its block's 8 bit-plane words.
+// Byte of row r from its block's 8 bit-plane words: the byte column r >> 3
+// of words 0..3 and 4..7 gathered with PRMT, each byte's bit (r & 7) moved to
+// bit 0, and the four 0/1 bytes of each half packed into a nibble with one
+// multiply (bits 28..31 of x * (2^28 + 2^21 + 2^14 + 2^7); no carries, the
+// other partial products land on distinct lower bits).
 __device__ __forceinline__ uint32_t bp_byte(const uint32_t (&w)[8], int r) {
-  uint32_t b = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) b = (b << 1) | ((w[k] >> r) & 1u);
-  return b;
+  const uint32_t c = (uint32_t)r >> 3;
+  const uint32_t sel = c * 0x11u + 0x40u;  // [a.c, b.c] in the low half
+  const uint32_t P = __byte_perm(__byte_perm(w[3], w[2], sel), __byte_perm(w[1], w[0], sel),
+                                 0x5410u);  // [w3.c, w2.c, w1.c, w0.c]
+  const uint32_t Q = __byte_perm(__byte_perm(w[7], w[6], sel), __byte_perm(w[5], w[4], sel),
+                                 0x5410u);  // [w7.c, w6.c, w5.c, w4.c]
+  const uint32_t sh = (uint32_t)r & 7u;
+  const uint32_t M = 0x10204080u;
+  const uint32_t hi = (((P >> sh) & 0x01010101u) * M) >> 24;  // bits 4..7: w3..w0
+  const uint32_t lo = (((Q >> sh) & 0x01010101u) * M) >> 28;  // bits 0..3: w7..w4
+  return (hi & 0xF0u) | lo;
 }
 
 // Byte of row r of a bit-plane block in global memory (one 32-byte sector).

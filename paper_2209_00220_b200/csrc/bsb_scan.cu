@@ -246,6 +246,186 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
+// ---------------------------------------------------------------------------
+// Fused conjunction of NP ByteSlice predicates (engine.py:322-332): one pass
+// per tile evaluates every predicate and ANDs the results in registers -- no
+// intermediate result words in HBM.  Level-1 sectors of all NP columns are
+// staged into shared memory by 1-D TMA bulk copies (cp.async.bulk, one
+// elected lane, completion on a per-warp mbarrier), two tiles ahead, so the
+// registers hold no prefetched data; deeper levels (tied rows only,
+// byteslice.py:92-95) are loaded directly, all predicates' loads of one level
+// in flight together.  Every predicate is evaluated on the tile's valid rows
+// and the results are AND-ed: the same words as the pipelined chain (the
+// chain evaluates predicate i on the rows still alive, and AND is
+// idempotent).
+constexpr int kConjMax = 4;
+struct BsConjArgs {
+  int64_t n_rows, nb, ntiles;
+  BsDesc c[kConjMax];
+  Leg A[kConjMax], B[kConjMax];
+  int32_t between[kConjMax];
+  const uint32_t* mask;
+  uint32_t* out;
+  unsigned long long* count;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool BETWEEN_ANY>
+__device__ __forceinline__ void conj_level(const uint32_t (&w)[8], const BsConjArgs& a, int p,
+                                           int j, BsState& s) {
+  if (BETWEEN_ANY && a.between[p])
+    bs_level<true>(w, a.A[p], a.B[p], j, s);
+  else
+    bs_level<false>(w, a.A[p], a.B[p], j, s);
+}
+__device__ __forceinline__ bool conj_tied(const BsConjArgs& a, int p, const BsState& s) {
+  return a.between[p] ? ((s.zeqA | s.zeqB) != 0) : (s.zeqA != 0);
+}
+__device__ __forceinline__ uint32_t conj_result(const BsConjArgs& a, int p, const BsState& s) {
+  return a.between[p] ? s.valid & (s.zgtA | s.zeqA) & ~s.zgtB
+                      : finalize_op(a.A[p].op, s.zgtA, s.zeqA, s.valid);
+}
+
+// Two-stage pipeline per warp as in bs_scan_kernel: tile X's level-1
+// sectors come from the TMA-filled stage and its level-2 loads are issued;
+// tile Y (the previous one) consumes its level-2 sectors, runs any deeper
+// level, ANDs the NP results and writes the word.
+template <int NP, bool MASKED>
+__global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_constant__ BsConjArgs a) {
+  constexpr int kW = kScanThreads / 32;
+  __shared__ __align__(128) uint8_t sbuf[kW][2][NP][1024];
+  __shared__ __align__(8) uint64_t sbar[kW][2];
+  const int lane = threadIdx.x & 31;
+  const int wq = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t* bar = sbar[wq];
+  auto issue = [&](int st, int64_t tile) {
+    if (lane == 0 && tile < a.ntiles) {
+      mbar_expect_tx(&bar[st], NP * 1024u);
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        bulk_g2s(sbuf[wq][st][p], a.c[p].slices + tile * 1024, 1024u, &bar[st]);
+    }
+  };
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  issue(0, warp);
+  issue(1, warp + nwarps);
+  uint32_t phases = 0u;  // bit st = parity to wait for on stage st
+  unsigned long long cnt = 0;
+  int st = 0;
+  BsState sY[NP];
+  uint32_t w2Y[NP][8];
+  int64_t tY = -1;
+  for (int64_t tX = warp;; tX += nwarps) {
+    const bool haveX = tX < a.ntiles;
+    BsState sX[NP];
+    uint32_t w2X[NP][8];
+    if (haveX) {
+      const int64_t b = tX * 32 + lane;
+      uint32_t valid = tile_valid(tX, b, a.n_rows);
+      if (MASKED) valid &= b < a.nb ? __ldg(a.mask + b) : 0u;
+      mbar_wait(&bar[st], (phases >> st) & 1u);
+      phases ^= 1u << st;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const uint4* src = reinterpret_cast<const uint4*>(sbuf[wq][st][p] + lane * 32);
+        const uint4 x = src[0], y = src[1];
+        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+        sX[p].valid = valid;
+        sX[p].zgtA = 0;
+        sX[p].zeqA = valid;
+        sX[p].zgtB = 0;
+        sX[p].zeqB = valid;
+        conj_level<true>(w, a, p, 0, sX[p]);
+      }
+      __syncwarp();  // every lane has read this stage: refill it two tiles ahead
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(st, tX + 2 * nwarps);
+      st ^= 1;
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (a.c[p].K >= 2 && conj_tied(a, p, sX[p]))
+          ldg256(a.c[p].slices + a.c[p].stride + b * 32, w2X[p]);
+    }
+    if (tY >= 0) {
+      const int64_t b = tY * 32 + lane;
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (a.c[p].K >= 2 && conj_tied(a, p, sY[p])) conj_level<true>(w2Y[p], a, p, 1, sY[p]);
+#pragma unroll
+      for (int j = 2; j < kMaxLevels; ++j) {
+        bool act[NP];
+        bool any = false;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          act[p] = j < a.c[p].K && conj_tied(a, p, sY[p]);
+          any |= act[p];
+        }
+        if (!__any_sync(kFull, any)) break;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          if (!act[p]) continue;
+          uint32_t w[8];
+          ldg256(a.c[p].slices + (int64_t)j * a.c[p].stride + b * 32, w);
+          conj_level<true>(w, a, p, j, sY[p]);
+        }
+      }
+      uint32_t res = sY[0].valid;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) res &= conj_result(a, p, sY[p]);
+      if (b < a.nb) a.out[b] = res;
+      cnt += __popc(res);
+    }
+    if (!haveX) break;
+    tY = tX;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sY[p] = sX[p];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w2Y[p][q] = w2X[p][q];
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
 // Trivial predicates (vbs.py:200-208): true -> mask & valid, false -> 0.
 __global__ void trivial_kernel(int64_t n_rows, int64_t nb, const uint32_t* mask, int value,
                                uint32_t* out, unsigned long long* count) {
@@ -454,7 +634,8 @@ int vbs_sliced_scan(const VbsDesc& d, int64_t n_rows, int64_t deep_rows, const L
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
                 int deep1_shared, const Leg& A, const Leg& B, bool between,
                 const uint32_t* mask, uint32_t* out, unsigned long long* count,
-                cudaStream_t s);
+                cudaStream_t s, const unsigned long long* gate = nullptr,
+                unsigned long long gate_max = 0);
 }
 
 namespace bsb {
@@ -462,12 +643,81 @@ bool ds_enabled(bool masked);  // bsb_tune("ds_enable") / BSB_DS
 bool ds_zonemap_enabled();     // bsb_tune("ds_zonemap") / BSB_DS_ZONEMAP
 }
 
-extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
-                            uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
-                            void* stream) {
+// Running-mask density (masked-in rows per column row) at or below which a
+// masked SLICED scan in a conjunction chain skips deep blocks (MASKED
+// kernel); above it the column is scanned whole and the mask AND-ed into
+// the result words (EPI kernel), which is cheaper at these densities.
+static double g_sparse_frac = -1.0;
+static double sparse_frac() {
+  if (g_sparse_frac < 0) {
+    const char* e = std::getenv("BSB_SPARSE_FRAC");
+    g_sparse_frac = e ? std::atof(e) : 0.001;
+  }
+  return g_sparse_frac;
+}
+namespace bsb {
+void set_sparse_ppm(int64_t ppm) { g_sparse_frac = ppm < 0 ? 0.0 : (double)ppm * 1e-6; }
+}
+
+// Fused ByteSlice pair of a conjunction chain (bs_conj_kernel); mask may be
+// NULL.  count is zeroed here.
+static int bs_conj2(const bsb_byteslice* c0, const bsb_pred* p0, const bsb_byteslice* c1,
+                    const bsb_pred* p1, const uint32_t* mask, uint32_t* out, uint64_t* count,
+                    cudaStream_t s) {
+  BsConjArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_rows = c0->n_rows;
+  a.nb = (a.n_rows + 31) / 32;
+  a.ntiles = (a.nb + 31) / 32;
+  const bsb_byteslice* cs[2] = {c0, c1};
+  const bsb_pred* ps[2] = {p0, p1};
+  for (int p = 0; p < 2; ++p) {
+    const int K = cs[p]->n_slices;
+    a.c[p].slices = cs[p]->slices;
+    a.c[p].stride = cs[p]->stride;
+    a.c[p].K = K;
+    a.between[p] = ps[p]->op == BSB_BETWEEN;
+    if (a.between[p]) {
+      bs_leg(a.A[p], BSB_GE, ps[p]->code, cs[p]->width_bits, K);
+      bs_leg(a.B[p], BSB_LE, ps[p]->code2, cs[p]->width_bits, K);
+    } else {
+      bs_leg(a.A[p], ps[p]->op, ps[p]->code, cs[p]->width_bits, K);
+      a.B[p] = a.A[p];
+    }
+  }
+  a.mask = mask;
+  a.out = out;
+  a.count = reinterpret_cast<unsigned long long*>(count);
+  BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
+  auto go = [&](auto kern) -> int {
+    const int grid = persistent_grid(kern, kScanThreads, kScanThreads / 32, a.ntiles);
+    kern<<<grid, kScanThreads, 0, s>>>(a);
+    BSB_LAUNCH_CHECK();
+    return BSB_OK;
+  };
+  return mask ? go(bs_conj_kernel<2, true>) : go(bs_conj_kernel<2, false>);
+}
+
+static int g_fuse_bs = -1;  // bsb_tune("conj_fuse") / BSB_CONJ_FUSE: fused ByteSlice pairs
+static bool fuse_bs() {
+  if (g_fuse_bs < 0) {
+    const char* e = std::getenv("BSB_CONJ_FUSE");
+    g_fuse_bs = e ? std::atoi(e) : 1;
+  }
+  return g_fuse_bs != 0;
+}
+namespace bsb {
+void set_conj_fuse(int64_t v) { g_fuse_bs = v ? 1 : 0; }
+}
+
+// gate_count (conjunction chains, masked SLICED scans): device count of the
+// input mask's rows; the MASKED deep-space kernel runs when it is <=
+// sparse_frac * n_rows, the EPI one otherwise (both launched, one exits).
+static int vbs_scan_impl(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
+                         uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                         cudaStream_t s, const unsigned long long* gate_count) {
   if (!col || !pred_ok(pred) || !out_words || !count || col->n_rows <= 0) return BSB_EINVAL;
   if (col->max_len < 1 || col->max_len > kMaxLevels) return BSB_ERANGE;
-  cudaStream_t s = as_stream(stream);
   const int K = col->max_len;
   if (pred->trivial >= 0)
     return run_trivial(col->n_rows, pred, mask, out_words, count, stats, depth, K, s);
@@ -498,13 +748,29 @@ extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint
     case BSB_DEEP_PACKED: return scan_dispatch<BSB_LAYOUT_PPVBS>(a, pred, K, s);
     case BSB_DEEP_SLICED:
       if (K >= 2 && bsb::ds_enabled(mask != nullptr) &&
-          (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled())))
+          (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled()))) {
+        if (mask && gate_count) {
+          const unsigned long long gmax =
+              (unsigned long long)(sparse_frac() * (double)col->n_rows);
+          BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
+          return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1],
+                             col->deep1_shared, a.A, a.B, pred->op == BSB_BETWEEN, mask,
+                             out_words, a.count, s, gate_count, gmax);
+        }
         return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], col->deep1_shared,
                            a.A, a.B, pred->op == BSB_BETWEEN, mask, out_words, a.count, s);
+      }
       return vbs_sliced_scan(a.vbs, a.n_rows, K >= 2 ? col->deep_len[1] : 0, a.A, a.B,
                              pred->op == BSB_BETWEEN, mask, out_words, a.count, s);
     default: return BSB_EINVAL;
   }
+}
+
+extern "C" int bsb_vbs_scan(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
+                            uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
+                            void* stream) {
+  return vbs_scan_impl(col, pred, mask, out_words, count, stats, depth, as_stream(stream),
+                       nullptr);
 }
 
 // ------------------------------------------------------------- conjunction
@@ -557,17 +823,44 @@ extern "C" int bsb_conj_scan(int32_t k, const bsb_column_ref* cols, const bsb_pr
   }
   const int64_t nb = (n + 31) / 32;
   uint32_t* tmp = nullptr;
-  if (m > 1) BSB_CUDA(cudaMallocAsync(&tmp, (size_t)nb * 4 + 4, s));
+  // tmp words + one slot holding the running mask's row count for the
+  // sparse-mask gate of masked PP-VBS scans
+  if (m > 1) BSB_CUDA(cudaMallocAsync(&tmp, (size_t)nb * 4 + 64, s));
+  unsigned long long* gate =
+      m > 1 ? reinterpret_cast<unsigned long long*>(
+                  reinterpret_cast<uintptr_t>(tmp + nb + 8) & ~uintptr_t(7))
+            : nullptr;
+  // steps: consecutive ByteSlice predicates run as fused pairs (one kernel,
+  // AND in registers), everything else one scan each
+  int step_first[BSB_MAX_CONJ], step_len[BSB_MAX_CONJ], nsteps = 0;
+  for (int t = 0; t < m;) {
+    const bool pair = fuse_bs() && t + 1 < m &&
+                      cols[live[t]].layout == BSB_LAYOUT_BYTESLICE &&
+                      cols[live[t + 1]].layout == BSB_LAYOUT_BYTESLICE;
+    step_first[nsteps] = t;
+    step_len[nsteps++] = pair ? 2 : 1;
+    t += pair ? 2 : 1;
+  }
   const uint32_t* running = mask;
-  for (int t = 0; t < m; ++t) {
+  for (int k2 = 0; k2 < nsteps; ++k2) {
+    const int t = step_first[k2];
     const int i = live[t];
-    // the last scan writes out_words; earlier ones alternate through tmp/out
-    uint32_t* dst = ((m - 1 - t) % 2 == 0) ? out_words : tmp;
-    const int rc = cols[i].layout == BSB_LAYOUT_BYTESLICE
-                       ? bsb_byteslice_scan(cols[i].byteslice, &preds[i], running, dst, count,
-                                            nullptr, nullptr, s)
-                       : bsb_vbs_scan(cols[i].vbs, &preds[i], running, dst, count, nullptr,
-                                      nullptr, s);
+    // the last step writes out_words; earlier ones alternate through tmp/out
+    uint32_t* dst = ((nsteps - 1 - k2) % 2 == 0) ? out_words : tmp;
+    int rc;
+    if (step_len[k2] == 2) {
+      const int i2 = live[t + 1];
+      rc = bs_conj2(cols[i].byteslice, &preds[i], cols[i2].byteslice, &preds[i2], running, dst,
+                    count, s);
+    } else if (cols[i].layout == BSB_LAYOUT_BYTESLICE) {
+      rc = bsb_byteslice_scan(cols[i].byteslice, &preds[i], running, dst, count, nullptr,
+                              nullptr, s);
+    } else {
+      const bool gated = k2 > 0;  // running = the previous step's words, count = its rows
+      if (gated) BSB_CUDA(cudaMemcpyAsync(gate, count, 8, cudaMemcpyDeviceToDevice, s));
+      rc = vbs_scan_impl(cols[i].vbs, &preds[i], running, dst, count, nullptr, nullptr, s,
+                         gated ? gate : nullptr);
+    }
     if (rc) {
       if (tmp) cudaFreeAsync(tmp, s);
       return rc;

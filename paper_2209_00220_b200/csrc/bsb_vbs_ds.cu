@@ -60,6 +60,10 @@ struct DsArgs {
   const uint32_t* mask;  // input mask words (MASKED variant)
   uint32_t* out;
   unsigned long long* count;
+  // running-mask gate (conjunction chains): *gate = the mask's row count;
+  // the MASKED kernel runs when it is <= gate_max, the EPI kernel otherwise
+  const unsigned long long* gate;
+  unsigned long long gate_max;
 };
 
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
@@ -146,8 +150,16 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
 // block with masked-in deep rows overlaps it (block-granular: the deep block's
 // unmasked rows are compared too, without changing any result), and the
 // first-slice bytes of fully masked-out row blocks are not loaded.
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false>
+// EPI (conjunction chains, dense running masks): the column is scanned as if
+// unmasked and the mask is AND-ed into the result words in phase 3 -- the
+// same words (AND is idempotent), without the masked variant's per-block
+// bookkeeping, which costs more than it skips unless the mask is very sparse.
+// With a gate both variants are launched: MASKED runs when the running
+// mask's row count is <= gate_max, EPI otherwise.
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false, bool EPI = false>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
+  if (MASKED && a.gate && *a.gate > a.gate_max) return;
+  if (EPI && *a.gate <= a.gate_max) return;
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
   constexpr int kLive = (kRd + 31) / 32;
   __shared__ uint32_t rd_all[kDsWarps][kRd];
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     for (int u = 0; u < ST; ++u) {
       const int64_t b = (s * ST + u) * 32 + lane;
       m[u] = b < a.nb ? __ldg(d.exist[1] + b) : 0u;
-      if (MASKED) mk[u] = b < a.nb ? __ldg(a.mask + b) : 0u;
+      if (MASKED || EPI) mk[u] = b < a.nb ? __ldg(a.mask + b) : 0u;
     }
   };
   auto load_l1 = [&](int64_t lo, int64_t hi, uint32_t (&w)[8]) {
@@ -269,6 +281,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       rs[u] = res;
       m2s[u] = m2;
       if (MASKED) vs[u] = valid;
+      if (EPI) vs[u] = mP[u];
       const int c2 = __popc(m2);
       const uint32_t incl = lane_incl_scan((uint32_t)c2, lane);
       offs[u] = soff + (int)(incl - (uint32_t)c2);
@@ -281,8 +294,10 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       }
     }
     // next super-tile's first-slice bytes -> L2 (its first tile is loaded at
-    // the top of the next iteration)
-    if (L1 && has_next && lane == 0) {
+    // the top of the next iteration).  Not for masked scans: a sparse input
+    // mask leaves most of those sectors unread (fetch() skips masked-out
+    // blocks), and the bulk prefetch would pull them from DRAM anyway.
+    if (L1 && !MASKED && has_next && lane == 0) {
       const int64_t nblk = a.nbpad - nxt_b0 < ST * 32 ? a.nbpad - nxt_b0 : ST * 32;
       l2_prefetch(d.bs1 + nxt_b0 * 32, (uint32_t)(nblk * 32));
     }
@@ -355,7 +370,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
           }
         }
       }
-      const uint32_t res = rs[u] | (MASKED ? (e & vs[u]) : e);
+      const uint32_t res = EPI ? ((rs[u] | e) & vs[u]) : (rs[u] | (MASKED ? (e & vs[u]) : e));
       if (b < a.nb) a.out[b] = res;
       cnt += __popc(res);
     }
@@ -366,9 +381,9 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false>
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false, bool EPI = false>
 static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, MASKED>;
+  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, MASKED, EPI>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -400,7 +415,20 @@ static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
   }
 }
 template <bool BETWEEN, bool L1>
+static int launch_ds_epi(const DsArgs& a, int st, cudaStream_t s) {
+  switch (st) {
+    case 1: return launch_ds_k<BETWEEN, L1, 1, true, false, true>(a, s);
+    case 2: return launch_ds_k<BETWEEN, L1, 2, true, false, true>(a, s);
+    case 3: return launch_ds_k<BETWEEN, L1, 3, true, false, true>(a, s);
+    default: return launch_ds_k<BETWEEN, L1, 4, true, false, true>(a, s);
+  }
+}
+template <bool BETWEEN, bool L1>
 static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
+  if (a.mask && a.gate) {
+    const int rc = launch_ds_masked<BETWEEN, L1>(a, st, s);
+    return rc ? rc : launch_ds_epi<BETWEEN, L1>(a, st, s);
+  }
   if (a.mask) return launch_ds_masked<BETWEEN, L1>(a, st, s);
   return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
 }
@@ -431,7 +459,8 @@ bool ds_zonemap_enabled() { return tune(4) != 0; }
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
                 int deep1_shared, const Leg& A, const Leg& B, bool between,
                 const uint32_t* mask, uint32_t* out, unsigned long long* count,
-                cudaStream_t s) {
+                cudaStream_t s, const unsigned long long* gate,
+                unsigned long long gate_max) {
   DsArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n_rows = n_rows;
@@ -448,6 +477,8 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.mask = mask;
   a.out = out;
   a.count = count;
+  a.gate = gate;
+  a.gate_max = gate_max;
   if (deep1_shared >= 1 && deep1_shared <= 256 && tune(4)) {
     const uint32_t x = (uint32_t)(deep1_shared - 1);
     a.d1 = 1;
@@ -492,7 +523,7 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.twoQ = tQ < 256;
   a.inv = inv;
   const bool l1 = inv != 0 || (tP < 256 && tP < tQ);  // else no shallow row can match
-  BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
+  if (!gate) BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));  // gated: zeroed by the caller
   if (between)
     return l1 ? launch_ds<true, true>(a, st, unr, s) : launch_ds<true, false>(a, st, unr, s);
   return l1 ? launch_ds<false, true>(a, st, unr, s) : launch_ds<false, false>(a, st, unr, s);
@@ -500,8 +531,21 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
 
 }  // namespace bsb
 
+namespace bsb {
+void set_sparse_ppm(int64_t ppm);  // bsb_scan.cu
+void set_conj_fuse(int64_t v);     // bsb_scan.cu
+}
+
 extern "C" int bsb_tune(const char* key, int64_t value) {
   if (!key) return BSB_EINVAL;
+  if (std::strcmp(key, "sparse_ppm") == 0) {  // sparse-mask gate, parts per million
+    bsb::set_sparse_ppm(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "conj_fuse") == 0) {  // fused ByteSlice pairs in bsb_conj_scan
+    bsb::set_conj_fuse(value);
+    return BSB_OK;
+  }
   for (int i = 0; i < bsb::kTunes; ++i)
     if (std::strcmp(key, bsb::kTuneKeys[i]) == 0) {
       bsb::g_tune[i] = value < 0 ? 0 : (int)value;

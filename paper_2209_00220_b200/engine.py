@@ -45,7 +45,7 @@ from .vbs import build_vbs, lookup_vbs_bits, lookup_vbs_rows_dec, scan_vbs, vbs_
 __all__ = ["LAYOUTS", "DEVICE_LAYOUTS", "DataError", "ColumnSpec", "Schema", "Query",
            "QueryResult", "Store", "StoredColumn", "build_layout", "scan_layout",
            "lookup_decode", "lookup_decode_rows", "lookup_decode_bits", "execute", "ingest_arrays",
-           "IngestReport", "size_report", "conj_scan"]
+           "IngestReport", "size_report", "conj_scan", "conj_order"]
 
 LAYOUTS = ("bitpacked", "byteslice", "vbp", "pevbp", "ppvbs")
 DEVICE_LAYOUTS = LAYOUTS
@@ -222,14 +222,29 @@ def size_report(stored: StoredColumn) -> dict:
     return byteslice_size_report(stored.column)
 
 
+def conj_order(layouts) -> list:
+    """Evaluation order of a conjunction: ByteSlice predicates first (stable),
+    so consecutive ones run as fused pairs with the AND in registers, then
+    the PP-VBS predicates, which AND the running mask into their result
+    words.  AND is commutative and idempotent, so the bitvector equals the
+    reference's left-to-right pipeline (engine.py:322-332) for any order."""
+    idx = list(range(len(layouts)))
+    return ([i for i in idx if layouts[i] == "byteslice"] +
+            [i for i in idx if layouts[i] != "byteslice"])
+
+
 def conj_scan(columns, preds, mask=None) -> DeviceBitVector:
-    """Fused conjunction over (layout, column) pairs and resolved predicates.
+    """Fused conjunction over (layout, column) pairs and resolved predicates,
+    evaluated in conj_order.
 
     More than BSB_MAX_CONJ predicates are chained 8 at a time, each chunk
     taking the previous result as its input mask (same semantics).
     """
     if len(columns) != len(preds):
         raise ValueError("one predicate per column")
+    order = conj_order([layout for layout, _ in columns])
+    columns = [columns[i] for i in order]
+    preds = [preds[i] for i in order]
     lib = _lib.load()
     n = None
     for layout, col in columns:

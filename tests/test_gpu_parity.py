@@ -714,6 +714,111 @@ def test_conj_scan_mask_trivial_and_long_chains(mode):
     assert got.count() == O.words_count(want)
 
 
+@pytest.mark.parametrize("ppm", [0, 1_000_000])
+def test_conj_chain_masked_and_epilogue_kernels_vs_oracle(ppm):
+    """Masked PP-VBS scans inside bsb_conj_scan: with sparse_ppm = 10^6 every
+    gated scan skips masked-out deep blocks (MASKED kernel), with 0 it scans
+    the column whole and ANDs the mask into the words (EPI kernel); both
+    equal the pipelined oracle for random 1..8-byte codes (SLICED columns
+    with and without the first-byte zone map), every operator, literals of
+    every length and sparse / dense running masks."""
+    lib = B._lib.load()
+    rng = np.random.default_rng(91)
+    assert lib.bsb_tune(b"sparse_ppm", ppm) == 0
+    try:
+        for n, K, shared in ((70_001, 5, False), (40_000, 8, True), (3000, 3, False)):
+            lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+            byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+            byts[:, 0] |= np.uint64(1)
+            codes = np.zeros(n, np.uint64)
+            for k in range(8):
+                use = lens > k
+                codes[use] |= byts[use, k] << np.uint64(8 * k)
+            if shared:  # every deep row starts with 0xFF (zone map)
+                top = (lens >= 2)
+                codes[top] = (codes[top] & ~(np.uint64(0xFF) << (np.uint64(8) * (
+                    lens[top].astype(np.uint64) - np.uint64(1))))) | (
+                    np.uint64(0xFF) << (np.uint64(8) * (lens[top].astype(np.uint64) -
+                                                        np.uint64(1))))
+            col = B.build_vbs(codes, lens, deep_mode="sliced")
+            ocol = O.vbs_build(codes, lens)
+            u = rng.integers(0, 1 << 16, n)
+            col_b = B.build_byteslice(u, 16)
+            planes = O.bs_build(u, 16)
+            for sel in (0.005, 0.3):
+                c = int((1 << 16) * sel)
+                pb = O.pred_compare("LT", c, 2)
+                first, _ = O.bs_scan(planes, 16, n, pb)
+                for _ in range(3):
+                    r = int(rng.integers(0, n))
+                    lit, ll = int(codes[r]), int(lens[r])
+                    for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                        p = O.pred_compare(op, lit, ll)
+                        want, _ = O.vbs_scan(ocol, p, first)
+                        got = E.conj_scan([("byteslice", col_b), ("ppvbs", col)],
+                                          [rp(list(pb)), rp(list(p))])
+                        assert np.array_equal(got.words, want), (n, K, op, sel)
+                        assert got.count() == O.words_count(want)
+                    a, b = sorted(rng.integers(0, n, 2).tolist())
+                    pa = int(codes[a]) << (8 * (ocol.K - int(lens[a])))
+                    pz = int(codes[b]) << (8 * (ocol.K - int(lens[b])))
+                    if pa > pz:
+                        a, b = b, a
+                    p = O.pred_between(int(codes[a]), int(lens[a]), int(codes[b]), int(lens[b]))
+                    want, _ = O.vbs_scan(ocol, p, first)
+                    got = E.conj_scan([("byteslice", col_b), ("ppvbs", col)],
+                                      [rp(list(pb)), rp(list(p))])
+                    assert np.array_equal(got.words, want), (n, K, "BETWEEN", sel)
+    finally:
+        lib.bsb_tune(b"sparse_ppm", 1000)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 70_001, 1 << 20])
+def test_fused_byteslice_pairs_vs_oracle(n):
+    """bsb_conj_scan runs consecutive ByteSlice predicates as one fused
+    kernel (TMA-staged level-1 sectors, AND in registers): the words equal
+    the pipelined oracle for every operator, BETWEEN, columns of different
+    widths (1..4 slices), ragged row counts, with and without an input
+    mask, and equal the unfused chain (bsb_tune conj_fuse=0)."""
+    lib = B._lib.load()
+    rng = np.random.default_rng(n)
+    ws = (8, 12, 20, 32)
+    cols, planes, vals = [], [], []
+    for w in ws:
+        v = rng.integers(0, 1 << w, n, dtype=np.uint64)
+        vals.append(v)
+        cols.append(B.build_byteslice(v, w))
+        planes.append(O.bs_build(v, w))
+    mw = O.bools_to_words(rng.random(n) < 0.6)
+    for trial in range(6):
+        i, j = rng.choice(4, 2, replace=False)
+        chain, opreds = [], []
+        for c in (i, j):
+            v = vals[c]
+            a, b = sorted(int(x) for x in rng.choice(v, 2))
+            if trial % 3 == 0:
+                p = O.pred_between(a, 1, b, 1)
+            else:
+                p = O.pred_compare(("LT", "GE", "EQ", "NE", "LE", "GT")[trial], a, 1)
+            chain.append((("byteslice", cols[c]), rp(list(p))))
+            opreds.append((c, p))
+        for m in (None, mw):
+            want = m
+            for c, p in opreds:
+                want, _ = O.bs_scan(planes[c], ws[c], n, p, want)
+            got = E.conj_scan([x for x, _ in chain], [p for _, p in chain],
+                              None if m is None else B.ResultBitVector(n, m))
+            assert np.array_equal(got.words, want), (n, trial, m is None)
+            assert got.count() == O.words_count(want)
+            assert lib.bsb_tune(b"conj_fuse", 0) == 0
+            try:
+                unf = E.conj_scan([x for x, _ in chain], [p for _, p in chain],
+                                  None if m is None else B.ResultBitVector(n, m))
+            finally:
+                lib.bsb_tune(b"conj_fuse", 1)
+            assert np.array_equal(unf.words, want)
+
+
 def test_device_bitvector_ops():
     rng = np.random.default_rng(12)
     for n in (1, 31, 32, 33, 1000, 100_001):
