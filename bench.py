@@ -398,11 +398,13 @@ def run_b200(args):
 
 METRIC5 = ("scan Gcodes/s (cfg5: 4 columns x 2^32 rows row-range sharded; u0<q10, u1>=q50, "
            "z0 BETWEEN q80,q95, z1<=q60 and their 4-way AND + global row ids)")
-KERNEL5 = {"u0": "scan_kernel<ByteSlice> (LT, w=32)",
-           "u1": "scan_kernel<ByteSlice> (GE, w=32)",
+KERNEL5 = {"u0": "bs_scan_kernel<LT> (ByteSlice w=32, bit-plane sectors)",
+           "u1": "bs_scan_kernel<GE> (ByteSlice w=32, bit-plane sectors)",
            "z0": "vbs_ds_kernel<BETWEEN> (PP-VBS SLICED, deep-row space)",
-           "z1": "vbs_ds_kernel (PP-VBS SLICED, LE)",
-           "and4": "bsb_conj_scan chain (ByteSlice + masked ByteSlice + 2 masked vbs_ds_kernel)"}
+           "z1": "vbs_ds_kernel<LE> (PP-VBS SLICED, deep-row space)",
+           "and4": "bsb_conj_scan: bs_conj_kernel (u0 AND u1, TMA-staged, AND in registers) "
+                   "+ vbs_ds_kernel<EPI> z0 + vbs_ds_kernel<EPI> z1 (running mask AND-ed in "
+                   "the epilogue)"}
 
 
 def run_cfg5(args, world, rank, local):
@@ -440,6 +442,9 @@ def run_cfg5(args, world, rank, local):
                          f"(AND pipelined) with the numpy oracle on {thr} threads, median "
                          f"after 1 warm-up",
                "threads_1": {"value": round(cs["one"], 6), "unit": "Gcodes/s", "cores": 1}}
+        import bench_cpu
+        cpu["cpu_model"] = bench_cpu.cpu_model()
+        cpu["extras"] = bench_cpu.cpu_extras()
     tab.free_raw()
     # ---- the step as one CUDA graph (C ABI calls + two tiny torch reductions)
     nst = args.cfg5_streams
@@ -516,7 +521,9 @@ def run_cfg5(args, world, rank, local):
                       "alg_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
                       "selected_global": glob[q],
                       "predicate": tab.literals.get(q, "u0 AND u1 AND z0 AND z1")}
-    dom = max(C.QUERIES, key=lambda q: kt[q])
+    # the dominant KERNEL: the single-predicate scans are one kernel each; the
+    # AND is a chain of three (its legs run the same kernels as the singles)
+    dom = max(("u0", "u1", "z0", "z1"), key=lambda q: kt[q])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic_cfg5.json")
     if os.path.exists(tp):
@@ -563,6 +570,8 @@ def run_cfg5(args, world, rank, local):
                                        "per launch)" if traffic else None,
                      "alg_bytes_per_launch": int(ab[dom] / S),
                      "us_per_launch": dq["us_per_segment"],
+                     # the kernel runs once alone and once as an AND leg per segment
+                     "step_share_est": round(2 * kt[dom] / sum(kt.values()), 3),
                      "whole_step_frac": round(step_frac, 4)},
         "queries": queries,
         "parity": {"checked": "every segment's bitvector of every query == packed device "

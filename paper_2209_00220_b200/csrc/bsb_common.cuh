@@ -71,6 +71,15 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
+// Same load without "volatile": the compiler may hoist it above independent
+// work (row gathers issue every level's sector before using any of them).
+__device__ __forceinline__ void ldg256_free(const void* p, uint32_t (&w)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7])
+      : "l"(p));
+}
+
 // ---------------------------------------------------------------------------
 // Bit-plane block layout of a byte plane ("BP32").  Every byte plane of the
 // device layouts (ByteSlice slices, the PP-VBS first slice, the SLICED deep
@@ -170,7 +179,7 @@ __device__ __forceinline__ uint32_t bp_byte(const uint32_t (&w)[8], int r) {
 // Byte of row r of a bit-plane block in global memory (one 32-byte sector).
 __device__ __forceinline__ uint32_t bp_row_byte(const uint8_t* blk, int r) {
   uint32_t w[8];
-  ldg256(blk, w);
+  ldg256_free(blk, w);
   return bp_byte(w, r);
 }
 // ... and of a block staged in shared memory (16-byte aligned).

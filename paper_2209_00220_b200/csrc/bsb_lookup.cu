@@ -49,12 +49,14 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
       lr[u] = (int)(r & 31);
       c[u] = 0;
     }
-    for (int j = 0; j < K; ++j) {
+#pragma unroll
+    for (int j = 0; j < kMaxLevels; ++j) {
+      if (j >= K) break;
       uint32_t w[kIdsPerThread][8];
 #pragma unroll
       for (int u = 0; u < kIdsPerThread; ++u) {
         if (i0 + u * nthr < n_ids) {
-          ldg256(slices + (int64_t)j * stride + blk[u] * 32, w[u]);
+          ldg256_free(slices + (int64_t)j * stride + blk[u] * 32, w[u]);
         } else {
 #pragma unroll
           for (int q = 0; q < 8; ++q) w[u][q] = 0;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
             if (j <= KL) m[j] = (in && deep) ? __ldg(vd.exist[j - 1] + blk) : 0u;
           sdir[lane] = (in && deep && MODE != BSB_DEEP_PACKED) ? __ldg(vd.dir[1] + blk) : 0;
           uint32_t v[8];
-          ldg256(vd.bs1 + blk * 32, v);
+          ldg256_free(vd.bs1 + blk * 32, v);
           sts256(stage + lane * 32, v);
           if (MODE == BSB_DEEP_PACKED) {
 #pragma unroll
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
       } else if (w) {
         for (int j = 0; j < K; ++j) {
           uint32_t v[8];
-          ldg256(slices + j * stride + blk * 32, v);
+          ldg256_free(slices + j * stride + blk * 32, v);
           sts256(stage + j * 1024 + lane * 32, v);
         }
       }
