@@ -109,3 +109,97 @@ def test_shard_range_alignment():
             assert spans[0][0] == 0 and spans[-1][1] == n
             for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
                 assert a1 == b0 and (a0 % 1024 == 0 or a0 == n)
+
+
+# ---------------------------------------------------------------- cfg5 plan
+# The bench's cfg5 table (bench_cfg5.Cfg5Table) on CPU: 8 fixed segments
+# owned in contiguous runs (sharded.owned_segments), exact global quantiles of
+# uint32 codes by the radix select over all ranks (global_nearest_rank_u32),
+# global per-value counts by one all_reduce, per-segment oracle scans, and the
+# AND's global row ids at each rank's exclusive-prefix offset.
+
+SEG = 4096
+NSEG = 8
+
+
+def _seg_values(ci, s):
+    import bench_cfg5 as C
+    if ci < 2:
+        return C.gen_host(ci, "uniform", s, SEG).astype(np.int64)
+    return O.gen_zipf(1.1, 12, SEG, C.chunk_seed(ci, s))
+
+
+def _cfg5_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        segs = list(S.owned_segments(NSEG, world, rank))
+        raw = {ci: [_seg_values(ci, s) for s in segs] for ci in range(4)}
+        n_total = NSEG * SEG
+        qs = [S.global_nearest_rank_u32([torch.from_numpy(v + (1 << 31)) for v in raw[ci]],
+                                        [x], n_total)[0] for ci, x in ((0, 0.10), (1, 0.50))]
+        dicts = []
+        for ci in (2, 3):
+            w = torch.zeros(1 << 12, dtype=torch.int64)
+            for v in raw[ci]:
+                w += torch.bincount(torch.from_numpy(v), minlength=1 << 12)
+            dist.all_reduce(w)
+            u = torch.nonzero(w).flatten()
+            dicts.append(O.OracleDict(u.numpy(), w[u].numpy(), "prefix_preserving"))
+        z0lo = int(np.sort(np.concatenate([_seg_values(2, s) for s in range(NSEG)]))[
+            int(0.8 * n_total)]) if rank == 0 else 0
+        t = torch.tensor([z0lo])
+        dist.broadcast(t, 0)
+        z0lo = int(t.item())
+        local_ids, local_cnt = [], 0
+        for si, s in enumerate(segs):
+            run = None
+            for ci in range(4):
+                v = raw[ci][si]
+                if ci < 2:
+                    planes = O.bs_build((v + (1 << 31)).astype(np.uint64), 32)
+                    p = O.pred_compare("LT" if ci == 0 else "GE", qs[ci], 4)
+                    run, _ = O.bs_scan(planes, 32, SEG, p, run)
+                else:
+                    d = dicts[ci - 2]
+                    col = O.vbs_build(*d.row_codes(d.encode_rows(v)))
+                    p = (d.encode_literal("GE", z0lo) if ci == 2 else
+                         d.encode_literal("LE", 40))
+                    run, _ = O.vbs_scan(col, p, run)
+            rows = O.words_to_rows(run, SEG) + s * SEG
+            local_ids.extend(rows.tolist())
+            local_cnt += len(rows)
+        counts, total, offset = S.exchange_counts(torch.tensor([local_cnt], dtype=torch.int64))
+        q.put((rank, segs, qs, total, offset, counts, local_ids))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_cfg5_segment_plan_matches_one_rank(world):
+    """Sharding the cfg5 table over 2 / 4 ranks (gloo) gives the 1-rank
+    quantiles, dictionaries and AND row ids, each rank's ids at its
+    exclusive-prefix offset of the global id array."""
+    results = {}
+    for w in (1, world):
+        port = _free_port()
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_cfg5_worker, args=(r, w, port, q)) for r in range(w)]
+        for p in procs:
+            p.start()
+        out = sorted(q.get(timeout=300) for _ in procs)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        results[w] = out
+    one = results[1][0]
+    all_ids = one[6]
+    assert len(all_ids) == one[3] > 0
+    segs_seen = []
+    for rank, segs, qs, total, offset, counts, ids in results[world]:
+        assert qs == one[2]                      # global quantiles identical at every world
+        assert total == one[3]
+        assert ids == all_ids[offset:offset + len(ids)]
+        segs_seen += segs
+    assert segs_seen == list(range(NSEG))
