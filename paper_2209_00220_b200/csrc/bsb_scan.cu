@@ -690,6 +690,11 @@ static int bs_conj2(const bsb_byteslice* c0, const bsb_pred* p0, const bsb_bytes
   a.count = reinterpret_cast<unsigned long long*>(count);
   BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
   auto go = [&](auto kern) -> int {
+    static bool carved[2] = {false, false};
+    if (!carved[mask != nullptr]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      carved[mask != nullptr] = true;
+    }
     const int grid = persistent_grid(kern, kScanThreads, kScanThreads / 32, a.ntiles);
     kern<<<grid, kScanThreads, 0, s>>>(a);
     BSB_LAUNCH_CHECK();
