@@ -227,7 +227,31 @@ def measure_cfg4(reps: int = 20, log2n: int = 27, advise_count: int = 100) -> di
                   if s.layout == "ppvbs" else None)
     ab = _alg_bytes([(s.layout, s.column, e) for s, e in zip(stored, ex)], rps)
     peak, _ = hbm_peak()
+    # advisor timing on the device: bytes mode per column, and wall mode twice
+    # on the columns whose AUCs are closest (the decision must not flip)
+    from paper_2209_00220_b200.advisor import advise_column
+    adv = {}
+    for nm in ("z16", "u16"):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a = advise_column(nm, cols[nm], ColumnKind.NUMERIC, count=advise_count, cost="bytes")
+        torch.cuda.synchronize()
+        adv[f"{nm}/bytes"] = {"s": round(time.perf_counter() - t0, 3), "chosen": a.chosen}
+    close = sorted((abs(e["advice"]["auc_byteslice"] - e["advice"]["auc_ppvbs"]) /
+                    max(e["advice"]["auc_byteslice"], e["advice"]["auc_ppvbs"]), e["name"])
+                   for e in store.manifest["columns"] if "advice" in e)[:2]
+    for _, nm in close:
+        picks = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a = advise_column(nm, cols[nm], ColumnKind.NUMERIC, count=advise_count, cost="wall")
+            picks.append(a.chosen)
+        adv[f"{nm}/wall"] = {"s": round(time.perf_counter() - t0, 3), "chosen": picks,
+                             "ingest_choice": advice[nm]["layout"],
+                             "stable": len(set(picks + [advice[nm]["layout"]])) == 1}
     return {
+        "advisor_device": adv,
         "workload": "cfg4: 16 columns x 2^27 (8 uniform, 8 Zipf; seeds 100+i), advisor in GPU "
                     "wall mode, query u16<32768 AND z12 BETWEEN q(.2),q(.9) AND u24>=q(.6) AND "
                     "z16<=q(.7) -> u32, z24, u20 + SUM(u32)",

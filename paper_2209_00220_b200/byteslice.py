@@ -100,19 +100,20 @@ def build_byteslice(codes, width_bits: int, lanes: LaneConfig = DEFAULT_LANES
     return ByteSliceColumn(n, int(width_bits), lanes, stride, planes)
 
 
-def _scan_stats(col: ByteSliceColumn, pred: ResolvedPredicate, mask) -> ScanStats:
+def _scan_stats(col: ByteSliceColumn, pred: ResolvedPredicate, mask,
+                with_depth: bool = True) -> ScanStats:
     lib = _lib.load()
     nb = col.n_blocks
     dev = col.planes.device
     st = torch.zeros(_lib.STATS_WORDS, dtype=torch.int64, device=dev)
-    depth = torch.zeros(max(nb, 1), dtype=torch.int8, device=dev)
+    depth = torch.zeros(max(nb, 1), dtype=torch.int8, device=dev) if with_depth else None
     out = torch.empty(nb, dtype=torch.int32, device=dev)
     cnt = torch.empty(1, dtype=torch.int64, device=dev)
     cp = pred.to_c()
     _lib.check(lib.bsb_byteslice_scan(col.desc_ref, ctypes.byref(cp),
                                       None if mask is None else mask.dwords.data_ptr(),
                                       out.data_ptr(), cnt.data_ptr(), st.data_ptr(),
-                                      depth.data_ptr(), stream()), "scan_byteslice(stats)")
+                                      _lib.ptr(depth), stream()), "scan_byteslice(stats)")
     h = st.cpu().numpy()
     K = col.n_slices
     skipped = int(h[17])
@@ -120,7 +121,8 @@ def _scan_stats(col: ByteSliceColumn, pred: ResolvedPredicate, mask) -> ScanStat
         skipped = min(int(h[17]), int(h[19]))
     return ScanStats(levels=K, blocks_total=nb, blocks_skipped=skipped,
                      words_loaded=h[0:K].copy(), bytes_loaded=h[8:8 + K].copy(),
-                     mask_bytes=0, block_depth=depth[:nb].cpu().numpy())
+                     mask_bytes=0,
+                     block_depth=None if depth is None else depth[:nb].cpu().numpy())
 
 
 def scan_byteslice(col: ByteSliceColumn, pred: ResolvedPredicate, mask=None,
@@ -145,7 +147,7 @@ def scan_byteslice(col: ByteSliceColumn, pred: ResolvedPredicate, mask=None,
                                       out.data_ptr(), cnt.data_ptr(), None, None, stream()),
                "scan_byteslice")
     return DeviceBitVector(col.n_rows, out, cnt), LazyScanStats(
-        lambda: _scan_stats(col, pred, m))
+        lambda with_depth: _scan_stats(col, pred, m, with_depth))
 
 
 def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=None,

@@ -119,7 +119,7 @@ def scan_vbp(col: VbpColumn, pred: ResolvedPredicate, mask=None, threads: int = 
         if m.n_rows != col.n_rows:
             raise ValueError("input mask length mismatch")
     bv, _, _ = _scan(col, pred, m, False)
-    return bv, LazyScanStats(lambda: _stats(col, pred, m))
+    return bv, LazyScanStats(lambda with_depth: _stats(col, pred, m))
 
 
 def lookup_vbp_bits(col: VbpColumn, selection, decoder=None,

@@ -211,18 +211,19 @@ def _mask_bytes(col: VbsColumn, live: int, length: int) -> int:
     return live * 4 * (min(length + 1, col.max_len) - 1)
 
 
-def _scan_stats(col: VbsColumn, pred: ResolvedPredicate, mask) -> ScanStats:
+def _scan_stats(col: VbsColumn, pred: ResolvedPredicate, mask,
+                with_depth: bool = True) -> ScanStats:
     lib = _lib.load()
     nb = col.n_blocks
     dev = col.bs1.device
     st = torch.zeros(_lib.STATS_WORDS, dtype=torch.int64, device=dev)
-    depth = torch.zeros(max(nb, 1), dtype=torch.int8, device=dev)
+    depth = torch.zeros(max(nb, 1), dtype=torch.int8, device=dev) if with_depth else None
     out = torch.empty(nb, dtype=torch.int32, device=dev)
     cnt = torch.empty(1, dtype=torch.int64, device=dev)
     cp = pred.to_c()
     _lib.check(lib.bsb_vbs_scan(col.desc_ref, ctypes.byref(cp),
                                 None if mask is None else mask.dwords.data_ptr(),
-                                out.data_ptr(), cnt.data_ptr(), st.data_ptr(), depth.data_ptr(),
+                                out.data_ptr(), cnt.data_ptr(), st.data_ptr(), _lib.ptr(depth),
                                 stream()), "scan_vbs(stats)")
     h = st.cpu().numpy()
     K = col.max_len
@@ -237,7 +238,8 @@ def _scan_stats(col: VbsColumn, pred: ResolvedPredicate, mask) -> ScanStats:
         mb = _mask_bytes(col, nb - skipped, pred.length)
     return ScanStats(levels=K, blocks_total=nb, blocks_skipped=skipped,
                      words_loaded=h[0:K].copy(), bytes_loaded=h[8:8 + K].copy(),
-                     mask_bytes=mb, block_depth=depth[:nb].cpu().numpy())
+                     mask_bytes=mb,
+                     block_depth=None if depth is None else depth[:nb].cpu().numpy())
 
 
 def scan_vbs(col: VbsColumn, pred: ResolvedPredicate, mask=None, threads: int = 1):
@@ -259,7 +261,7 @@ def scan_vbs(col: VbsColumn, pred: ResolvedPredicate, mask=None, threads: int = 
                                 None if m is None else m.dwords.data_ptr(), out.data_ptr(),
                                 cnt.data_ptr(), None, None, stream()), "scan_vbs")
     return DeviceBitVector(col.n_rows, out, cnt), LazyScanStats(
-        lambda: _scan_stats(col, pred, m))
+        lambda with_depth: _scan_stats(col, pred, m, with_depth))
 
 
 def _vbs_order(col: VbsColumn, order: str) -> str:
