@@ -231,6 +231,63 @@ __device__ __forceinline__ void cmp_word_packed(uint32_t w, LevelLit L, uint32_t
   e4 = nib4(__byte_perm(ev + L.cge, od + L.cge, 0x7351));
 }
 
+// pdep by 8-bit table lookups in shared memory: for every mask byte m the
+// values pdep8(v, m), v < 2^popc(m), sit at pdep_off[m] + v (3^8 = 6561
+// entries; pdep_off[m] = sum over m' < m of 2^popc(m')).  A 32-bit pdep is
+// four byte lookups plus the running shift of x: ~20 integer ops and 8
+// shared loads instead of the ~45 integer ops of the butterfly below -- the
+// deep-space scan is ALU-bound, the shared-memory pipe is idle.
+constexpr int kPdepTab = 6561;
+struct PdepTables {
+  uint16_t off[256];
+  uint8_t val[kPdepTab + 7];
+};
+// Cooperative fill by a whole CTA (then __syncthreads).
+__device__ __forceinline__ void pdep_tables_init(PdepTables& t) {
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) {
+    uint32_t off = 0, p3 = 1;  // sum over set bits i of m: 2^popc(m >> (i+1)) * 3^i
+    for (int i = 0; i < 8; ++i) {
+      if ((m >> i) & 1) off += (1u << __popc((uint32_t)m >> (i + 1))) * p3;
+      p3 *= 3;
+    }
+    t.off[m] = (uint16_t)off;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x >> 3; m < 256; m += blockDim.x >> 3) {
+    const int nv = 1 << __popc((uint32_t)m);
+    for (int v = threadIdx.x & 7; v < nv; v += 8) {
+      uint32_t r = 0, k = 0;
+      for (int i = 0; i < 8; ++i)
+        if ((m >> i) & 1) r |= ((v >> k++) & 1u) << i;
+      t.val[t.off[m] + v] = (uint8_t)r;
+    }
+  }
+}
+__device__ __forceinline__ uint32_t pdep_tab(const PdepTables& t, uint32_t x, uint32_t m) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const uint32_t mb = (m >> (8 * b)) & 0xFFu;
+    const uint32_t c = __popc(mb);
+    r |= (uint32_t)t.val[t.off[mb] + (x & ((1u << c) - 1u))] << (8 * b);
+    x >>= c;
+  }
+  return r;
+}
+// Same lookups from a global copy (read-only path: the 7 KB stay in L1).
+__device__ __forceinline__ uint32_t pdep_tab_g(const PdepTables* t, uint32_t x, uint32_t m) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const uint32_t mb = (m >> (8 * b)) & 0xFFu;
+    const uint32_t c = __popc(mb);
+    const uint32_t o = __ldg(t->off + mb);
+    r |= (uint32_t)__ldg(t->val + o + (x & ((1u << c) - 1u))) << (8 * b);
+    x >>= c;
+  }
+  return r;
+}
+
 // Hacker's Delight "expand" (pdep) as a 5-stage butterfly.  The stage masks
 // depend only on the mask m and are shared by every word expanded with it.
 struct ExpandNet {

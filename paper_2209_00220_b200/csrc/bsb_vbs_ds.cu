@@ -64,7 +64,25 @@ struct DsArgs {
   // the MASKED kernel runs when it is <= gate_max, the EPI kernel otherwise
   const unsigned long long* gate;
   unsigned long long gate_max;
+  const PdepTables* pdep;  // 8-bit pdep tables (g_pdep_tables, filled once)
 };
+
+__device__ PdepTables g_pdep_tables;
+
+__global__ void pdep_tables_kernel() { pdep_tables_init(g_pdep_tables); }
+
+// Fills the global pdep tables once per process (on the caller's stream, so
+// a first call inside graph capture records the fill into the graph).
+static const PdepTables* pdep_tables(cudaStream_t s) {
+  static const PdepTables* ptr = nullptr;
+  if (!ptr) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_pdep_tables) != cudaSuccess) return nullptr;
+    pdep_tables_kernel<<<1, 256, 0, s>>>();
+    ptr = static_cast<const PdepTables*>(p);
+  }
+  return ptr;
+}
 
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -360,7 +378,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       const uint32_t ntm = __ballot_sync(kFull, ntr);
       if (ntm) {
         if (__popc(ntm) > a.serial_blocks) {
-          if (ntr) e = expand_apply(expand_setup(m2), x);
+          if (ntr) e = pdep_tab_g(a.pdep, x, m2);
         } else {
           for (uint32_t r = ntm; r; r &= r - 1) {
             const int L = __ffs(r) - 1;
@@ -479,6 +497,8 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.count = count;
   a.gate = gate;
   a.gate_max = gate_max;
+  a.pdep = pdep_tables(s);
+  if (!a.pdep) return BSB_ECUDA;
   if (deep1_shared >= 1 && deep1_shared <= 256 && tune(4)) {
     const uint32_t x = (uint32_t)(deep1_shared - 1);
     a.d1 = 1;
