@@ -144,7 +144,8 @@ const char* bsb_version(void);
  * (masked PP-VBS scans inside bsb_conj_scan skip masked-out deep blocks when
  * the running mask holds at most this many rows per million, and otherwise
  * scan the column whole and AND the mask into the result words; default
- * 1000).  Unknown key: BSB_EINVAL. */
+ * 0 = always the latter, which measured faster at every density cfg4 / cfg5
+ * produce and saves the second, gated launch).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

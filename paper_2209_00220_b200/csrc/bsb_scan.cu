@@ -651,7 +651,7 @@ static double g_sparse_frac = -1.0;
 static double sparse_frac() {
   if (g_sparse_frac < 0) {
     const char* e = std::getenv("BSB_SPARSE_FRAC");
-    g_sparse_frac = e ? std::atof(e) : 0.001;
+    g_sparse_frac = e ? std::atof(e) : 0.0;
   }
   return g_sparse_frac;
 }

@@ -177,7 +177,7 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
 template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false, bool EPI = false>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
   if (MASKED && a.gate && *a.gate > a.gate_max) return;
-  if (EPI && *a.gate <= a.gate_max) return;
+  if (EPI && a.gate && *a.gate <= a.gate_max) return;
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
   constexpr int kLive = (kRd + 31) / 32;
   __shared__ uint32_t rd_all[kDsWarps][kRd];
@@ -444,6 +444,11 @@ static int launch_ds_epi(const DsArgs& a, int st, cudaStream_t s) {
 template <bool BETWEEN, bool L1>
 static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
   if (a.mask && a.gate) {
+    if (a.gate_max == 0) {  // gate off (sparse_ppm 0): the epilogue variant alone
+      DsArgs e = a;
+      e.gate = nullptr;
+      return launch_ds_epi<BETWEEN, L1>(e, st, s);
+    }
     const int rc = launch_ds_masked<BETWEEN, L1>(a, st, s);
     return rc ? rc : launch_ds_epi<BETWEEN, L1>(a, st, s);
   }

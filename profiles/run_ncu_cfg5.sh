@@ -14,6 +14,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file "$OUT/launches_cfg5_$TAG.csv" $CMD > "$OUT/ncu_launches_cfg5_$TAG.log" 2>&1
 # the timed launches: skip the build / parity kernels, capture each query's scan
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:'scan_kernel|vbs_ds_kernel' -s ${SKIP:-0} -c ${COUNT:-40} -o "$OUT/prof_cfg5_$TAG" \
+    -k regex:'scan_kernel|vbs_ds_kernel|bs_conj_kernel' -s ${SKIP:-0} -c ${COUNT:-40} -o "$OUT/prof_cfg5_$TAG" \
     $CMD > "$OUT/ncu_full_cfg5_$TAG.log" 2>&1
 echo done

@@ -48,7 +48,7 @@ def test_library_exports_every_header_symbol(lib):
 def test_tune_knobs(lib):
     # host-side knobs of the deep-row-space PP-VBS scan; unknown keys rejected
     for key, val in ((b"ds_serial", 6), (b"ds_tiles", 0), (b"ds_unroll", 1), (b"ds_enable", 1),
-                     (b"sparse_ppm", 1000)):
+                     (b"sparse_ppm", 0)):
         assert lib.bsb_tune(key, val) == 0
     assert lib.bsb_tune(b"no_such_knob", 1) != 0
     assert lib.bsb_tune(None, 1) != 0
