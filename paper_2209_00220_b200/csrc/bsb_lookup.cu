@@ -21,6 +21,11 @@ static int grid_for_l(int64_t items, int threads, int cap = 148 * 16) {
 // Each thread takes kIdsPerThread ids per iteration so their random sector
 // loads are in flight together.
 constexpr int kIdsPerThread = 4;
+// PP-VBS row ids: a row gathers up to K sectors of 8 registers each
+constexpr int kVbsIds = 1;
+// ByteSlice row ids: one id per thread at a time with all K sector loads in
+// flight together (8 registers each) keeps more threads resident
+constexpr int kBsIds = 1;
 
 __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t stride, int K,
                                  int width, const int64_t* __restrict__ rows, int64_t n_ids,
@@ -33,12 +38,12 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
   bool oob = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
-       i0 += nthr * kIdsPerThread) {
-    int64_t blk[kIdsPerThread];
-    int lr[kIdsPerThread];
-    uint64_t c[kIdsPerThread];
+       i0 += nthr * kBsIds) {
+    int64_t blk[kBsIds];
+    int lr[kBsIds];
+    uint64_t c[kBsIds];
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
+    for (int u = 0; u < kBsIds; ++u) {
       const int64_t i = i0 + u * nthr;
       int64_t r = i < n_ids ? __ldg(rows + i) : 0;
       if ((uint64_t)r >= (uint64_t)n_rows) {  // IndexError in the reference; never read it
@@ -52,9 +57,9 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
 #pragma unroll
     for (int j = 0; j < kMaxLevels; ++j) {
       if (j >= K) break;
-      uint32_t w[kIdsPerThread][8];
+      uint32_t w[kBsIds][8];
 #pragma unroll
-      for (int u = 0; u < kIdsPerThread; ++u) {
+      for (int u = 0; u < kBsIds; ++u) {
         if (i0 + u * nthr < n_ids) {
           ldg256_free(slices + (int64_t)j * stride + blk[u] * 32, w[u]);
         } else {
@@ -63,10 +68,10 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
         }
       }
 #pragma unroll
-      for (int u = 0; u < kIdsPerThread; ++u) c[u] = (c[u] << 8) | bp_byte(w[u], lr[u]);
+      for (int u = 0; u < kBsIds; ++u) c[u] = (c[u] << 8) | bp_byte(w[u], lr[u]);
     }
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
+    for (int u = 0; u < kBsIds; ++u) {
       const int64_t i = i0 + u * nthr;
       if (i >= n_ids) break;
       const uint64_t cd = c[u] >> shift;
@@ -322,7 +327,7 @@ extern "C" int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t
     const int rc = alloc_err(&err, s);
     if (rc) return rc;
   }
-  bs_lookup_kernel<<<grid_for_l((n_ids + kIdsPerThread - 1) / kIdsPerThread, 256), 256, 0, s>>>(
+  bs_lookup_kernel<<<grid_for_l((n_ids + kBsIds - 1) / kBsIds, 256), 256, 0, s>>>(
       col->slices, col->stride, col->n_slices, col->width_bits, rows, n_ids, out_codes,
       rank_values, out_values, out_values32, col->n_rows, err);
   BSB_LAUNCH_CHECK();
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   const int KD = KL > 1 ? KL - 1 : 0;
   uint8_t* wbase = dsm + (DK == 3 ? 2048 : 0) + (threadIdx.x >> 5) * bits_stage_bytes(VBS, KL);
   using Rec = typename std::conditional<VBS, uint32_t, uint16_t>::type;
-  constexpr int kRowsPerLane = VBS ? 4 : 2;  // rows assembled per lane at a time
+  constexpr int kRowsPerLane = 1;  // rows assembled per lane at a time (bit-plane sectors: 8 registers per level in flight)
   Rec* idx = reinterpret_cast<Rec*>(wbase);
   uint8_t* stage = wbase + 1024 * sizeof(Rec);
   uint32_t* smeta = reinterpret_cast<uint32_t*>(stage + 1024);  // PACKED: m[(j-2)*32 + b]
@@ -717,7 +722,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   if (bad) *err = ~0ull;
 }
 
-// Row-id lookup + general decode; kIdsPerThread ids per thread in flight.
+// Row-id lookup + general decode; kVbsIds ids per thread in flight.
 template <int MODE>
 __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc vd,
                                            const int64_t* __restrict__ rows, int64_t n_ids,
@@ -735,11 +740,11 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
   bool bad = false, oob = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n_ids;
-       i0 += nthr * kIdsPerThread) {
-    uint64_t code[kIdsPerThread];
-    int len[kIdsPerThread];
+       i0 += nthr * kVbsIds) {
+    uint64_t code[kVbsIds];
+    int len[kVbsIds];
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
+    for (int u = 0; u < kVbsIds; ++u) {
       const int64_t i = i0 + u * nthr;
       int64_t r = i < n_ids ? __ldg(rows + i) : 0;
       if ((uint64_t)r >= (uint64_t)vd.n_rows) {  // IndexError in the reference; never read it
@@ -766,7 +771,7 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
       }
     }
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
+    for (int u = 0; u < kVbsIds; ++u) {
       const int64_t i = i0 + u * nthr;
       if (i >= n_ids) break;
       const uint64_t padded = code[u] << (8 * (vd.K - len[u]));
@@ -915,7 +920,7 @@ extern "C" int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, 
     BSB_CUDA(cudaMallocAsync(&err, 4, s));
     BSB_CUDA(cudaMemsetAsync(err, 0, 4, s));
   }
-  const int g = grid_for_l((n_ids + kIdsPerThread - 1) / kIdsPerThread, 256);
+  const int g = grid_for_l((n_ids + kVbsIds - 1) / kVbsIds, 256);
   switch (col->deep_mode) {
 #define BSB_ROWS_DEC(M)                                                                   \
   case M:                                                                                 \
