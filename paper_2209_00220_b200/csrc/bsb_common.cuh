@@ -71,6 +71,17 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
+// 256-bit load of a sparse, dependent sector (a level read only for blocks
+// with tied rows): the L2::64B hint keeps the L2 from fetching a whole 128-B
+// line from DRAM for one 32-B sector.
+__device__ __forceinline__ void ldg256_sparse(const void* p, uint32_t (&w)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7])
+      : "l"(p));
+}
+
 // Same load without "volatile": the compiler may hoist it above independent
 // work (row gathers issue every level's sector before using any of them).
 __device__ __forceinline__ void ldg256_free(const void* p, uint32_t (&w)[8]) {

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
       sX.zgtB = 0;
       sX.zeqB = sX.valid;
       bs_level<BETWEEN>(w1, a.A, a.B, 0, sX);
-      if (K >= 2 && bs_tied<BETWEEN>(sX)) ldg256(sl + stride + (tX * 32 + lane) * 32, w2X);
+      if (K >= 2 && bs_tied<BETWEEN>(sX)) ldg256_sparse(sl + stride + (tX * 32 + lane) * 32, w2X);
     }
     // ---- stage Y: levels 2..K of tile tY, result word
     if (tY >= 0) {
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
           if (!__any_sync(kFull, act)) break;
           if (act) {
             uint32_t w[8];
-            ldg256(sl + (int64_t)j * stride + (tY * 32 + lane) * 32, w);
+            ldg256_sparse(sl + (int64_t)j * stride + (tY * 32 + lane) * 32, w);
             bs_level<BETWEEN>(w, a.A, a.B, j, sY);
           }
         }
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_c
 #pragma unroll
       for (int p = 0; p < NP; ++p)
         if (a.c[p].K >= 2 && conj_tied(a, p, sX[p]))
-          ldg256(a.c[p].slices + a.c[p].stride + b * 32, w2X[p]);
+          ldg256_sparse(a.c[p].slices + a.c[p].stride + b * 32, w2X[p]);
     }
     if (tY >= 0) {
       const int64_t b = tY * 32 + lane;
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_c
         for (int p = 0; p < NP; ++p) {
           if (!act[p]) continue;
           uint32_t w[8];
-          ldg256(a.c[p].slices + (int64_t)j * a.c[p].stride + b * 32, w);
+          ldg256_sparse(a.c[p].slices + (int64_t)j * a.c[p].stride + b * 32, w);
           conj_level<true>(w, a, p, j, sY[p]);
         }
       }

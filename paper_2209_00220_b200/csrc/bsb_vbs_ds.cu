@@ -132,7 +132,10 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
 #pragma unroll
     for (int q = 0; q < 8; ++q) w[q] = pre[q];
   } else if (act) {
-    ldg256(d.deep[j - 1] + dbk * 32, w);
+    if (j >= 3)
+      ldg256_sparse(d.deep[j - 1] + dbk * 32, w);  // only deep blocks still tied
+    else
+      ldg256(d.deep[j - 1] + dbk * 32, w);
   } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q) w[q] = 0;
