@@ -987,8 +987,10 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
     rng3 = np.random.default_rng(3)
     codes = torch.from_numpy(rng3.integers(0, 1 << 24, n, dtype=np.int64)).cuda()
     col_b = build_byteslice(codes, 24)
+    raw_b = codes.to(torch.int32)  # parity check of every lookup against the raw values
     del codes
     vals = gen_zipf_device(ZipfSpec(1.0, 20, n, seed=4))
+    raw_v = vals.to(torch.int32)
     u, c, ranks = freq_table_and_ranks(vals)
     d = Dictionary.build(FrequencyTable(u.cpu().numpy(), c.cpu().numpy(), ColumnKind.NUMERIC),
                          "prefix_preserving")
@@ -1057,8 +1059,16 @@ def measure_lookups(steps: int, log2n: int = 28, only: str | None = None):
             else:
                 fn = lambda: lookup_vbs_rows_dec(col_v, drows, dec_v, out_dtype=torch.int32)
             ms = timed(fn)
+            raw = raw_b if layout == "byteslice" else raw_v
             if not is_bits:
-                gathered[(layout, name)] = fn()
+                gathered[(layout, name)] = got = fn()
+                if not torch.equal(got.to(torch.int32), raw[drows]):
+                    raise RuntimeError(f"{layout}/{name}: looked-up values != raw values")
+            else:
+                fn()
+                got = (o64 if layout == "byteslice" else o32)[:nsel].to(torch.int32)
+                if not torch.equal(got, raw[torch.from_numpy(rows).cuda()]):
+                    raise RuntimeError(f"{layout}/{name}: fused lookup values != raw values")
             if is_bits and int(cnt.item()) != nsel:
                 raise RuntimeError(f"{layout}/{name}: fused lookup count mismatch")
             K = col_b.n_slices if layout == "byteslice" else col_v.max_len

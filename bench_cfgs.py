@@ -209,12 +209,21 @@ def measure_cfg4(reps: int = 20, log2n: int = 27, advise_count: int = 100) -> di
     m = ((h["u16"] < 32768) & (h["z12"] >= preds[1].value) & (h["z12"] <= preds[1].value_high)
          & (h["u24"] >= preds[2].value) & (h["z16"] <= preds[3].value))
     want_count, want_sum = int(m.sum()), int(h["u32"][m].astype(np.int64).sum())
-    del h, m
+    m_host = m
+    del h
     stored = [store.columns[p.column] for p in preds]
     rps = [s.dictionary.encode_literal(p) for s, p in zip(stored, preds)]
     pairs = [(s.layout, s.column) for s in stored]
     sel = conj_scan(pairs, rps)
     assert sel.count() == want_count, "cfg4 conjunction count"
+    # word-for-word against the raw-value filter (tests/helpers.py:35-52)
+    from bench_cfg5 import pack_bools
+    dflags = torch.from_numpy(m_host).cuda()
+    assert torch.equal(sel.dwords, pack_bools(dflags)), "cfg4 conjunction words"
+    for nm in ("u32", "z24", "u20"):
+        got = lookup_decode_bits(store.columns[nm], sel)
+        assert torch.equal(got, cols[nm][dflags]), f"cfg4 projection {nm}"
+    del dflags
     got_sum = int(lookup_decode_bits(store.columns["u32"], sel).sum().item())
     assert got_sum == want_sum, "cfg4 SUM(u32)"
     ms_scan = _time(lambda: conj_scan(pairs, rps), reps)
