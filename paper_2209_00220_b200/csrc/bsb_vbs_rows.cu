@@ -35,9 +35,7 @@ struct RowArgs {
 
 // byte j of deep row q (SLICED: bit-plane 32-deep-row blocks)
 __device__ __forceinline__ uint32_t plane_byte(const VbsDesc& d, int64_t q, int j) {
-  uint32_t w[8];
-  ldg256_free(d.deep[j - 1] + (q >> 5) * 32, w);
-  return bp_byte(w, (int)(q & 31));
+  return bp_row_byte(d.deep[j - 1] + (q >> 5) * 32, (int)(q & 31));
 }
 
 __global__ void __launch_bounds__(256) vbs_rowscan_kernel(const __grid_constant__ RowArgs a) {
@@ -50,35 +48,25 @@ __global__ void __launch_bounds__(256) vbs_rowscan_kernel(const __grid_constant_
   unsigned long long cnt = 0;
   long long words[kMaxLevels] = {0}, bytes[kMaxLevels] = {0}, skipped = 0;
   for (int64_t b = warp; b < a.nb; b += nwarps) {
-    // every load of the block is independent of the others: issue them together
     uint32_t valid = tail_valid(b, a.n_rows);
     if (a.mask) valid &= __ldg(a.mask + b);
-    uint32_t m[kMaxLevels];
-#pragma unroll
-    for (int j = 2; j <= kMaxLevels; ++j) m[j - 1] = (j <= K) ? __ldg(d.exist[j - 1] + b) : 0u;
-    const int64_t dir2 = K >= 2 ? __ldg(d.dir[1] + b) : 0;
-    uint32_t w1[8];
-    ldg256_free(d.bs1 + b * 32, w1);
     const bool v = (valid >> lane) & 1u;
     int t = 0;
     bool gt = false, eq = false;
+    uint32_t m[kMaxLevels];
     int len = 1;
 #pragma unroll
-    for (int j = 2; j <= kMaxLevels; ++j) len += (j <= K) && ((m[j - 1] >> lane) & 1u);
+    for (int j = 2; j <= kMaxLevels; ++j) {
+      m[j - 1] = (j <= K) ? __ldg(d.exist[j - 1] + b) : 0u;
+      len += (j <= K) && ((m[j - 1] >> lane) & 1u);
+    }
     if (v) {
       const uint32_t below = (1u << lane) - 1u;
-      const int64_t q = dir2 + __popc(m[1] & below);
-      // the row's bytes 2..min(len, l) in one round trip (byte j is needed
-      // only while the row stays tied, but fetching them together beats a
-      // dependent load per level)
-      const int need = len < l ? len : l;
-      uint32_t cb[kMaxLevels];
-      cb[0] = bp_byte(w1, lane);
-#pragma unroll
-      for (int j = 2; j <= kMaxLevels; ++j) cb[j - 1] = j <= need ? plane_byte(d, q, j) : 0u;
+      const int64_t q = K >= 2 ? __ldg(d.dir[1] + b) + __popc(m[1] & below) : 0;
       t = 1;
       for (int j = 1;; ++j) {
-        const uint32_t cj = cb[j - 1];
+        const uint32_t cj = j == 1 ? bp_row_byte(d.bs1 + b * 32, lane)
+                                   : plane_byte(d, q, j);
         const uint32_t lj = a.L.byte[j - 1];
         if (cj != lj) {
           gt = cj > lj;
