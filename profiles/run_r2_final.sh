@@ -19,5 +19,5 @@ timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
     python bench.py --profile --no-graph --steps 1 --warmup 1 --no-extra --no-cpu-baseline \
     > "$OUT/ncu_launches_bench_$TAG.log" 2>&1
 echo "launch list rc=$?"
-TAG=$TAG COUNT=10 timeout 1200 bash profiles/run_ncu_cfg5.sh > "$OUT/ncu_cfg5_$TAG.log" 2>&1
+TAG=$TAG COUNT=27 timeout 1200 bash profiles/run_ncu_cfg5.sh > "$OUT/ncu_cfg5_$TAG.log" 2>&1
 echo "cfg5 full rc=$?"

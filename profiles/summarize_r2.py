@@ -46,16 +46,16 @@ for r in rows[2:]:
                  f"{rec['launch__registers_per_thread']:.0f}")
 open(out_txt, "w").write("\n".join(lines) + "\n")
 # probe order (tools/cfg5_probe.py --reps=1: 2 warm-ups + 1 timed launch per
-# query): u0 x3, u1 x3, z0 x3, z1 x3, then 3 AND chains of 5 launches each
-# (bs_conj_kernel, then per PP-VBS leg the gated MASKED / EPI pair of which
-# one exits at once); the last launch of each group is used
+# query): u0 x3, u1 x3, z0 x3, z1 x3, then 3 AND chains (bs_conj_kernel + the
+# two epilogue-masked vbs_ds_kernel legs); the last launch of each group
 traffic = {}
 for nm, k in (("u0", 2), ("u1", 5), ("z0", 8), ("z1", 11)):
     if k < len(recs):
         traffic[nm] = int((recs[k]["dram__bytes_read.sum"] + recs[k]["dram__bytes_write.sum"]) * 1e6)
-if len(recs) >= 27:
+conj = [i for i, r in enumerate(recs) if "bs_conj_kernel" in r["kernel"]]
+if conj and conj[-1] + 3 <= len(recs):
     traffic["and4"] = int(sum(r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"]
-                              for r in recs[22:27]) * 1e6)
+                              for r in recs[conj[-1]:conj[-1] + 3]) * 1e6)
 json.dump({"source": rep, "unit": "bytes per launch (dram read + write, ncu, one 2^29-row "
                                   "segment per column)", **traffic}, open(out_json, "w"), indent=1)
 print(open(out_txt).read())
