@@ -380,9 +380,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N > 1 path on a one-GPU box (never a perf
+    # number): BSB_FORCE_DEVICE=0 BSB_DIST_BACKEND=gloo puts every rank on
+    # cuda:0 with host-staged collectives
+    local = int(os.environ.get("BSB_FORCE_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BSB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.workload == "cfg5":
             out = run_cfg5(args, world, rank, local)
@@ -461,6 +469,8 @@ def run_cfg5(args, world, rank, local):
         torch.cuda.current_stream().wait_stream(capst)
 
     gath = torch.zeros(world, len(C.QUERIES), dtype=torch.int64, device="cuda")
+    gath_list = list(gath.unbind(0))  # (gloo functional check only)
+    nccl = world > 1 and dist.get_backend() == "nccl"
 
     def one_step():
         if graph is not None:
@@ -471,8 +481,10 @@ def run_cfg5(args, world, rank, local):
                 st.wait_stream(cur)
             step.local(streams)
             cur.wait_stream(streams[0])
-        if world > 1:
+        if world > 1 and nccl:
             dist.all_gather_into_tensor(gath, step.totals)
+        elif world > 1:
+            dist.all_gather(gath_list, step.totals)
         else:
             gath[0].copy_(step.totals)
 

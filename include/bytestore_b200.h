@@ -145,7 +145,10 @@ const char* bsb_version(void);
  * the running mask holds at most this many rows per million, and otherwise
  * scan the column whole and AND the mask into the result words; default
  * 0 = always the latter, which measured faster at every density cfg4 / cfg5
- * produce and saves the second, gated launch).  Unknown key: BSB_EINVAL. */
+ * produce and saves the second, gated launch), "ctas_per_sm" (cap on the
+ * CTAs per SM of the persistent scan kernels, 0 = none: room for a kernel
+ * of another stream; measured slower, kept for experiments).  Unknown key:
+ * BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

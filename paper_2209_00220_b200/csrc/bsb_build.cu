@@ -3,6 +3,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -32,6 +33,16 @@ void ensure_init() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
 }
+
+static int g_ctas_cap = -1;
+int ctas_per_sm_cap() {
+  if (g_ctas_cap < 0) {
+    const char* e = std::getenv("BSB_CTAS_PER_SM");
+    g_ctas_cap = e ? std::atoi(e) : 0;
+  }
+  return g_ctas_cap;
+}
+void set_ctas_per_sm_cap(int v) { g_ctas_cap = v < 0 ? 0 : v; }
 
 int sm_count() {
   static int cached = -1;

@@ -47,15 +47,19 @@ inline cudaStream_t as_stream(void* s) {
   return reinterpret_cast<cudaStream_t>(s);
 }
 
-// Grid sizing: persistent grid-stride kernels use (SMs x resident CTAs).
+// Grid sizing: persistent grid-stride kernels use (SMs x resident CTAs),
+// optionally capped at ctas_per_sm_cap() CTAs per SM (bsb_tune
+// "ctas_per_sm": leaves room on every SM for a kernel of another stream --
+// e.g. an ALU-bound PP-VBS scan next to a DRAM-bound ByteSlice scan).
 int sm_count();
+int ctas_per_sm_cap();  // 0 = no cap
 template <typename K>
 int persistent_grid(K kernel, int threads, int64_t work_items_per_cta_iter, int64_t total_items) {
-  static thread_local int cached_blocks = -1;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
   if (per_sm < 1) per_sm = 1;
-  (void)cached_blocks;
+  const int capc = ctas_per_sm_cap();
+  if (capc > 0 && per_sm > capc) per_sm = capc;
   int64_t want = (total_items + work_items_per_cta_iter - 1) / work_items_per_cta_iter;
   int64_t cap = (int64_t)sm_count() * per_sm;
   if (want < 1) want = 1;

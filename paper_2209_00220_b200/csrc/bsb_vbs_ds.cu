@@ -408,6 +408,7 @@ static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
   const int64_t nsuper = (a.ntiles + ST - 1) / ST;
   const int64_t want = (nsuper + kDsWarps - 1) / kDsWarps;
   const int64_t cap = (int64_t)sm_count() * per_sm;
@@ -562,12 +563,17 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
 namespace bsb {
 void set_sparse_ppm(int64_t ppm);  // bsb_scan.cu
 void set_conj_fuse(int64_t v);     // bsb_scan.cu
+void set_ctas_per_sm_cap(int v);   // bsb_build.cu
 }
 
 extern "C" int bsb_tune(const char* key, int64_t value) {
   if (!key) return BSB_EINVAL;
   if (std::strcmp(key, "sparse_ppm") == 0) {  // sparse-mask gate, parts per million
     bsb::set_sparse_ppm(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "ctas_per_sm") == 0) {  // persistent-grid cap (0 = none)
+    bsb::set_ctas_per_sm_cap((int)value);
     return BSB_OK;
   }
   if (std::strcmp(key, "conj_fuse") == 0) {  // fused ByteSlice pairs in bsb_conj_scan
