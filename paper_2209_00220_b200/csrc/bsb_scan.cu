@@ -636,6 +636,12 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
                 const uint32_t* mask, uint32_t* out, unsigned long long* count,
                 cudaStream_t s, const unsigned long long* gate = nullptr,
                 unsigned long long gate_max = 0);
+void shallow_thresholds(const Leg& A, const Leg& B, bool between, int& tP, int& tQ,
+                        uint32_t& inv);
+int vbs_ds_stats_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int deep1_shared,
+                      const Leg& A, const Leg& B, bool between, int tP, int tQ, uint32_t inv,
+                      const uint32_t* mask, uint32_t* out, unsigned long long* count,
+                      int64_t* stats, int8_t* depth, cudaStream_t s);
 }
 
 namespace bsb {
@@ -703,6 +709,12 @@ static int bs_conj2(const bsb_byteslice* c0, const bsb_pred* p0, const bsb_bytes
   return mask ? go(bs_conj_kernel<2, true>) : go(bs_conj_kernel<2, false>);
 }
 
+static int g_stats_rows = 0;  // bsb_tune("stats_rows"): PP-VBS stats via the row kernel
+static bool stats_rows() { return g_stats_rows != 0; }
+namespace bsb {
+void set_stats_rows(int64_t v) { g_stats_rows = v ? 1 : 0; }
+}
+
 static int g_fuse_bs = -1;  // bsb_tune("conj_fuse") / BSB_CONJ_FUSE: fused ByteSlice pairs
 static bool fuse_bs() {
   if (g_fuse_bs < 0) {
@@ -747,8 +759,22 @@ static int vbs_scan_impl(const bsb_vbs* col, const bsb_pred* pred, const uint32_
   a.count = reinterpret_cast<unsigned long long*>(count);
   a.stats = stats;
   a.depth = depth;
-  if (col->deep_mode == BSB_DEEP_SLICED && stats != nullptr)
+  if (col->deep_mode == BSB_DEEP_SLICED && stats != nullptr) {
+    // ScanStats: the deep-space kernel with survival counters when the column
+    // has what it needs, else the row-parallel kernel (bsb_tune stats_rows=1
+    // forces the latter)
+    if (K >= 2 && !stats_rows() &&
+        (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled()))) {
+      int tP, tQ;
+      uint32_t inv;
+      const bool between = pred->op == BSB_BETWEEN;
+      shallow_thresholds(a.A, a.B, between, tP, tQ, inv);
+      return vbs_ds_stats_scan(a.vbs, a.n_rows, col->stride,
+                               col->deep[0] ? 0 : col->deep1_shared, a.A, a.B, between, tP, tQ,
+                               inv, mask, out_words, a.count, stats, depth, s);
+    }
     return vbs_rows_scan(a.vbs, a.n_rows, pred, mask, out_words, count, stats, depth, s);
+  }
   switch (col->deep_mode) {
     case BSB_DEEP_PACKED: return scan_dispatch<BSB_LAYOUT_PPVBS>(a, pred, K, s);
     case BSB_DEEP_SLICED:

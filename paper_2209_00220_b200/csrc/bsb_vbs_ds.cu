@@ -73,7 +73,7 @@ __global__ void pdep_tables_kernel() { pdep_tables_init(g_pdep_tables); }
 
 // Fills the global pdep tables once per process (on the caller's stream, so
 // a first call inside graph capture records the fill into the graph).
-static const PdepTables* pdep_tables(cudaStream_t s) {
+const PdepTables* pdep_tables(cudaStream_t s) {
   static const PdepTables* ptr = nullptr;
   if (!ptr) {
     void* p = nullptr;
@@ -482,6 +482,37 @@ bool ds_enabled(bool masked) { return masked ? tune(0) == 1 : tune(0) != 0; }
 bool ds_zonemap_enabled() { return tune(4) != 0; }
 
 
+// Shallow rows (vbs.py:272-284 with M_2 = 0): gt = byte > lit, eq_final =
+// byte == lit only for a 1-byte literal, so the result of a 1-byte-code row
+// is ([byte >= tP] & ~[byte >= tQ]) ^ inv with thresholds per operator (tQ =
+// 256: no Q compare).  For BETWEEN, [byte >= tP] is exactly GE(lo).
+void shallow_thresholds(const Leg& A, const Leg& B, bool between, int& tP, int& tQ,
+                        uint32_t& inv) {
+  const int la = (int)A.byte[0], lb = (int)B.byte[0];
+  const int ge_a = la + (A.len >= 2 ? 1 : 0);  // [byte >= ge_a] == gt | eq_final
+  tP = 256;
+  tQ = 256;
+  inv = 0;
+  if (between) {
+    tP = ge_a;
+    tQ = lb + 1;
+  } else {
+    switch (A.op) {
+      case BSB_GT: tP = la + 1; break;
+      case BSB_GE: tP = ge_a; break;
+      case BSB_LT: tP = ge_a; inv = kFull; break;
+      case BSB_LE: tP = la + 1; inv = kFull; break;
+      case BSB_EQ:
+        if (A.len == 1) { tP = la; tQ = la + 1; }
+        break;
+      default:  // NE
+        if (A.len == 1) { tP = la; tQ = la + 1; }
+        inv = kFull;
+        break;
+    }
+  }
+}
+
 // Scan of a SLICED column that carries deep[0] (K >= 2), optionally masked.
 int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_rows,
                 int deep1_shared, const Leg& A, const Leg& B, bool between,
@@ -523,30 +554,9 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
     st = per_tile > 0 ? (int)(28.0 / per_tile + 0.5) : 4;
     st = st < 1 ? 1 : (st > 4 ? 4 : st);
   }
-  // shallow rows (vbs.py:272-284 with M_2 = 0): gt = byte > lit, eq_final =
-  // byte == lit only for a 1-byte literal
-  const int la = (int)A.byte[0], lb = (int)B.byte[0];
-  const int ge_a = la + (A.len >= 2 ? 1 : 0);  // [byte >= ge_a] == gt | eq_final
-  int tP = 256, tQ = 256;
-  uint32_t inv = 0;
-  if (between) {
-    tP = ge_a;
-    tQ = lb + 1;
-  } else {
-    switch (A.op) {
-      case BSB_GT: tP = la + 1; break;
-      case BSB_GE: tP = ge_a; break;
-      case BSB_LT: tP = ge_a; inv = kFull; break;
-      case BSB_LE: tP = la + 1; inv = kFull; break;
-      case BSB_EQ:
-        if (A.len == 1) { tP = la; tQ = la + 1; }
-        break;
-      default:  // NE
-        if (A.len == 1) { tP = la; tQ = la + 1; }
-        inv = kFull;
-        break;
-    }
-  }
+  int tP, tQ;
+  uint32_t inv;
+  shallow_thresholds(A, B, between, tP, tQ, inv);
   a.tP = make_plane_thr(tP);
   a.tQ = make_plane_thr(tQ);
   a.twoQ = tQ < 256;
@@ -564,12 +574,17 @@ namespace bsb {
 void set_sparse_ppm(int64_t ppm);  // bsb_scan.cu
 void set_conj_fuse(int64_t v);     // bsb_scan.cu
 void set_ctas_per_sm_cap(int v);   // bsb_build.cu
+void set_stats_rows(int64_t v);    // bsb_scan.cu
 }
 
 extern "C" int bsb_tune(const char* key, int64_t value) {
   if (!key) return BSB_EINVAL;
   if (std::strcmp(key, "sparse_ppm") == 0) {  // sparse-mask gate, parts per million
     bsb::set_sparse_ppm(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "stats_rows") == 0) {  // PP-VBS ScanStats via the row kernel
+    bsb::set_stats_rows(value);
     return BSB_OK;
   }
   if (std::strcmp(key, "ctas_per_sm") == 0) {  // persistent-grid cap (0 = none)

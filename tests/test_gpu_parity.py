@@ -819,6 +819,71 @@ def test_fused_byteslice_pairs_vs_oracle(n):
             assert np.array_equal(unf.words, want)
 
 
+def _same_stats(st, o):
+    assert st.levels == o.levels
+    assert st.blocks_total == o.blocks_total
+    assert st.blocks_skipped == o.blocks_skipped
+    assert list(st.words_loaded) == list(o.words_loaded)
+    assert list(st.bytes_loaded) == list(o.bytes_loaded)
+    assert st.mask_bytes == o.mask_bytes
+    assert st.block_depth.tolist() == o.block_depth.tolist()
+
+
+@pytest.mark.parametrize("rows_kernel", [0, 1])
+def test_sliced_scan_stats_deep_space_vs_oracle(rows_kernel):
+    """ScanStats of SLICED PP-VBS scans (the deep-space stats kernel, and the
+    row-parallel one with bsb_tune stats_rows=1) == the oracle's for every
+    operator, BETWEEN (two pipelined legs: leg 2 counts rows passing GE(lo)),
+    input masks, zone-mapped and deep[0] columns, literals of every length;
+    the result words equal the plain scan's."""
+    lib = B._lib.load()
+    rng = np.random.default_rng(33)
+    assert lib.bsb_tune(b"stats_rows", rows_kernel) == 0
+    try:
+        cases = []
+        vals, od, codes, lens = _ppe_column(1.2, 16, 50_003, 7)     # zone map
+        cases.append((codes, lens))
+        for n, K in ((40_001, 5), (3000, 8), (70, 3)):              # deep[0]
+            lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+            byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+            byts[:, 0] |= np.uint64(1)
+            codes = np.zeros(n, np.uint64)
+            for k in range(8):
+                use = lens > k
+                codes[use] |= byts[use, k] << np.uint64(8 * k)
+            cases.append((codes, lens))
+        for codes, lens in cases:
+            n = len(codes)
+            col = B.build_vbs(codes, lens, deep_mode="sliced")
+            ocol = O.vbs_build(codes, lens)
+            mw = O.bools_to_words(rng.random(n) < 0.4)
+            for _ in range(3):
+                r = int(rng.integers(0, n))
+                lit, ll = int(codes[r]), int(lens[r])
+                for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+                    p = O.pred_compare(op, lit, ll)
+                    for m_o in (None, mw):
+                        want, ost = O.vbs_scan(ocol, p, m_o)
+                        bv, st = B.scan_vbs(col, rp(list(p)),
+                                            None if m_o is None else B.ResultBitVector(n, m_o))
+                        _same_stats(st.materialize(), ost)
+                        assert np.array_equal(bv.words, want), op
+                a, b = sorted(rng.integers(0, n, 2).tolist())
+                pa = int(codes[a]) << (8 * (ocol.K - int(lens[a])))
+                pz = int(codes[b]) << (8 * (ocol.K - int(lens[b])))
+                if pa > pz:
+                    a, b = b, a
+                p = O.pred_between(int(codes[a]), int(lens[a]), int(codes[b]), int(lens[b]))
+                for m_o in (None, mw):
+                    want, ost = O.vbs_scan(ocol, p, m_o)
+                    bv, st = B.scan_vbs(col, rp(list(p)),
+                                        None if m_o is None else B.ResultBitVector(n, m_o))
+                    _same_stats(st.materialize(), ost)
+                    assert np.array_equal(bv.words, want)
+    finally:
+        lib.bsb_tune(b"stats_rows", 0)
+
+
 def test_device_bitvector_ops():
     rng = np.random.default_rng(12)
     for n in (1, 31, 32, 33, 1000, 100_001):

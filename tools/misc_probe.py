@@ -58,8 +58,23 @@ def main():
             for _ in range(3):
                 fn(col, rp)[1].materialize()
             t_stats = (time.perf_counter() - t0) / 3 * 1e6
+            # the stats call alone on the device (C ABI, events; no host copies)
+            import ctypes
+            from paper_2209_00220_b200 import _lib
+            lib = _lib.load()
+            nb = col.n_blocks
+            stw = torch.zeros(_lib.STATS_WORDS, dtype=torch.int64, device="cuda")
+            dep = torch.zeros(nb, dtype=torch.int8, device="cuda")
+            out = torch.empty(nb, dtype=torch.int32, device="cuda")
+            cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+            cp = rp.to_c()
+            f = lib.bsb_vbs_scan if name == "ppvbs" else lib.bsb_byteslice_scan
+            t_dev = ev_time(lambda: f(col.desc_ref, ctypes.byref(cp), None, out.data_ptr(),
+                                      cnt.data_ptr(), stw.data_ptr(), dep.data_ptr(),
+                                      _lib.stream_ptr()), 5)
             print(f"cfg2 p={p} {name}: scan {t_scan:.1f} us, stats (wall) {t_stats:.1f} us "
-                  f"= {t_stats / t_scan:.1f}x")
+                  f"= {t_stats / t_scan:.1f}x; stats call on the device {t_dev:.1f} us "
+                  f"= {t_dev / t_scan:.1f}x")
 
 
 if __name__ == "__main__":
