@@ -136,19 +136,22 @@ typedef struct bsb_column_ref {
 
 /* ----------------------------------------------------------------- misc */
 const char* bsb_version(void);
-/* Run-time tuning knobs of the PP-VBS deep-row-space scan (benchmarks and
- * experiments; never changes results): "ds_enable" (0 off, 1 on, 2 unmasked
- * scans only), "ds_serial" (warp-cooperative pdep up to this many blocks per
- * tile), "ds_tiles" (tiles per super-tile, 0 = auto), "ds_unroll" (0/1),
- * "ds_zonemap" (0/1: settle level 1 from deep1_shared), "sparse_ppm"
- * (masked PP-VBS scans inside bsb_conj_scan skip masked-out deep blocks when
- * the running mask holds at most this many rows per million, and otherwise
- * scan the column whole and AND the mask into the result words; default
- * 0 = always the latter, which measured faster at every density cfg4 / cfg5
- * produce and saves the second, gated launch), "ctas_per_sm" (cap on the
- * CTAs per SM of the persistent scan kernels, 0 = none: room for a kernel
- * of another stream; measured slower, kept for experiments).  Unknown key:
- * BSB_EINVAL. */
+/* Run-time tuning knobs (benchmarks and experiments; never change results;
+ * a negative value restores the default): "ds_enable" (0 off, 1 on, 2
+ * unmasked scans only), "ds_serial" (warp-cooperative pdep up to this many
+ * blocks per tile), "ds_tiles" (tiles per super-tile, 0 = auto),
+ * "ds_unroll" (0/1), "ds_zonemap" (0/1: settle level 1 from deep1_shared),
+ * "sparse_ppm" (masked SLICED PP-VBS scans run the compacted kernel -- work
+ * over the masked-in blocks only -- when the mask holds at most this many
+ * rows per million, else scan the column whole and AND the mask into the
+ * result words; the mask's row count is the chain's running count inside
+ * bsb_conj_scan, a sampled estimate otherwise; default 60000, 0 = always the
+ * latter), "ds_masked" (1: masked scans always scan whole), "dsm_cfg"
+ * (compacted kernel shape 0..3), "conj_fuse" (0/1: fused ByteSlice pairs in
+ * bsb_conj_scan), "stats_rows" (1: PP-VBS ScanStats through the
+ * row-parallel kernel instead of the deep-row-space one), "ctas_per_sm"
+ * (cap on the CTAs per SM of the persistent scan kernels, 0 = none: room for
+ * a kernel of another stream; measured slower).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

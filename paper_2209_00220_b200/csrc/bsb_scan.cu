@@ -649,20 +649,41 @@ bool ds_enabled(bool masked);  // bsb_tune("ds_enable") / BSB_DS
 bool ds_zonemap_enabled();     // bsb_tune("ds_zonemap") / BSB_DS_ZONEMAP
 }
 
-// Running-mask density (masked-in rows per column row) at or below which a
-// masked SLICED scan in a conjunction chain skips deep blocks (MASKED
-// kernel); above it the column is scanned whole and the mask AND-ed into
-// the result words (EPI kernel), which is cheaper at these densities.
+// Mask density (masked-in rows per column row) at or below which a masked
+// SLICED scan runs the compacted kernel (work over the masked-in blocks
+// only); above it the column is scanned whole and the mask AND-ed into the
+// result words (EPI), which is cheaper for dense masks (cfg5 segment, z1:
+// 0.75 % 119 vs 215 us, 5 % 211 vs 215, 20 % 252 vs 215).
 static double g_sparse_frac = -1.0;
 static double sparse_frac() {
   if (g_sparse_frac < 0) {
     const char* e = std::getenv("BSB_SPARSE_FRAC");
-    g_sparse_frac = e ? std::atof(e) : 0.0;
+    g_sparse_frac = e ? std::atof(e) : 0.06;
   }
   return g_sparse_frac;
 }
+
+// Row count of a mask estimated from 8192 evenly spaced words (the gate of a
+// masked scan called outside a conjunction chain: a heuristic only -- both
+// gated kernels return the same words).
+__global__ void mask_sample_kernel(const uint32_t* __restrict__ mask, int64_t nb,
+                                   unsigned long long* est) {
+  constexpr int64_t kSample = 8192;
+  const int64_t step = nb > kSample ? nb / kSample : 1;
+  const int64_t n = nb > kSample ? kSample : nb;
+  unsigned long long c = 0;
+#pragma unroll 8
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += __popc(__ldg(mask + i * step));
+  for (int dd = 16; dd > 0; dd >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, dd);
+  __shared__ unsigned long long tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
+  __syncthreads();
+  if (threadIdx.x == 0) *est = tot * (unsigned long long)step;
+}
 namespace bsb {
-void set_sparse_ppm(int64_t ppm) { g_sparse_frac = ppm < 0 ? 0.0 : (double)ppm * 1e-6; }
+void set_sparse_ppm(int64_t ppm) { g_sparse_frac = ppm < 0 ? -1.0 : (double)ppm * 1e-6; }  // < 0: default
 }
 
 // Fused ByteSlice pair of a conjunction chain (bs_conj_kernel); mask may be
@@ -712,7 +733,7 @@ static int bs_conj2(const bsb_byteslice* c0, const bsb_pred* p0, const bsb_bytes
 static int g_stats_rows = 0;  // bsb_tune("stats_rows"): PP-VBS stats via the row kernel
 static bool stats_rows() { return g_stats_rows != 0; }
 namespace bsb {
-void set_stats_rows(int64_t v) { g_stats_rows = v ? 1 : 0; }
+void set_stats_rows(int64_t v) { g_stats_rows = v > 0 ? 1 : 0; }  // < 0: default (off)
 }
 
 static int g_fuse_bs = -1;  // bsb_tune("conj_fuse") / BSB_CONJ_FUSE: fused ByteSlice pairs
@@ -724,11 +745,11 @@ static bool fuse_bs() {
   return g_fuse_bs != 0;
 }
 namespace bsb {
-void set_conj_fuse(int64_t v) { g_fuse_bs = v ? 1 : 0; }
+void set_conj_fuse(int64_t v) { g_fuse_bs = v < 0 ? -1 : (v ? 1 : 0); }  // < 0: default
 }
 
 // gate_count (conjunction chains, masked SLICED scans): device count of the
-// input mask's rows; the MASKED deep-space kernel runs when it is <=
+// input mask's rows; the compacted deep-space kernel runs when it is <=
 // sparse_frac * n_rows, the EPI one otherwise (both launched, one exits).
 static int vbs_scan_impl(const bsb_vbs* col, const bsb_pred* pred, const uint32_t* mask,
                          uint32_t* out_words, uint64_t* count, int64_t* stats, int8_t* depth,
@@ -780,13 +801,23 @@ static int vbs_scan_impl(const bsb_vbs* col, const bsb_pred* pred, const uint32_
     case BSB_DEEP_SLICED:
       if (K >= 2 && bsb::ds_enabled(mask != nullptr) &&
           (col->deep[0] || (col->deep1_shared > 0 && bsb::ds_zonemap_enabled()))) {
-        if (mask && gate_count) {
+        if (mask) {
+          // gate: the chain's running count, else a sampled estimate
           const unsigned long long gmax =
               (unsigned long long)(sparse_frac() * (double)col->n_rows);
+          unsigned long long* est = nullptr;
+          if (!gate_count && gmax > 0) {
+            BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&est), 8, s));
+            mask_sample_kernel<<<1, 1024, 0, s>>>(mask, a.nb, est);
+            BSB_LAUNCH_CHECK();
+          }
           BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));
-          return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1],
-                             col->deep1_shared, a.A, a.B, pred->op == BSB_BETWEEN, mask,
-                             out_words, a.count, s, gate_count, gmax);
+          const int rc = vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1],
+                                     col->deep1_shared, a.A, a.B, pred->op == BSB_BETWEEN,
+                                     mask, out_words, a.count, s,
+                                     gate_count ? gate_count : est, gmax);
+          if (est) BSB_CUDA(cudaFreeAsync(est, s));
+          return rc;
         }
         return vbs_ds_scan(a.vbs, a.n_rows, col->stride, col->deep_len[1], col->deep1_shared,
                            a.A, a.B, pred->op == BSB_BETWEEN, mask, out_words, a.count, s);

@@ -25,7 +25,7 @@
 // The next super-tile's directory, M_2 words and level-1 deep sectors are
 // requested across phases; the L1 variant prefetches the next super-tile's
 // first-slice bytes into L2 (cp.async.bulk.prefetch) instead of holding them
-// in registers.  MASKED (conjunction chains): see the kernel.
+// in registers.  Masked scans: EPI (this kernel) or vbs_dsm_kernel (below).
 // Measured and dropped: L2 prefetch of deep levels, level j+1
 // requested with level j, cp.async staging of deep levels in shared memory,
 // 5-6 CTAs/SM, extra compare bodies (0x00 / adjacent literal bytes) -- the
@@ -57,11 +57,11 @@ struct DsArgs {
   uint32_t d1gA, d1eA, d1gB, d1eB;
   VbsDesc d;
   Leg A, B;
-  const uint32_t* mask;  // input mask words (MASKED variant)
+  const uint32_t* mask;  // input mask words (masked scans)
   uint32_t* out;
   unsigned long long* count;
   // running-mask gate (conjunction chains): *gate = the mask's row count;
-  // the MASKED kernel runs when it is <= gate_max, the EPI kernel otherwise
+  // the compacted kernel runs when it is <= gate_max, the EPI kernel otherwise
   const unsigned long long* gate;
   unsigned long long gate_max;
   const PdepTables* pdep;  // 8-bit pdep tables (g_pdep_tables, filled once)
@@ -119,7 +119,7 @@ __device__ __forceinline__ uint32_t lane_incl_scan(uint32_t v, int lane) {
 
 // One Alg. 3 level over the lane's deep block (vbs.py:258-284 in deep-row
 // space); false once no lane of the warp has a tied row left.
-template <bool BETWEEN, bool DEADLEG>
+template <bool BETWEEN, bool DEADLEG, bool SPARSE = false>
 __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, const uint32_t* pre,
                                          uint32_t& zA, uint32_t& zB, uint32_t& gtA,
                                          uint32_t& eqA, uint32_t& gtB, uint32_t& eqB) {
@@ -132,7 +132,7 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
 #pragma unroll
     for (int q = 0; q < 8; ++q) w[q] = pre[q];
   } else if (act) {
-    if (j >= 3)
+    if (j >= 3 || SPARSE)
       ldg256_sparse(d.deep[j - 1] + dbk * 32, w);  // only deep blocks still tied
     else
       ldg256(d.deep[j - 1] + dbk * 32, w);
@@ -166,27 +166,16 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
   return true;
 }
 
-// MASKED: rows outside the input mask are dropped from the shallow result and
-// from the deposited deep results; a deep block is scanned only when a row
-// block with masked-in deep rows overlaps it (block-granular: the deep block's
-// unmasked rows are compared too, without changing any result), and the
-// first-slice bytes of fully masked-out row blocks are not loaded.
-// EPI (conjunction chains, dense running masks): the column is scanned as if
-// unmasked and the mask is AND-ed into the result words in phase 3 -- the
-// same words (AND is idempotent), without the masked variant's per-block
-// bookkeeping, which costs more than it skips unless the mask is very sparse.
-// With a gate both variants are launched: MASKED runs when the running
-// mask's row count is <= gate_max, EPI otherwise.
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false, bool EPI = false>
+// EPI (masked scans with a dense mask): the column is scanned as if unmasked
+// and the mask is AND-ed into the result words in phase 3 -- the same words
+// (AND is idempotent).  With a gate, EPI runs when the mask's row count is
+// above gate_max and the compacted vbs_dsm_kernel otherwise.
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool EPI = false>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
-  if (MASKED && a.gate && *a.gate > a.gate_max) return;
   if (EPI && a.gate && *a.gate <= a.gate_max) return;
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
-  constexpr int kLive = (kRd + 31) / 32;
   __shared__ uint32_t rd_all[kDsWarps][kRd];
-  __shared__ uint32_t live_all[kDsWarps][MASKED ? kLive : 1];
   uint32_t* rd = rd_all[threadIdx.x >> 5];
-  uint32_t* live = live_all[threadIdx.x >> 5];  // MASKED: deep blocks to scan
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -225,7 +214,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     for (int u = 0; u < ST; ++u) {
       const int64_t b = (s * ST + u) * 32 + lane;
       m[u] = b < a.nb ? __ldg(d.exist[1] + b) : 0u;
-      if (MASKED || EPI) mk[u] = b < a.nb ? __ldg(a.mask + b) : 0u;
+      if (EPI) mk[u] = b < a.nb ? __ldg(a.mask + b) : 0u;
     }
   };
   auto load_l1 = [&](int64_t lo, int64_t hi, uint32_t (&w)[8]) {
@@ -259,19 +248,8 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
     int offs[ST];
     int soff = 0;  // deep rows of this super-tile so far
     const int sh0 = (int)(dlo & 31);
-    if (MASKED) {
-      if (lane < kLive) live[lane] = 0u;
-      __syncwarp();
-    }
     // first tile's bytes (L2-prefetched by the previous super-tile)
-    if (L1) {
-      if (!MASKED || mP[0]) {
-        fetch(st * ST * 32 + lane, wN, m2s[0], true);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) wN[i] = 0;
-      }
-    }
+    if (L1) fetch(st * ST * 32 + lane, wN, m2s[0], true);
     // ---------------- phase 1: shallow rows (lane = row block)
 #pragma unroll
     for (int u = 0; u < ST; ++u) {
@@ -280,59 +258,41 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       const uint32_t m2 = m2P[u];
       uint32_t valid =
           tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
-      if (MASKED) valid &= mP[u];
       uint32_t res = 0;
       if (L1) {
         uint32_t w[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i] = wN[i];
         uint32_t unused;
-        if (u + 1 < ST) {
-          if (!MASKED || mP[u + 1]) {
-            fetch(b + 32, wN, unused, true);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) wN[i] = 0;
-          }
-        }
+        if (u + 1 < ST) fetch(b + 32, wN, unused, true);
         const uint32_t P = bp_ge(w, a.tP);
         const uint32_t Q = a.twoQ ? bp_ge(w, a.tQ) : 0u;
         res = valid & ~m2 & ((P & ~Q) ^ a.inv);
       }
       rs[u] = res;
       m2s[u] = m2;
-      if (MASKED) vs[u] = valid;
       if (EPI) vs[u] = mP[u];
       const int c2 = __popc(m2);
       const uint32_t incl = lane_incl_scan((uint32_t)c2, lane);
       offs[u] = soff + (int)(incl - (uint32_t)c2);
       soff += (int)__shfl_sync(kFull, incl, 31);
-      if (MASKED && (valid & m2)) {  // deep blocks holding this block's masked-in deep rows
-        const int o = sh0 + offs[u];
-        const int lo = o >> 5, hi = (o + c2 - 1) >> 5;
-        atomicOr(&live[lo >> 5], 1u << (lo & 31));
-        if (hi != lo) atomicOr(&live[hi >> 5], 1u << (hi & 31));
-      }
     }
     // next super-tile's first-slice bytes -> L2 (its first tile is loaded at
-    // the top of the next iteration).  Not for masked scans: a sparse input
-    // mask leaves most of those sectors unread (fetch() skips masked-out
-    // blocks), and the bulk prefetch would pull them from DRAM anyway.
-    if (L1 && !MASKED && has_next && lane == 0) {
+    // the top of the next iteration)
+    if (L1 && has_next && lane == 0) {
       const int64_t nblk = a.nbpad - nxt_b0 < ST * 32 ? a.nbpad - nxt_b0 : ST * 32;
       l2_prefetch(d.bs1 + nxt_b0 * 32, (uint32_t)(nblk * 32));
     }
     // ---------------- phase 2: deep rows (lane = deep block)
     const int64_t db0 = dlo >> 5;
     const int ndt = (sh0 + soff + 31) >> 5;
-    if (MASKED) __syncwarp();
     for (int t0 = 0; t0 < ndt; t0 += 32) {
       const int t = t0 + lane;
       const bool has = t < ndt;
       const int64_t dbk = db0 + t;
       // (the L1 variant's registers go to phase 1: no level-1 prefetch there)
       const uint32_t* pre = (!L1 && t0 == 0) ? wP : nullptr;
-      const bool go = has && (!MASKED || ((live[t >> 5] >> (t & 31)) & 1u));
+      const bool go = has;
       uint32_t zA = go ? kFull : 0u, zB = (BETWEEN && go) ? kFull : 0u;
       uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
       int j0 = 1;
@@ -391,7 +351,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
           }
         }
       }
-      const uint32_t res = EPI ? ((rs[u] | e) & vs[u]) : (rs[u] | (MASKED ? (e & vs[u]) : e));
+      const uint32_t res = EPI ? ((rs[u] | e) & vs[u]) : (rs[u] | e);
       if (b < a.nb) a.out[b] = res;
       cnt += __popc(res);
     }
@@ -402,9 +362,303 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool MASKED = false, bool EPI = false>
+// 16-byte cp.async into shared memory, 64-byte DRAM fetch (sparse sectors).
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+// 16-byte cp.async of the first src_bytes (zero-filled after), dense stream.
+__device__ __forceinline__ void cp_async16z(void* smem, const void* g, int src_bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Masked scans with compacted work (conjunction legs under a sparse running
+// mask, masked scan_vbs).  Same three phases as vbs_ds_kernel, but every
+// phase runs over a per-warp list instead of lane = block:
+//   * lists: lane = R consecutive row blocks of the super-tile (32 R blocks;
+//     their M_2 / mask words staged one super-tile ahead by cp.async);
+//     valid = tail & mask; one packed warp scan gives every block's deep-row
+//     offset and its slot in L_1 (blocks with masked-in shallow rows: the
+//     first-slice compare) and L_3 (blocks with masked-in deep rows: the
+//     deposit); L_d (deep blocks holding L_3's rows) follows from L_3's
+//     sorted deep-row ranges;
+//   * L_1's first-slice sectors are staged in shared memory by cp.async
+//     while phase 2 runs, so the two dependent chains overlap;
+//   * phase 2 runs Alg. 3 over L_d only (lane = list entry), phase 1
+//     compares the staged sectors, phase 3 deposits L_3's windows;
+//   * each lane writes its R result words (zeros where the mask empties a
+//     block; the same words as scanning whole and AND-ing the mask).
+// Instructions and sectors scale with the masked-in blocks, not the column.
+template <bool BETWEEN, bool L1, int R, int WARPS, int MINB, int STAGE>
+__global__ void __launch_bounds__(WARPS * 32, MINB) vbs_dsm_kernel(const __grid_constant__ DsArgs a) {
+  if (a.gate && *a.gate > a.gate_max) return;
+  static_assert(R == 4 || R == 8, "R row blocks per lane: 4 or 8");
+  constexpr int NB = R * 32;    // row blocks per super-tile
+  constexpr int kRd = NB + 8;   // deep blocks touched by a super-tile (+ guard)
+  constexpr int kStage = L1 ? STAGE : 1;  // staged first-slice sectors per super-tile
+  // packed scan fields: deep rows | L_1 entries | L_3 entries
+  constexpr int kB1 = R == 4 ? 14 : 14, kB3 = R == 4 ? 23 : 23;
+  struct __align__(16) Sm {
+    uint32_t sec[kStage][8];
+    uint32_t pm2[NB], pmk[NB];  // next super-tile's M_2 / mask words (cp.async)
+    uint32_t res[NB], m2[NB], vw[NB], rd[kRd];
+    uint16_t offs[NB], l1[NB], l3[NB], ld[kRd];
+  };
+  __shared__ Sm sm_all[WARPS];
+  Sm& S = sm_all[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const VbsDesc& d = a.d;
+  const int K = d.K;
+  const Leg& A = a.A;
+  const Leg& B = a.B;
+  const int lenA = A.len, lenB = BETWEEN ? B.len : 0;
+  const int maxlen = lenA > lenB ? lenA : lenB;
+  const int64_t nsuper = (a.nb + NB - 1) / NB;
+  unsigned long long cnt = 0;
+  auto dir_at = [&](int64_t blk) -> int64_t {
+    return __ldg(d.dir[1] + (blk < a.nbpad ? blk : a.nbpad));
+  };
+  // M_2 and mask words of super-tile s -> pm2 / pmk (one commit group;
+  // words past the column are zero-filled)
+  auto stage_m2 = [&](int64_t s) {
+#pragma unroll
+    for (int c = lane; c < NB / 4; c += 32) {
+      const int64_t w0 = s * NB + c * 4;
+      const int64_t rem = a.nb - w0;
+      const int nbytes = rem >= 4 ? 16 : (rem > 0 ? (int)rem * 4 : 0);
+      cp_async16z(&S.pm2[c * 4], d.exist[1] + (nbytes ? w0 : 0), nbytes);
+      cp_async16z(&S.pmk[c * 4], a.mask + (nbytes ? w0 : 0), nbytes);
+    }
+    cp_async_commit();
+  };
+
+  int64_t st = warp;
+  int64_t dlo = 0;
+  if (st < nsuper) {
+    dlo = dir_at(st * NB);
+    stage_m2(st);
+  }
+  for (; st < nsuper; st += nwarps) {
+    const int64_t sn = st + nwarps;
+    const bool has_next = sn < nsuper;
+    const int64_t nlo = has_next ? dir_at(sn * NB) : 0;
+    const int sh0 = (int)(dlo & 31);
+    const int64_t b0 = st * NB + lane * R;  // this lane's first row block
+    cp_async_wait_all();
+    __syncwarp();
+    // ---------------- lists (lane = R consecutive row blocks)
+    uint32_t m[R], v[R];
+#pragma unroll
+    for (int q = 0; q < R; q += 4) {
+      const uint4 x = *reinterpret_cast<const uint4*>(&S.pm2[lane * R + q]);
+      const uint4 y = *reinterpret_cast<const uint4*>(&S.pmk[lane * R + q]);
+      m[q] = x.x; m[q + 1] = x.y; m[q + 2] = x.z; m[q + 3] = x.w;
+      v[q] = y.x; v[q + 1] = y.y; v[q + 2] = y.z; v[q + 3] = y.w;
+    }
+    if ((st + 1) * NB * 32 > a.n_rows) {  // last super-tile: rows past the column
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] &= b0 + r < a.nb ? tail_valid(b0 + r, a.n_rows) : 0u;
+    }
+    uint32_t tot = 0, f1 = 0, f3 = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      tot += __popc(m[r]);
+      if (L1 && (v[r] & ~m[r])) f1 |= 1u << r;
+      if (v[r] & m[r]) f3 |= 1u << r;
+    }
+    const uint32_t pk = tot | ((uint32_t)__popc(f1) << kB1) | ((uint32_t)__popc(f3) << kB3);
+    const uint32_t incl = lane_incl_scan(pk, lane);
+    const uint32_t all = __shfl_sync(kFull, incl, 31);
+    const uint32_t ex = incl - pk;
+    const int n1 = (int)((all >> kB1) & ((1u << (kB3 - kB1)) - 1u));
+    const int n3 = (int)(all >> kB3);
+    {
+      int off = sh0 + (int)(ex & ((1u << kB1) - 1u));
+      int p1 = (int)((ex >> kB1) & ((1u << (kB3 - kB1)) - 1u));
+      int p3 = (int)(ex >> kB3);
+      uint16_t o16[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint16_t i = (uint16_t)(lane * R + r);
+        o16[r] = (uint16_t)off;
+        off += __popc(m[r]);
+        if ((f1 >> r) & 1u) S.l1[p1++] = i;
+        if ((f3 >> r) & 1u) S.l3[p3++] = i;
+      }
+#pragma unroll
+      for (int q = 0; q < R; q += 4) {
+        *reinterpret_cast<uint4*>(&S.m2[lane * R + q]) = make_uint4(m[q], m[q + 1], m[q + 2], m[q + 3]);
+        *reinterpret_cast<uint4*>(&S.vw[lane * R + q]) = make_uint4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        *reinterpret_cast<uint4*>(&S.res[lane * R + q]) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint2*>(&S.offs[lane * R + q]) =
+            make_uint2((uint32_t)o16[q] | ((uint32_t)o16[q + 1] << 16),
+                       (uint32_t)o16[q + 2] | ((uint32_t)o16[q + 3] << 16));
+      }
+    }
+    __syncwarp();
+    // first-slice sectors of L_1 -> shared memory (in flight during phase 2)
+    if (L1) {
+      const int ns = n1 < kStage ? n1 : kStage;
+      for (int i = lane; i < ns; i += 32) {
+        const uint8_t* g = d.bs1 + (st * NB + S.l1[i]) * 32;
+        cp_async16(&S.sec[i][0], g);
+        cp_async16(&S.sec[i][4], g + 16);
+      }
+      cp_async_commit();
+    }
+    // next super-tile's M_2 and mask words (always one group: wait_group 1
+    // below then means "the first-slice sectors have landed")
+    if (has_next) {
+      stage_m2(sn);
+    } else {
+      cp_async_commit();
+    }
+    // L_d: deep blocks of L_3's rows.  L_3 is in block order, so its deep-row
+    // ranges [lo, hi] (hi <= lo + 1) are sorted and meet only at endpoints.
+    int nd = 0;
+    {
+      int prev_hi = -1;
+      for (int k0 = 0; k0 < n3; k0 += 32) {
+        const int k = k0 + lane;
+        const bool has = k < n3;
+        int lo = 0, hi = 0;
+        if (has) {
+          const int blk = S.l3[k];
+          const int o = (int)S.offs[blk];
+          lo = o >> 5;
+          hi = (o + __popc(S.m2[blk]) - 1) >> 5;
+        }
+        int ph = __shfl_up_sync(kFull, hi, 1);
+        if (lane == 0) ph = prev_hi;
+        const bool e1 = has && lo != ph, e2 = has && hi != lo;
+        const uint32_t b1 = __ballot_sync(kFull, e1), b2 = __ballot_sync(kFull, e2);
+        const int pos = nd + __popc(b1 & lt) + __popc(b2 & lt);
+        if (e1) S.ld[pos] = (uint16_t)lo;
+        if (e2) S.ld[pos + (e1 ? 1 : 0)] = (uint16_t)hi;
+        nd += __popc(b1) + __popc(b2);
+        const int last = (n3 - k0 < 32 ? n3 - k0 : 32) - 1;
+        prev_hi = __shfl_sync(kFull, hi, last);
+      }
+    }
+    __syncwarp();
+    // ---------------- phase 2: listed deep blocks (lane = list entry)
+    const int64_t db0 = dlo >> 5;
+    for (int t0 = 0; t0 < nd; t0 += 32) {
+      const int i = t0 + lane;
+      const bool has = i < nd;
+      const int t = has ? (int)S.ld[i] : 0;
+      const int64_t dbk = db0 + t;
+      uint32_t zA = has ? kFull : 0u, zB = (BETWEEN && has) ? kFull : 0u;
+      uint32_t gtA = 0, eqA = 0, gtB = 0, eqB = 0;
+      int j0 = 1;
+      if (a.d1) {
+        vbs_transition(1, A.len, K, a.d1gA, a.d1eA, kFull, zA, gtA, eqA);
+        if (BETWEEN) {
+          vbs_transition(1, B.len, K, a.d1gB, a.d1eB, kFull, zB, gtB, eqB);
+          zB &= zA | gtA | eqA;
+        }
+        j0 = 2;
+      }
+#pragma unroll
+      for (int j = 1; j <= kMaxLevels; ++j) {
+        if (j < j0) continue;
+        if (j > maxlen ||
+            !ds_level<BETWEEN, L1, true>(a, j, dbk, nullptr, zA, zB, gtA, eqA, gtB, eqB))
+          break;
+      }
+      if (has) S.rd[t] = BETWEEN ? ((gtA | eqA) & ~gtB) : finalize_op(A.op, gtA, eqA, kFull);
+    }
+    // ---------------- phase 1: shallow rows of L_1
+    if (L1) {
+      cp_async_wait1();
+      __syncwarp();
+      for (int i = lane; i < n1; i += 32) {
+        const int blk = S.l1[i];
+        uint32_t w[8];
+        if (i < kStage) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = S.sec[i][q];
+        } else {
+          ldg256_sparse(d.bs1 + (st * NB + blk) * 32, w);
+        }
+        const uint32_t P = bp_ge(w, a.tP);
+        const uint32_t Q = a.twoQ ? bp_ge(w, a.tQ) : 0u;
+        S.res[blk] = S.vw[blk] & ~S.m2[blk] & ((P & ~Q) ^ a.inv);
+      }
+    }
+    __syncwarp();
+    // ---------------- phase 3: deep results of L_3 back to row space
+    for (int i = lane; i < n3; i += 32) {
+      const int blk = S.l3[i];
+      const uint32_t m2 = S.m2[blk];
+      const int o = (int)S.offs[blk];
+      const int wi = o >> 5, sb = o & 31;
+      const int c2 = __popc(m2);
+      const uint32_t lowm = c2 >= 32 ? kFull : ((1u << c2) - 1u);
+      const uint32_t x = __funnelshift_r(S.rd[wi], S.rd[wi + 1], sb) & lowm;
+      const uint32_t e = x == 0u ? 0u : (x == lowm ? m2 : pdep_tab_g(a.pdep, x, m2));
+      S.res[blk] |= e & S.vw[blk];
+    }
+    __syncwarp();
+    // ---------------- result words (lane = its R row blocks)
+#pragma unroll
+    for (int q = 0; q < R; q += 4) {
+      const uint4 r4 = *reinterpret_cast<const uint4*>(&S.res[lane * R + q]);
+      cnt += __popc(r4.x) + __popc(r4.y) + __popc(r4.z) + __popc(r4.w);
+      if (b0 + q + 4 <= a.nb) {
+        *reinterpret_cast<uint4*>(a.out + b0 + q) = r4;
+      } else {
+        const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (b0 + q + e < a.nb) a.out[b0 + q + e] = rr[e];
+      }
+    }
+    dlo = nlo;
+    __syncwarp();
+  }
+#pragma unroll
+  for (int dd = 16; dd > 0; dd >>= 1) cnt += __shfl_xor_sync(kFull, cnt, dd);
+  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
+template <bool BETWEEN, bool L1, int R, int WARPS, int MINB, int STAGE>
+static int launch_dsm_k(const DsArgs& a, cudaStream_t s) {
+  auto kern = vbs_dsm_kernel<BETWEEN, L1, R, WARPS, MINB, STAGE>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, 0);
+  if (per_sm < 1) per_sm = 1;
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
+  const int64_t nsuper = (a.nb + R * 32 - 1) / (R * 32);
+  const int64_t want = (nsuper + WARPS - 1) / WARPS;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  kern<<<grid, WARPS * 32, 0, s>>>(a);
+  BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}
+static int tune(int i);
+template <bool BETWEEN, bool L1>
+static int launch_dsm(const DsArgs& a, cudaStream_t s) {
+  switch (tune(6)) {
+    case 1: return launch_dsm_k<BETWEEN, L1, 4, 8, 6, 16>(a, s);
+    case 2: return launch_dsm_k<BETWEEN, L1, 8, 4, 6, 32>(a, s);
+    case 3: return launch_dsm_k<BETWEEN, L1, 8, 4, 4, 64>(a, s);
+    default: return launch_dsm_k<BETWEEN, L1, 4, 8, 4, 32>(a, s);
+  }
+}
+
+template <bool BETWEEN, bool L1, int ST, bool UNR, bool EPI = false>
 static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, MASKED, EPI>;
+  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, EPI>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -418,15 +672,6 @@ static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 
-template <bool BETWEEN, bool L1>
-static int launch_ds_masked(const DsArgs& a, int st, cudaStream_t s) {
-  switch (st) {
-    case 1: return launch_ds_k<BETWEEN, L1, 1, true, true>(a, s);
-    case 2: return launch_ds_k<BETWEEN, L1, 2, true, true>(a, s);
-    case 3: return launch_ds_k<BETWEEN, L1, 3, true, true>(a, s);
-    default: return launch_ds_k<BETWEEN, L1, 4, true, true>(a, s);
-  }
-}
 template <bool BETWEEN, bool L1, bool UNR>
 static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
@@ -439,39 +684,46 @@ static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
 template <bool BETWEEN, bool L1>
 static int launch_ds_epi(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
-    case 1: return launch_ds_k<BETWEEN, L1, 1, true, false, true>(a, s);
-    case 2: return launch_ds_k<BETWEEN, L1, 2, true, false, true>(a, s);
-    case 3: return launch_ds_k<BETWEEN, L1, 3, true, false, true>(a, s);
-    default: return launch_ds_k<BETWEEN, L1, 4, true, false, true>(a, s);
+    case 1: return launch_ds_k<BETWEEN, L1, 1, true, true>(a, s);
+    case 2: return launch_ds_k<BETWEEN, L1, 2, true, true>(a, s);
+    case 3: return launch_ds_k<BETWEEN, L1, 3, true, true>(a, s);
+    default: return launch_ds_k<BETWEEN, L1, 4, true, true>(a, s);
   }
 }
 template <bool BETWEEN, bool L1>
 static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
-  if (a.mask && a.gate) {
-    if (a.gate_max == 0) {  // gate off (sparse_ppm 0): the epilogue variant alone
-      DsArgs e = a;
-      e.gate = nullptr;
-      return launch_ds_epi<BETWEEN, L1>(e, st, s);
-    }
-    const int rc = launch_ds_masked<BETWEEN, L1>(a, st, s);
-    return rc ? rc : launch_ds_epi<BETWEEN, L1>(a, st, s);
+  if (!a.mask)
+    return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
+  // Masked: the compacted kernel and EPI behind the gate (the mask's row
+  // count vs gate_max; each exits at once when the other applies), or EPI
+  // alone when there is no gate, the gate is off (gate_max 0), bsb_tune
+  // ds_masked=1, or a word array is not 16-byte aligned (the compacted kernel
+  // moves M_2 / mask / result words 16 bytes at a time).
+  const bool al16 = (((uintptr_t)a.mask | (uintptr_t)a.d.exist[1] | (uintptr_t)a.out) & 15u) == 0;
+  if (!a.gate || a.gate_max == 0 || tune(5) != 0 || !al16) {
+    DsArgs e = a;
+    e.gate = nullptr;
+    return launch_ds_epi<BETWEEN, L1>(e, st, s);
   }
-  if (a.mask) return launch_ds_masked<BETWEEN, L1>(a, st, s);
-  return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
+  const int rc = launch_dsm<BETWEEN, L1>(a, s);
+  return rc ? rc : launch_ds_epi<BETWEEN, L1>(a, st, s);
 }
 
 // Run-time tunables (bsb_tune): 0 enable (0 off, 1 all scans, 2 unmasked
 // only), 1 serial pdep blocks, 2 tiles per super-tile (0 = auto), 3 unrolled
-// levels, 4 settle the deep rows' level 1 from the column's zone map (0/1).
-constexpr int kTunes = 5;
-static int g_tune[kTunes] = {-1, -1, -1, -1, -1};
-static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles",
-                                              "ds_unroll", "ds_zonemap"};
+// levels, 4 settle the deep rows' level 1 from the column's zone map (0/1),
+// 5 masked scans (0 gated compacted / EPI pair, 1 EPI only), 6 compacted
+// kernel shape (rows blocks per lane, warps, CTAs per SM; see launch_dsm).
+constexpr int kTunes = 7;
+static int g_tune[kTunes] = {-1, -1, -1, -1, -1, -1, -1};
+static const char* const kTuneKeys[kTunes] = {"ds_enable", "ds_serial", "ds_tiles", "ds_unroll",
+                                              "ds_zonemap", "ds_masked", "dsm_cfg"};
 static int tune(int i) {
   if (g_tune[i] < 0) {
     static const char* const env[kTunes] = {"BSB_DS", "BSB_DS_SERIAL", "BSB_DS_TILES",
-                                            "BSB_DS_UNROLL", "BSB_DS_ZONEMAP"};
-    static const int dflt[kTunes] = {1, 3, 0, 1, 1};
+                                            "BSB_DS_UNROLL", "BSB_DS_ZONEMAP", "BSB_DS_MASKED",
+                                            "BSB_DSM_CFG"};
+    static const int dflt[kTunes] = {1, 3, 0, 1, 1, 0, 0};
     const char* e = std::getenv(env[i]);
     g_tune[i] = e ? std::atoi(e) : dflt[i];
   }
@@ -597,7 +849,7 @@ extern "C" int bsb_tune(const char* key, int64_t value) {
   }
   for (int i = 0; i < bsb::kTunes; ++i)
     if (std::strcmp(key, bsb::kTuneKeys[i]) == 0) {
-      bsb::g_tune[i] = value < 0 ? 0 : (int)value;
+      bsb::g_tune[i] = value < 0 ? -1 : (int)value;  // < 0: back to the default
       return BSB_OK;
     }
   return BSB_EINVAL;

@@ -714,17 +714,20 @@ def test_conj_scan_mask_trivial_and_long_chains(mode):
     assert got.count() == O.words_count(want)
 
 
-@pytest.mark.parametrize("ppm", [0, 50_000, 1_000_000])
-def test_conj_chain_masked_and_epilogue_kernels_vs_oracle(ppm):
+@pytest.mark.parametrize("ppm,cfg", [(0, 0), (50_000, 0), (1_000_000, 0), (1_000_000, 1),
+                                     (1_000_000, 2), (1_000_000, 3)])
+def test_conj_chain_masked_and_epilogue_kernels_vs_oracle(ppm, cfg):
     """Masked PP-VBS scans inside bsb_conj_scan: with sparse_ppm = 10^6 every
-    gated scan skips masked-out deep blocks (MASKED kernel), with 0 it scans
-    the column whole and ANDs the mask into the words (EPI kernel); both
-    equal the pipelined oracle for random 1..8-byte codes (SLICED columns
-    with and without the first-byte zone map), every operator, literals of
-    every length and sparse / dense running masks."""
+    gated scan runs the compacted kernel (work over the masked-in blocks
+    only; every shape dsm_cfg selects), with 0 it scans the column whole and
+    ANDs the mask into the words (EPI kernel); both equal the pipelined
+    oracle for random 1..8-byte codes (SLICED columns with and without the
+    first-byte zone map), every operator, literals of every length and
+    sparse / dense running masks."""
     lib = B._lib.load()
     rng = np.random.default_rng(91)
     assert lib.bsb_tune(b"sparse_ppm", ppm) == 0
+    assert lib.bsb_tune(b"dsm_cfg", cfg) == 0
     try:
         for n, K, shared in ((70_001, 5, False), (40_000, 8, True), (3000, 3, False)):
             lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
@@ -770,7 +773,60 @@ def test_conj_chain_masked_and_epilogue_kernels_vs_oracle(ppm):
                                       [rp(list(pb)), rp(list(p))])
                     assert np.array_equal(got.words, want), (n, K, "BETWEEN", sel)
     finally:
-        lib.bsb_tune(b"sparse_ppm", 0)
+        lib.bsb_tune(b"sparse_ppm", -1)
+        lib.bsb_tune(b"dsm_cfg", -1)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_masked_sliced_scans_compacted_and_epi_vs_oracle(cfg):
+    """Public masked scan_vbs on SLICED columns: the sampled mask density
+    gates the compacted kernel (sparse masks) against EPI (dense masks);
+    ds_masked=1 forces EPI.  Masks of 0.1 % .. 50 % density, masks with
+    empty and full stretches, ragged column ends, every operator and
+    BETWEEN: words, counts equal the oracle."""
+    lib = B._lib.load()
+    rng = np.random.default_rng(400 + cfg)
+    assert lib.bsb_tune(b"dsm_cfg", cfg) == 0
+    try:
+        for n, K in ((300_007, 4), (1 << 17, 6), (40_001, 2)):
+            lens = rng.integers(1, K + 1, size=n).astype(np.uint8)
+            byts = rng.integers(0, 256, size=(n, 8), dtype=np.uint64)
+            byts[:, 0] |= np.uint64(1)
+            codes = np.zeros(n, np.uint64)
+            for k in range(8):
+                use = lens > k
+                codes[use] |= byts[use, k] << np.uint64(8 * k)
+            col = B.build_vbs(codes, lens, deep_mode="sliced")
+            ocol = O.vbs_build(codes, lens)
+            masks = []
+            for dens in (0.001, 0.03, 0.5):
+                masks.append(rng.random(n) < dens)
+            stretch = np.zeros(n, bool)
+            stretch[n // 3: n // 3 + 5000] = True
+            stretch[-37:] = True
+            masks.append(stretch)
+            for mb in masks:
+                mw = O.bools_to_words(mb)
+                r = int(rng.integers(0, n))
+                lit, ll = int(codes[r]), int(lens[r])
+                preds = [O.pred_compare(op, lit, ll) for op in ("EQ", "NE", "LT", "GE")]
+                a, b = sorted(rng.integers(0, n, 2).tolist())
+                pa = int(codes[a]) << (8 * (ocol.K - int(lens[a])))
+                pz = int(codes[b]) << (8 * (ocol.K - int(lens[b])))
+                if pa > pz:
+                    a, b = b, a
+                preds.append(O.pred_between(int(codes[a]), int(lens[a]), int(codes[b]),
+                                            int(lens[b])))
+                for p in preds:
+                    want, _ = O.vbs_scan(ocol, p, mw)
+                    for forced_epi in (0, 1):
+                        lib.bsb_tune(b"ds_masked", forced_epi)
+                        bv, _ = B.scan_vbs(col, rp(list(p)), B.ResultBitVector(n, mw))
+                        assert np.array_equal(bv.words, want), (n, K, p[0], forced_epi)
+                        assert bv.count() == O.words_count(want)
+    finally:
+        lib.bsb_tune(b"ds_masked", -1)
+        lib.bsb_tune(b"dsm_cfg", -1)
 
 
 @pytest.mark.parametrize("n", [1, 1000, 70_001, 1 << 20])

@@ -47,9 +47,12 @@ def test_library_exports_every_header_symbol(lib):
 
 def test_tune_knobs(lib):
     # host-side knobs of the deep-row-space PP-VBS scan; unknown keys rejected
-    for key, val in ((b"ds_serial", 6), (b"ds_tiles", 0), (b"ds_unroll", 1), (b"ds_enable", 1),
-                     (b"sparse_ppm", 0)):
-        assert lib.bsb_tune(key, val) == 0
+    keys = (b"ds_serial", b"ds_tiles", b"ds_unroll", b"ds_enable", b"ds_zonemap", b"ds_masked",
+            b"dsm_cfg", b"sparse_ppm", b"conj_fuse", b"stats_rows", b"ctas_per_sm")
+    for key in keys:
+        assert lib.bsb_tune(key, 1) == 0
+    for key in keys:  # < 0: back to the defaults (later tests in this process)
+        assert lib.bsb_tune(key, -1) == 0
     assert lib.bsb_tune(b"no_such_knob", 1) != 0
     assert lib.bsb_tune(None, 1) != 0
 
