@@ -110,19 +110,33 @@ def measure_cfg1(reps: int = 50) -> dict:
     # 2^24 rows are ~17 MB: a scan is a few microseconds of GPU work, below the
     # cost of one Python-side launch.  The headline number replays the 16
     # rotated scans as one CUDA graph of C ABI calls (as bench.py's step).
-    graph = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream()
-    cap.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.graph(graph, stream=cap):
+    # The reference's scan_byteslice returns the result words (its count is a
+    # separate ResultBitVector method), so the headline calls pass count =
+    # NULL; the same graph with the count (one memset node + atomics per
+    # scan) is reported beside it.
+    def graph_ms(with_count: bool) -> float:
+        for o in outs:
+            o.fill_(-1)
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(graph, stream=cap):
+            for i in range(16):
+                _lib.check(lib.bsb_byteslice_scan(
+                    replicas[i].desc_ref, ctypes_ref(cp), None, outs[i].data_ptr(),
+                    cnts[i].data_ptr() if with_count else None, None, None, cap.cuda_stream),
+                    "cfg1 scan")
+        torch.cuda.current_stream().wait_stream(cap)
+        ms = _time(graph.replay, max(3, reps // 16)) / 16
+        want_w = bv.dwords
         for i in range(16):
-            _lib.check(lib.bsb_byteslice_scan(replicas[i].desc_ref, ctypes_ref(cp), None,
-                                              outs[i].data_ptr(), cnts[i].data_ptr(), None,
-                                              None, cap.cuda_stream), "cfg1 scan")
-    torch.cuda.current_stream().wait_stream(cap)
-    greps = max(3, reps // 16)
-    ms_scan = _time(graph.replay, greps) / 16
-    for i in range(16):
-        assert int(cnts[i].item()) == nsel, "cfg1 graph scan count"
+            assert torch.equal(outs[i], want_w), "cfg1 graph scan words"
+            if with_count:
+                assert int(cnts[i].item()) == nsel, "cfg1 graph scan count"
+        return ms
+
+    ms_scan = graph_ms(False)
+    ms_scan_cnt = graph_ms(True)
     bvs = []
     for i in range(16):
         b, _ = scan_byteslice(replicas[i], pred)
@@ -143,7 +157,9 @@ def measure_cfg1(reps: int = 50) -> dict:
         "scan": {"us": round(ms_scan * 1e3, 2), "gcodes_s": round(n / ms_scan / 1e6, 1),
                  "alg_bytes_per_code": round(ab / n, 4),
                  "frac": round(ab / (ms_scan * 1e-3) / 1e9 / peak, 4),
-                 "timing": "CUDA graph of the 16 rotated C ABI scans, per scan",
+                 "timing": "CUDA graph of the 16 rotated C ABI scans (result words, count = "
+                           "NULL as the reference's scan), per scan",
+                 "with_count_us": round(ms_scan_cnt * 1e3, 2),
                  "eager_us": round(ms_eager * 1e3, 2)},
         "lookup": {"us": round(ms_look * 1e3, 2),
                    "mrows_s": round(nsel / ms_look / 1e3, 1)},

@@ -171,7 +171,11 @@ int bsb_byteslice_build_ranks(const int64_t* ranks, int64_t n_rows, int32_t widt
 int bsb_byteslice_export(const bsb_byteslice* col, uint8_t* out, void* stream);
 
 /* scan_byteslice (byteslice.py:109-140).  mask may be NULL (no input
- * bitvector).  out_words: ceil(n/32) words.  count: one uint64, overwritten.
+ * bitvector).  out_words: ceil(n/32) words.  count: one uint64, overwritten;
+ * NULL (without stats) = words only, like the reference's scan (no memset
+ * node, no atomics).  Columns up to ~19M rows take a single-wave kernel
+ * (every tile's sectors of a level in flight at once, launched with
+ * programmatic stream serialization).
  * stats/depth may be NULL; when given, BETWEEN runs as two pipelined legs and
  * stats (BSB_STATS_WORDS int64, see bsb_stats_layout) / depth (int8 per
  * block) reproduce the reference ScanStats exactly (stats.py:18-84). */

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
-  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+  if (lane == 0 && cnt && a.count) atomicAdd(a.count, cnt);
   flush_stats<STATS>(a, st);
 }
 
@@ -243,7 +243,71 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
-  if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+  if (lane == 0 && cnt && a.count) atomicAdd(a.count, cnt);
+}
+
+// Small columns (every tile fits in one wave of warps, e.g. cfg1's 2^24
+// rows): the persistent pipeline above leaves each warp a serial chain of
+// ~2 round trips per tile.  Here a warp takes T tiles at once and issues
+// every tile's sector of one level before comparing any, so the whole scan
+// is K dependent round trips (level j+1 only for blocks with tied rows,
+// byteslice.py:92-95).
+template <bool BETWEEN, int T>
+__global__ void __launch_bounds__(kScanThreads, 4) bs_scan_small_kernel(const __grid_constant__ ScanArgs a) {
+  // programmatic dependent launch: wait for the stream's previous grid (a
+  // no-op without the launch attribute), then let the next one start its
+  // launch while this one runs (it waits in turn before touching memory)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int K = a.bs.K;
+  const int64_t stride = a.bs.stride;
+  const uint8_t* sl = a.bs.slices;
+  BsState st[T];
+  uint32_t w[T][8];
+#pragma unroll
+  for (int u = 0; u < T; ++u) {
+    const int64_t tile = warp * T + u;
+    st[u].valid = tile < a.ntiles ? tail_valid(tile * 32 + lane, a.n_rows) : 0u;
+    if (st[u].valid) ldg256(sl + (tile * 32 + lane) * 32, w[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < T; ++u) {
+    st[u].zgtA = 0;
+    st[u].zeqA = st[u].valid;
+    st[u].zgtB = 0;
+    st[u].zeqB = st[u].valid;
+    if (st[u].valid) bs_level<BETWEEN>(w[u], a.A, a.B, 0, st[u]);
+  }
+#pragma unroll 1
+  for (int j = 1; j < K; ++j) {
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < T; ++u) {
+      const int64_t tile = warp * T + u;
+      if (bs_tied<BETWEEN>(st[u])) {
+        ldg256_sparse(sl + (int64_t)j * stride + (tile * 32 + lane) * 32, w[u]);
+        any = true;
+      }
+    }
+    if (!__any_sync(kFull, any)) break;
+#pragma unroll
+    for (int u = 0; u < T; ++u)
+      if (bs_tied<BETWEEN>(st[u])) bs_level<BETWEEN>(w[u], a.A, a.B, j, st[u]);
+  }
+  unsigned long long cnt = 0;
+#pragma unroll
+  for (int u = 0; u < T; ++u) {
+    const int64_t b = (warp * T + u) * 32 + lane;
+    const uint32_t res = BETWEEN ? st[u].valid & (st[u].zgtA | st[u].zeqA) & ~st[u].zgtB
+                                 : finalize_op(a.A.op, st[u].zgtA, st[u].zeqA, st[u].valid);
+    if (b < a.nb) a.out[b] = res;
+    cnt += __popc(res);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+  if (lane == 0 && cnt && a.count) atomicAdd(a.count, cnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,7 +506,7 @@ __global__ void trivial_kernel(int64_t n_rows, int64_t nb, const uint32_t* mask,
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+  if ((threadIdx.x & 31) == 0 && c && count) atomicAdd(count, c);
 }
 
 // ------------------------------------------------------------ host helpers
@@ -488,7 +552,7 @@ static int run_trivial(int64_t n, const bsb_pred* p, const uint32_t* mask, uint3
                        uint64_t* count, int64_t* stats, int8_t* depth, int levels,
                        cudaStream_t s) {
   const int64_t nb = (n + 31) / 32;
-  BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
+  if (count) BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
   int grid = (int)((nb + 255) / 256);
   if (grid > 4096) grid = 4096;
   if (grid < 1) grid = 1;
@@ -508,13 +572,64 @@ static int run_trivial(int64_t n, const bsb_pred* p, const uint32_t* mask, uint3
   return BSB_OK;
 }
 
+static int g_scan_nomemset = 0;  // bsb_tune("scan_nomemset"): diagnostics (count not zeroed)
+void set_scan_nomemset(int64_t v) { g_scan_nomemset = v > 0 ? 1 : 0; }
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// launching while the stream's previous kernel runs; it executes
+// griddepcontrol.wait before any memory access.  bsb_tune("pdl", 0): plain.
+static int g_pdl = -1;
+void set_pdl(int64_t v) { g_pdl = v < 0 ? -1 : (v ? 1 : 0); }
+static bool pdl_on() {
+  if (g_pdl < 0) {
+    const char* e = std::getenv("BSB_PDL");
+    g_pdl = e ? (std::atoi(e) != 0) : 1;
+  }
+  return g_pdl != 0;
+}
+template <typename Kern>
+static int launch_pdl(Kern kern, int grid, int block, cudaStream_t s, const ScanArgs& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  BSB_LAUNCH_CHECK();
+  return BSB_OK;
+}
+
+// Small-column ByteSlice path (bs_scan_small_kernel): when every tile fits
+// one wave of 4-tile warps at 4 CTAs per SM; bsb_tune("bs_small", 0) off.
+static int g_bs_small = -1;
+void set_bs_small(int64_t v) { g_bs_small = v < 0 ? -1 : (v ? 1 : 0); }
+static bool small_bs_ok(int64_t ntiles) {
+  if (g_bs_small < 0) {
+    const char* e = std::getenv("BSB_BS_SMALL");
+    g_bs_small = e ? (std::atoi(e) != 0) : 1;
+  }
+  return g_bs_small && ntiles <= (int64_t)sm_count() * 4 * (kScanThreads / 32) * 4;
+}
+
 template <int LAYOUT>
 static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_t s) {
   const bool between = p->op == BSB_BETWEEN;
   const bool stats = a.stats != nullptr;
-  BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
+  if (a.count && !g_scan_nomemset) BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
     if (LAYOUT == BSB_LAYOUT_BYTESLICE) {
+      if (!a.mask && small_bs_ok(a.ntiles)) {
+        constexpr int T = 4;
+        const int64_t warps = (a.ntiles + T - 1) / T;
+        const int grid = (int)((warps + kScanThreads / 32 - 1) / (kScanThreads / 32));
+        return launch_pdl(between ? bs_scan_small_kernel<true, T> : bs_scan_small_kernel<false, T>,
+                          grid, kScanThreads, s, a);
+      }
       if (a.mask) {
         if (between) return launch_scan(bs_scan_kernel<true, true>, a, s);
         return launch_scan(bs_scan_kernel<false, true>, a, s);
@@ -580,7 +695,8 @@ using namespace bsb;
 extern "C" int bsb_byteslice_scan(const bsb_byteslice* col, const bsb_pred* pred,
                                   const uint32_t* mask, uint32_t* out_words, uint64_t* count,
                                   int64_t* stats, int8_t* depth, void* stream) {
-  if (!col || !pred_ok(pred) || !out_words || !count || col->n_rows <= 0) return BSB_EINVAL;
+  if (!col || !pred_ok(pred) || !out_words || (!count && stats) || col->n_rows <= 0)
+    return BSB_EINVAL;
   if (col->n_slices < 1 || col->n_slices > kMaxLevels) return BSB_ERANGE;
   cudaStream_t s = as_stream(stream);
   if (pred->trivial >= 0)

@@ -827,6 +827,9 @@ void set_sparse_ppm(int64_t ppm);  // bsb_scan.cu
 void set_conj_fuse(int64_t v);     // bsb_scan.cu
 void set_ctas_per_sm_cap(int v);   // bsb_build.cu
 void set_stats_rows(int64_t v);    // bsb_scan.cu
+void set_scan_nomemset(int64_t v); // bsb_scan.cu
+void set_bs_small(int64_t v);      // bsb_scan.cu
+void set_pdl(int64_t v);           // bsb_scan.cu
 }
 
 extern "C" int bsb_tune(const char* key, int64_t value) {
@@ -837,6 +840,18 @@ extern "C" int bsb_tune(const char* key, int64_t value) {
   }
   if (std::strcmp(key, "stats_rows") == 0) {  // PP-VBS ScanStats via the row kernel
     bsb::set_stats_rows(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "pdl") == 0) {  // programmatic dependent launch (0/1)
+    bsb::set_pdl(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "bs_small") == 0) {  // small-column ByteSlice kernel (0/1)
+    bsb::set_bs_small(value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "scan_nomemset") == 0) {  // diagnostics: ByteSlice count not zeroed
+    bsb::set_scan_nomemset(value);
     return BSB_OK;
   }
   if (std::strcmp(key, "ctas_per_sm") == 0) {  // persistent-grid cap (0 = none)

@@ -106,6 +106,43 @@ def test_byteslice_random_large_between_and_masks():
                     assert bv.count() == O.words_count(want)
 
 
+@pytest.mark.parametrize("small", [0, 1])
+def test_byteslice_small_column_kernel_and_no_count(small):
+    """Columns that fit one wave take bs_scan_small_kernel (every tile's
+    sectors of a level in flight together, PDL launch); bsb_tune bs_small=0
+    forces the persistent kernel.  Both equal the oracle for w = 8..64,
+    ragged ends, every operator and BETWEEN; count = NULL returns the same
+    words without a count."""
+    import ctypes
+    lib = B._lib.load()
+    rng = np.random.default_rng(900 + small)
+    assert lib.bsb_tune(b"bs_small", small) == 0
+    try:
+        for w, n in ((16, 1 << 24), (8, 1000), (24, (1 << 20) + 33), (64, 70_001), (40, 32)):
+            hi_bound = (1 << w) if w < 64 else (1 << 63)
+            codes = rng.integers(0, hi_bound, size=n, dtype=np.uint64)
+            col = B.build_byteslice(codes, w)
+            planes = O.bs_build(codes, w)
+            K = planes.shape[0]
+            a, b = sorted(int(x) for x in rng.choice(codes, 2))
+            preds = [O.pred_between(a, K, b, K)] + [O.pred_compare(op, b, K) for op in
+                                                    ("EQ", "NE", "LT", "LE", "GT", "GE")]
+            out = torch.empty(-(-n // 32), dtype=torch.int32, device="cuda")
+            for p in preds:
+                want, _ = O.bs_scan(planes, w, n, p)
+                bv, _ = B.scan_byteslice(col, rp(list(p)))
+                assert np.array_equal(bv.words, want), (w, n, p[0])
+                assert bv.count() == O.words_count(want)
+                cp = rp(list(p)).to_c()
+                out.fill_(-1)
+                B._lib.check(lib.bsb_byteslice_scan(col.desc_ref, ctypes.byref(cp), None,
+                                                    out.data_ptr(), None, None, None,
+                                                    B._lib.stream_ptr()), "no-count scan")
+                assert np.array_equal(out.cpu().numpy().view(np.uint32), want), (w, n)
+    finally:
+        lib.bsb_tune(b"bs_small", -1)
+
+
 def test_byteslice_narrow_between_windows():
     """Narrow BETWEEN windows (level-1 inside rows found row by row), windows
     whose bounds share or neighbour their first byte, lo byte 0x00, lo > hi,
