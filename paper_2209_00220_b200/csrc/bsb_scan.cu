@@ -166,7 +166,10 @@ __device__ __forceinline__ bool bs_tied(const BsState& s) {
   return BETWEEN ? ((s.zeqA | s.zeqB) != 0) : (s.zeqA != 0);
 }
 
-template <bool BETWEEN, bool MASKED>
+// STATS (ScanStats of one non-BETWEEN leg, stats.py:18-45): per lane, the
+// blocks that read level j as packed 16-bit counters (bytes = 32 per read,
+// added on flush), blocks skipped by the mask, and the block's depth.
+template <bool BETWEEN, bool MASKED, bool STATS = false>
 __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_constant__ ScanArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -175,8 +178,13 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
   const int64_t stride = a.bs.stride;
   const uint8_t* sl = a.bs.slices;
   unsigned long long cnt = 0;
+  uint32_t lv[STATS ? kMaxLevels / 2 : 1] = {0};  // level-read counters, 2 x 16 bit
+  uint32_t skipped = 0;
   auto valid_of = [&](int64_t tile, uint32_t mword) -> uint32_t {
     return tile_valid(tile, tile * 32 + lane, a.n_rows) & (MASKED ? mword : kFull);
+  };
+  auto count_level = [&](int j) {
+    if (STATS) lv[j >> 1] += 1u << (16 * (j & 1));
   };
   int64_t tX = warp;
   uint32_t vN = 0, mN = kFull, wN[8];
@@ -189,11 +197,13 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
   BsState sY;
   uint32_t w2Y[8];
   int64_t tY = -1;
+  int dY = 0;
   for (;;) {
     // ---- stage X: level 1 of tile tX, issue its level-2 loads
     const bool haveX = tX < a.ntiles;
     BsState sX;
     uint32_t w2X[8];
+    int dX = 0;
     if (haveX) {
       uint32_t w1[8];
 #pragma unroll
@@ -210,7 +220,21 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
       sX.zgtB = 0;
       sX.zeqB = sX.valid;
       bs_level<BETWEEN>(w1, a.A, a.B, 0, sX);
-      if (K >= 2 && bs_tied<BETWEEN>(sX)) ldg256_sparse(sl + stride + (tX * 32 + lane) * 32, w2X);
+      if (STATS) {
+        if (sX.valid) {
+          dX = 1;
+          count_level(0);
+        } else if (tX * 32 + lane < a.nb) {
+          ++skipped;
+        }
+      }
+      if (K >= 2 && bs_tied<BETWEEN>(sX)) {
+        ldg256_sparse(sl + stride + (tX * 32 + lane) * 32, w2X);
+        if (STATS) {
+          dX = 2;
+          count_level(1);
+        }
+      }
     }
     // ---- stage Y: levels 2..K of tile tY, result word
     if (tY >= 0) {
@@ -224,6 +248,10 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
           if (act) {
             uint32_t w[8];
             ldg256_sparse(sl + (int64_t)j * stride + (tY * 32 + lane) * 32, w);
+            if (STATS) {
+              dY = j + 1;
+              count_level(j);
+            }
             bs_level<BETWEEN>(w, a.A, a.B, j, sY);
           }
         }
@@ -231,12 +259,23 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
       const uint32_t res = BETWEEN ? sY.valid & (sY.zgtA | sY.zeqA) & ~sY.zgtB
                                    : finalize_op(a.A.op, sY.zgtA, sY.zeqA, sY.valid);
       const int64_t b = tY * 32 + lane;
-      if (b < a.nb) a.out[b] = res;
+      if (b < a.nb) {
+        a.out[b] = res;
+        if (STATS && a.depth != nullptr) {
+          if (a.depth_max) {
+            const int8_t old = a.depth[b];
+            a.depth[b] = (int8_t)(dY > old ? dY : old);
+          } else {
+            a.depth[b] = (int8_t)dY;
+          }
+        }
+      }
       cnt += __popc(res);
     }
     if (!haveX) break;
     tY = tX;
     sY = sX;
+    dY = dX;
 #pragma unroll
     for (int q = 0; q < 8; ++q) w2Y[q] = w2X[q];
     tX += nwarps;
@@ -244,6 +283,23 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_kernel(const __grid_c
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
   if (lane == 0 && cnt && a.count) atomicAdd(a.count, cnt);
+  if (STATS) {
+#pragma unroll
+    for (int j = 0; j < kMaxLevels; ++j) {
+      unsigned long long w = (lv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) w += __shfl_xor_sync(kFull, w, d);
+      if (lane == 0 && w) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + j), w);
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 8 + j), 32ull * w);
+      }
+    }
+    unsigned long long sk = skipped;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sk += __shfl_xor_sync(kFull, sk, d);
+    if (lane == 0 && sk)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + a.skipped_slot), sk);
+  }
 }
 
 // Small columns (every tile fits in one wave of warps, e.g. cfg1's 2^24
@@ -650,13 +706,26 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   h[16] = a.nb;
   h[18] = levels;
   BSB_CUDA(cudaMemcpyAsync(a.stats, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  // one non-BETWEEN leg with stats: ByteSlice through the pipelined kernel
+  // (per-lane 16-bit level counters: at most 65535 tiles per warp)
+  auto leg = [&](const ScanArgs& g) -> int {
+    if (LAYOUT == BSB_LAYOUT_BYTESLICE) {
+      auto k = g.mask ? bs_scan_kernel<false, true, true> : bs_scan_kernel<false, false, true>;
+      const int grid = persistent_grid(k, kScanThreads, kScanThreads / 32, g.ntiles);
+      const int64_t per_warp = (g.ntiles + (int64_t)grid * 8 - 1) / ((int64_t)grid * 8);
+      if (per_warp < 65536) {
+        k<<<grid, kScanThreads, 0, s>>>(g);
+        BSB_LAUNCH_CHECK();
+        return BSB_OK;
+      }
+    }
+    return g.mask ? launch_scan(scan_kernel<LAYOUT, false, true, true>, g, s)
+                  : launch_scan(scan_kernel<LAYOUT, false, true, false>, g, s);
+  };
   if (!between) {
     a.skipped_slot = 17;
     a.depth_max = 0;
-    int rc = a.mask ? launch_scan(scan_kernel<LAYOUT, false, true, true>, a, s)
-                : launch_scan(scan_kernel<LAYOUT, false, true, false>, a, s);
-    BSB_CUDA(cudaStreamSynchronize(s));
-    return rc;
+    return leg(a);
   }
   uint32_t* tmp = nullptr;
   BSB_CUDA(cudaMallocAsync(&tmp, (size_t)a.nb * 4 + 4, s));
@@ -671,8 +740,7 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   BSB_CUDA(cudaMallocAsync(&dummy, 8, s));
   BSB_CUDA(cudaMemsetAsync(dummy, 0, 8, s));
   leg1.count = dummy;
-  int rc = leg1.mask ? launch_scan(scan_kernel<LAYOUT, false, true, true>, leg1, s)
-                   : launch_scan(scan_kernel<LAYOUT, false, true, false>, leg1, s);
+  int rc = leg(leg1);
   if (rc) return rc;
   ScanArgs leg2 = a;
   leg2.A = a.B;
@@ -680,11 +748,10 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   leg2.mask = tmp;
   leg2.skipped_slot = 19;
   leg2.depth_max = 1;
-  rc = launch_scan(scan_kernel<LAYOUT, false, true, true>, leg2, s);
+  rc = leg(leg2);
   if (rc) return rc;
   BSB_CUDA(cudaFreeAsync(tmp, s));
   BSB_CUDA(cudaFreeAsync(dummy, s));
-  BSB_CUDA(cudaStreamSynchronize(s));
   return BSB_OK;
 }
 
