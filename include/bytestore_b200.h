@@ -302,6 +302,29 @@ int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_i
  * skips the optimisation).  Syncs (the order check). */
 int bsb_rows_sort(const int64_t* rows, int64_t n_ids, int64_t n_rows, int64_t* sorted_rows,
                   int64_t* perm, int32_t* was_sorted, void* stream);
+/* The same locality without the sort, the perm array or the scatter pass
+ * (lists of < 2^32 - 1 ids over columns of < 2^32 - 1 rows; BSB_EINVAL
+ * otherwise): pairs[i] = row | position << 32, partitioned by row bucket (at
+ * most 2^13 buckets of consecutive rows, at least 2^10 rows each; any order
+ * inside a bucket).  bsb_byteslice_lookup_pairs / bsb_vbs_lookup_pairs_dec
+ * look a pair's row up and write the result at its position, so their output
+ * equals the row-id lookup of rows[] (byteslice.py:143-158 / vbs.py:331-371
+ * applied to the given rows; output order = input order).  An id outside
+ * [0, n_rows) becomes row 0xffffffff, which the lookups report as
+ * BSB_ERR_INDEX like any other bad id.  was_sorted NULL: no order check, no
+ * synchronisation; else *was_sorted = 1 and pairs[] untouched when the list
+ * looks ascending (the sampled check of bsb_rows_sort; syncs). */
+int bsb_rows_bucket(const int64_t* rows, int64_t n_ids, int64_t n_rows, uint64_t* pairs,
+                    int32_t* was_sorted, void* stream);
+/* bsb_byteslice_lookup_rows / bsb_vbs_lookup_rows_dec over bsb_rows_bucket
+ * pairs: out*[position] = the lookup of row. */
+int bsb_byteslice_lookup_pairs(const bsb_byteslice* col, const uint64_t* pairs, int64_t n_ids,
+                               uint64_t* out_codes, const int64_t* rank_values,
+                               int64_t* out_values, int32_t* out_values32, uint32_t* err_dev,
+                               void* stream);
+int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs, int64_t n_ids,
+                             const bsb_decode* dec, uint64_t* out_padded, int64_t* out_values,
+                             int32_t* out_values32, uint32_t* err_dev, void* stream);
 /* out[perm[i]] = in[i] for n elements of elem_bytes (4 or 8). */
 int bsb_scatter(const void* in, const int64_t* perm, int64_t n, int32_t elem_bytes, void* out,
                 void* stream);

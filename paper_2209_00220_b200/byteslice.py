@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import device, gather_order, host_u64, scatter_back, stream, to_dev_i64, to_dev_u64
+from .device import device, gather_order, gather_pairs, host_u64, scatter_back, stream, to_dev_i64, to_dev_u64
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
@@ -154,36 +154,40 @@ def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=
                           out_dtype=torch.int64, order: str = "auto", err=None):
     """Device lookup of a row-id list (any order, duplicates allowed; output
     in input order).  Returns codes, or decoded values rank_values[code] when
-    a device value table is given.  order="sort" gathers a long unsorted list
-    in row order and scatters the output back (device.gather_order); "auto"
-    is "keep" for ByteSlice: the order check, the sort and the scatter back
-    cost about what the K random sectors per id they save (measured, DESIGN.md
-    §5).  rank_values None + out_dtype int32: the codes as int32.  An id
-    outside [0, n_rows) raises IndexError (synchronises), unless `err` (a
-    zeroed device int32 word) is given: then the call stays asynchronous and
+    a device value table is given.  order="auto": a long list over a big
+    column that is not ascending is partitioned into bucket-ordered (row,
+    position) pairs first (device.gather_pairs: ids of one bucket share
+    sectors and DRAM pages) and the gather writes every result at its
+    position; "bucket" forces that, "keep" gathers the list as given, "sort"
+    is the older sort + scatter-back path (device.gather_order).
+    rank_values None + out_dtype int32: the codes as int32.  An id outside
+    [0, n_rows) raises IndexError (synchronises), unless `err` (a zeroed
+    device int32 word) is given: then the call stays asynchronous and
     _lib.ERR_INDEX is OR-ed into it."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
-    g, perm = gather_order(rows, col.n_rows, "keep" if order == "auto" else order)
+    pairs = None if order == "sort" else gather_pairs(rows, col.n_rows, order)
+    if pairs is not None:
+        fn, g, perm = lib.bsb_byteslice_lookup_pairs, pairs, None
+    else:
+        fn = lib.bsb_byteslice_lookup_rows
+        g, perm = gather_order(rows, col.n_rows, order if order == "sort" else "keep")
     if rank_values is None:
         if out_dtype == torch.int32:  # codes as int32 (identity dictionaries)
             out = torch.empty(n, dtype=torch.int32, device=rows.device)
-            _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n, None, None,
-                                                     None, out.data_ptr(), _lib.ptr(err), stream()),
-                       "lookup_byteslice")
+            _lib.check(fn(col.desc_ref, g.data_ptr(), n, None, None, None, out.data_ptr(),
+                          _lib.ptr(err), stream()), "lookup_byteslice")
             return scatter_back(out, perm)
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
-        _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n,
-                                                 out.data_ptr(), None, None, None, _lib.ptr(err), stream()),
-                   "lookup_byteslice")
+        _lib.check(fn(col.desc_ref, g.data_ptr(), n, out.data_ptr(), None, None, None,
+                      _lib.ptr(err), stream()), "lookup_byteslice")
         return scatter_back(out, perm)
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
-    _lib.check(lib.bsb_byteslice_lookup_rows(col.desc_ref, g.data_ptr(), n, None,
-                                             rank_values.data_ptr(), p64, p32, _lib.ptr(err), stream()),
-               "lookup_byteslice")
+    _lib.check(fn(col.desc_ref, g.data_ptr(), n, None, rank_values.data_ptr(), p64, p32,
+                  _lib.ptr(err), stream()), "lookup_byteslice")
     return scatter_back(out, perm)
 
 

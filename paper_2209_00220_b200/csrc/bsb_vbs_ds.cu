@@ -830,6 +830,7 @@ void set_stats_rows(int64_t v);    // bsb_scan.cu
 void set_scan_nomemset(int64_t v); // bsb_scan.cu
 void set_bs_small(int64_t v);      // bsb_scan.cu
 void set_pdl(int64_t v);           // bsb_scan.cu
+void set_pair_bits(int64_t v);     // bsb_gather.cu
 }
 
 extern "C" int bsb_tune(const char* key, int64_t value) {
@@ -856,6 +857,10 @@ extern "C" int bsb_tune(const char* key, int64_t value) {
   }
   if (std::strcmp(key, "ctas_per_sm") == 0) {  // persistent-grid cap (0 = none)
     bsb::set_ctas_per_sm_cap((int)value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "pair_bits") == 0) {  // row buckets of bsb_rows_bucket (2^bits)
+    bsb::set_pair_bits(value);
     return BSB_OK;
   }
   if (std::strcmp(key, "conj_fuse") == 0) {  // fused ByteSlice pairs in bsb_conj_scan

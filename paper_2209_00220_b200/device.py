@@ -116,6 +116,39 @@ def gather_order(rows: torch.Tensor, n_rows: int, order: str = "auto"):
     return (rows, None) if was.value else (srt, perm)
 
 
+# Row-id gathers over big columns: lists at least this long are partitioned
+# into bucket-ordered (row, position) pairs (bsb_rows_bucket) unless ascending.
+BUCKET_GATHER_MIN = 1 << 18
+BUCKET_ROWS_MIN = 1 << 24
+_PAIR_LIMIT = (1 << 32) - 1
+
+
+def gather_pairs(rows: torch.Tensor, n_rows: int, order: str = "auto"):
+    """Bucket-ordered row | position << 32 pairs for the *_lookup_pairs entry
+    points, or None when the list should be gathered as given (order="keep",
+    a short list, a small column, an ascending list, or sizes the 32-bit
+    pairs cannot hold).  order="bucket" forces the pairs (no order check, no
+    synchronisation)."""
+    import ctypes
+
+    if order not in ("auto", "sort", "bucket", "keep"):
+        raise ValueError(f"unknown order {order!r}")
+    n = rows.numel()
+    if order == "keep" or n == 0 or n >= _PAIR_LIMIT or n_rows >= _PAIR_LIMIT:
+        return None
+    if order != "bucket" and n < BUCKET_GATHER_MIN:
+        return None
+    if order == "auto" and n_rows < BUCKET_ROWS_MIN:
+        return None
+    lib = _lib.load()
+    pairs = torch.empty(n, dtype=torch.int64, device=rows.device)
+    was = ctypes.c_int32(0)
+    _lib.check(lib.bsb_rows_bucket(rows.data_ptr(), n, int(n_rows), pairs.data_ptr(),
+                                   None if order == "bucket" else ctypes.byref(was), stream()),
+               "gather_pairs")
+    return None if was.value else pairs
+
+
 def scatter_back(out: torch.Tensor, perm) -> torch.Tensor:
     """Output of a gather over sorted ids back in input order."""
     if perm is None:

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import (device, gather_order, host_u32, host_u64, scatter_back, stream, to_dev_i64,
+from .device import (device, gather_order, gather_pairs, host_u32, host_u64, scatter_back, stream, to_dev_i64,
                      to_dev_u8, to_dev_u64)
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
@@ -274,21 +274,34 @@ def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
                     out_dtype=torch.int64, level_counts=None, order: str = "auto", err=None):
     """Device lookup of a row-id list (any order, output in input order):
     padded codes, or decoded values when the dictionary's sorted padded codes
-    / values are given.  order: see lookup_byteslice_rows; "auto" sorts for
-    columns with codes of 3+ bytes (a deep row costs up to ~2K random
-    sectors: bs1, existence words, directory, deep bytes).  Ids outside
-    [0, n_rows) raise IndexError; `err` as in lookup_byteslice_rows."""
+    / values are given.  order: see lookup_byteslice_rows (a deep row costs up
+    to ~2K random sectors: bs1, existence words, directory, deep bytes, so
+    locality matters more here); with a binary-search dictionary or
+    level_counts the long unsorted lists take the sort + scatter-back path.
+    Ids outside [0, n_rows) raise IndexError; `err` as in
+    lookup_byteslice_rows."""
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
-    g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order))
     lc = None if level_counts is None else level_counts.data_ptr()
     if sorted_padded is None:
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
+        pairs = None
+        if lc is None and order != "sort":
+            pairs = gather_pairs(rows, col.n_rows, order)
+        if pairs is not None:
+            _lib.check(lib.bsb_vbs_lookup_pairs_dec(col.desc_ref, pairs.data_ptr(), n, None,
+                                                    out.data_ptr(), None, None, _lib.ptr(err),
+                                                    stream()), "lookup_vbs")
+            return out
+        g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order) if order in
+                               ("auto", "sort") else "keep")
         _lib.check(lib.bsb_vbs_lookup_rows(col.desc_ref, g.data_ptr(), n, out.data_ptr(),
                                            None, None, 0, None, None, lc, _lib.ptr(err), stream()),
                    "lookup_vbs")
         return scatter_back(out, perm)
+    g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order) if order in
+                           ("auto", "sort") else "keep")
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
@@ -306,14 +319,17 @@ def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64,
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
-    g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order))
+    pairs = None if order == "sort" else gather_pairs(rows, col.n_rows, order)
+    if pairs is not None:
+        fn, g, perm = lib.bsb_vbs_lookup_pairs_dec, pairs, None
+    else:
+        fn = lib.bsb_vbs_lookup_rows_dec
+        g, perm = gather_order(rows, col.n_rows, order if order == "sort" else "keep")
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None
-    _lib.check(lib.bsb_vbs_lookup_rows_dec(col.desc_ref, g.data_ptr(), n,
-                                           ctypes.byref(decoder), None, p64, p32,
-                                           _lib.ptr(err), stream()),
-               "lookup_vbs")
+    _lib.check(fn(col.desc_ref, g.data_ptr(), n, ctypes.byref(decoder), None, p64, p32,
+                  _lib.ptr(err), stream()), "lookup_vbs")
     return scatter_back(out, perm)
 
 

@@ -260,6 +260,69 @@ def test_row_lookups_sorted_gather():
     assert np.array_equal(got, vals[ids].astype(np.int32))
 
 
+@pytest.mark.parametrize("n", [1_500, 70_001, 3_000_017, (1 << 25) + 12_345])
+def test_row_lookups_bucket_pairs(n):
+    """Row-id lookups through bucket-ordered (row, position) pairs
+    (bsb_rows_bucket + *_lookup_pairs): output in input order with duplicates,
+    skewed id lists (one hot bucket), one- and two-pass bucket plans, both
+    layouts, codes / decoded values, bad ids reported; and the pairs
+    themselves are a permutation of (row, position) ordered by bucket."""
+    import ctypes
+
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.device import stream
+    rng = np.random.default_rng(n)
+    m = 200_003 if n < (1 << 25) else 1_000_003
+    ids = rng.integers(0, n, size=m)
+    ids[:1000] = ids[1000:2000]  # duplicates
+    ids[5000:60_000] = rng.integers(n // 3, n // 3 + min(n // 4, 900), size=55_000)  # hot bucket
+    t = torch.from_numpy(ids).cuda()
+    # the pairs: every (row, position) once, buckets ascending
+    pairs = torch.empty(m, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.load().bsb_rows_bucket(t.data_ptr(), m, n, pairs.data_ptr(), None, stream()),
+               "bsb_rows_bucket")
+    ph = pairs.cpu().numpy().view(np.uint64)
+    prow, ppos = (ph & np.uint64(0xFFFFFFFF)).astype(np.int64), (ph >> np.uint64(32)).astype(np.int64)
+    assert np.array_equal(np.sort(ppos), np.arange(m))
+    assert np.array_equal(prow, ids[ppos])
+    bits = max(1, int(n - 1).bit_length())
+    bb = min(13, max(1, bits - 10))
+    bucket = np.minimum(prow >> (bits - bb), (1 << bb) - 1)
+    assert np.all(np.diff(bucket) >= 0)
+    codes = rng.integers(0, 1 << 20, size=n, dtype=np.uint64)
+    col = B.build_byteslice(codes, 20)
+    got = B.lookup_byteslice_rows(col, t, order="bucket").cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), codes[ids])
+    got = B.lookup_byteslice_rows(col, t, out_dtype=torch.int32, order="auto").cpu().numpy()
+    assert np.array_equal(got, codes[ids].astype(np.int32))
+    vals, od, vcodes, lens = _ppe_column(1.1, 16, n, 9)
+    vcol = B.build_vbs(vcodes, lens)
+    K = vcol.max_len
+    padded = vcodes << (np.uint64(8) * (np.uint64(K) - lens.astype(np.uint64)))
+    got = B.lookup_vbs_rows(vcol, t, order="bucket").cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), padded[ids])
+    d = B.Dictionary.build(B.build_frequency_table(vals, B.ColumnKind.NUMERIC),
+                           "prefix_preserving")
+    for order in ("bucket", "auto"):
+        got = B.lookup_vbs_rows_dec(vcol, t, d.dev_decoder, out_dtype=torch.int32,
+                                    order=order).cpu().numpy()
+        assert np.array_equal(got, vals[ids].astype(np.int32)), order
+    # ascending lists are gathered as given under "auto"; same values
+    srt = np.sort(ids)
+    got = B.lookup_byteslice_rows(col, torch.from_numpy(srt), order="auto").cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), codes[srt])
+    # bad ids: IndexError / the async error word, through the pairs as well
+    for bad in (n, -1, 1 << 40):
+        ids2 = ids.copy()
+        ids2[m // 2] = bad
+        t2 = torch.from_numpy(ids2).cuda()
+        with pytest.raises(IndexError):
+            B.lookup_byteslice_rows(col, t2, order="bucket")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        B.lookup_vbs_rows_dec(vcol, t2, d.dev_decoder, order="bucket", err=err)
+        assert int(err.item()) & _lib.ERR_INDEX
+
+
 def test_byteslice_errors():
     with pytest.raises(ValueError):
         B.build_byteslice([], 8)
