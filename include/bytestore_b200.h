@@ -302,29 +302,49 @@ int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_i
  * skips the optimisation).  Syncs (the order check). */
 int bsb_rows_sort(const int64_t* rows, int64_t n_ids, int64_t n_rows, int64_t* sorted_rows,
                   int64_t* perm, int32_t* was_sorted, void* stream);
-/* The same locality without the sort, the perm array or the scatter pass
- * (lists of < 2^32 - 1 ids over columns of < 2^32 - 1 rows; BSB_EINVAL
- * otherwise): pairs[i] = row | position << 32, partitioned by row bucket (at
- * most 2^13 buckets of consecutive rows, at least 2^10 rows each; any order
- * inside a bucket).  bsb_byteslice_lookup_pairs / bsb_vbs_lookup_pairs_dec
- * look a pair's row up and write the result at its position, so their output
- * equals the row-id lookup of rows[] (byteslice.py:143-158 / vbs.py:331-371
- * applied to the given rows; output order = input order).  An id outside
- * [0, n_rows) becomes row 0xffffffff, which the lookups report as
- * BSB_ERR_INDEX like any other bad id.  was_sorted NULL: no order check, no
- * synchronisation; else *was_sorted = 1 and pairs[] untouched when the list
- * looks ascending (the sampled check of bsb_rows_sort; syncs). */
+/* The same locality without the sort or the perm array (lists of < 2^32 - 1
+ * ids over columns of < 2^32 - 1 rows; BSB_EINVAL otherwise): pairs[i] =
+ * row | position << 32, partitioned by row bucket (at most 2^13 buckets of
+ * consecutive rows, at least 2^10 rows each; any order inside a bucket).  An
+ * id outside [0, n_rows) becomes row 0xffffffff, which the pair lookups
+ * report as BSB_ERR_INDEX like any other bad id.  Never synchronises.
+ * unsorted_dev NULL: always partition.  Else *unsorted_dev (a device word) =
+ * 0 when the list looks ascending (the sampled check of bsb_rows_sort) and
+ * the partition kernels exit at once, 1 otherwise: the verdict stays on the
+ * device and gates the pair lookups below. */
 int bsb_rows_bucket(const int64_t* rows, int64_t n_ids, int64_t n_rows, uint64_t* pairs,
-                    int32_t* was_sorted, void* stream);
+                    uint32_t* unsorted_dev, void* stream);
 /* bsb_byteslice_lookup_rows / bsb_vbs_lookup_rows_dec over bsb_rows_bucket
- * pairs: out*[position] = the lookup of row. */
-int bsb_byteslice_lookup_pairs(const bsb_byteslice* col, const uint64_t* pairs, int64_t n_ids,
+ * pairs: out*[position] = the lookup of row, i.e. the row-id lookup of the
+ * list the pairs were made from (byteslice.py:143-158 / vbs.py:331-371
+ * applied to the given rows; output order = input order).  rows /
+ * unsorted_dev NULL: the pairs are used.  With both given (the list and the
+ * verdict bsb_rows_bucket left), *unsorted_dev == 0 gathers rows[] as given
+ * instead -- the alternative that does not apply is launched and exits, so
+ * the choice costs no host synchronisation. */
+int bsb_byteslice_lookup_pairs(const bsb_byteslice* col, const uint64_t* pairs,
+                               const int64_t* rows, const uint32_t* unsorted_dev, int64_t n_ids,
                                uint64_t* out_codes, const int64_t* rank_values,
                                int64_t* out_values, int32_t* out_values32, uint32_t* err_dev,
                                void* stream);
-int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs, int64_t n_ids,
-                             const bsb_decode* dec, uint64_t* out_padded, int64_t* out_values,
-                             int32_t* out_values32, uint32_t* err_dev, void* stream);
+int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs, const int64_t* rows,
+                             const uint32_t* unsorted_dev, int64_t n_ids, const bsb_decode* dec,
+                             uint64_t* out_padded, int64_t* out_values, int32_t* out_values32,
+                             uint32_t* err_dev, void* stream);
+/* bsb_byteslice_lookup_rows / bsb_vbs_lookup_rows_dec with the locality
+ * chosen on the device: the sampled order check, then the gather of rows[] as
+ * given and the bucket partition + pair gather, each gated on the verdict
+ * (the one that does not apply exits at once).  Same arguments, same output,
+ * no host synchronisation beyond err_dev == NULL's.  Lists of fewer than 2
+ * ids or sizes the 32-bit pairs cannot hold are gathered as given. */
+int bsb_byteslice_lookup_rows_auto(const bsb_byteslice* col, const int64_t* rows, int64_t n_ids,
+                                   uint64_t* out_codes, const int64_t* rank_values,
+                                   int64_t* out_values, int32_t* out_values32,
+                                   uint32_t* err_dev, void* stream);
+int bsb_vbs_lookup_rows_dec_auto(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
+                                 const bsb_decode* dec, uint64_t* out_padded,
+                                 int64_t* out_values, int32_t* out_values32, uint32_t* err_dev,
+                                 void* stream);
 /* out[perm[i]] = in[i] for n elements of elem_bytes (4 or 8). */
 int bsb_scatter(const void* in, const int64_t* perm, int64_t n, int32_t elem_bytes, void* out,
                 void* stream);

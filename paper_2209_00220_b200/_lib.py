@@ -97,11 +97,15 @@ _SIGS = {
     "bsb_vbs_lookup_rows_dec": (c_int32, [POINTER(BsbVbs), _P, c_int64, POINTER(BsbDecode), _P,
                                           _P, _P, _P, _P]),
     "bsb_rows_sort": (c_int32, [_P, c_int64, c_int64, _P, _P, POINTER(c_int32), _P]),
-    "bsb_rows_bucket": (c_int32, [_P, c_int64, c_int64, _P, POINTER(c_int32), _P]),
-    "bsb_byteslice_lookup_pairs": (c_int32, [POINTER(BsbByteSlice), _P, c_int64, _P, _P, _P, _P,
-                                             _P, _P]),
-    "bsb_vbs_lookup_pairs_dec": (c_int32, [POINTER(BsbVbs), _P, c_int64, POINTER(BsbDecode), _P,
-                                           _P, _P, _P, _P]),
+    "bsb_rows_bucket": (c_int32, [_P, c_int64, c_int64, _P, _P, _P]),
+    "bsb_byteslice_lookup_pairs": (c_int32, [POINTER(BsbByteSlice), _P, _P, _P, c_int64, _P, _P,
+                                             _P, _P, _P, _P]),
+    "bsb_vbs_lookup_pairs_dec": (c_int32, [POINTER(BsbVbs), _P, _P, _P, c_int64,
+                                           POINTER(BsbDecode), _P, _P, _P, _P, _P]),
+    "bsb_byteslice_lookup_rows_auto": (c_int32, [POINTER(BsbByteSlice), _P, c_int64, _P, _P, _P,
+                                                 _P, _P, _P]),
+    "bsb_vbs_lookup_rows_dec_auto": (c_int32, [POINTER(BsbVbs), _P, c_int64, POINTER(BsbDecode),
+                                               _P, _P, _P, _P, _P]),
     "bsb_scatter": (c_int32, [_P, _P, c_int64, c_int32, _P, _P]),
     "bsb_bits_to_rows": (c_int32, [_P, c_int64, _P, POINTER(c_int64), _P]),
     "bsb_bits_to_rows_async": (c_int32, [_P, c_int64, c_int64, _P, _P, _P]),

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import device, gather_order, gather_pairs, host_u64, scatter_back, stream, to_dev_i64, to_dev_u64
+from .device import device, host_u64, row_gather_plan, scatter_back, stream, to_dev_i64, to_dev_u64
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
 
@@ -155,10 +155,10 @@ def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=
     """Device lookup of a row-id list (any order, duplicates allowed; output
     in input order).  Returns codes, or decoded values rank_values[code] when
     a device value table is given.  order="auto": a long list over a big
-    column that is not ascending is partitioned into bucket-ordered (row,
-    position) pairs first (device.gather_pairs: ids of one bucket share
-    sectors and DRAM pages) and the gather writes every result at its
-    position; "bucket" forces that, "keep" gathers the list as given, "sort"
+    column is partitioned into bucket-ordered (row, position) pairs first
+    (bsb_rows_bucket: ids of one bucket share sectors and DRAM pages) unless
+    a sampled check on the device finds it ascending, the results go back to
+    their positions, and nothing synchronises; "bucket" skips the check, "keep" gathers the list as given, "sort"
     is the older sort + scatter-back path (device.gather_order).
     rank_values None + out_dtype int32: the codes as int32.  An id outside
     [0, n_rows) raises IndexError (synchronises), unless `err` (a zeroed
@@ -167,12 +167,8 @@ def lookup_byteslice_rows(col: ByteSliceColumn, rows: torch.Tensor, rank_values=
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
-    pairs = None if order == "sort" else gather_pairs(rows, col.n_rows, order)
-    if pairs is not None:
-        fn, g, perm = lib.bsb_byteslice_lookup_pairs, pairs, None
-    else:
-        fn = lib.bsb_byteslice_lookup_rows
-        g, perm = gather_order(rows, col.n_rows, order if order == "sort" else "keep")
+    fn, g, perm = row_gather_plan(rows, col.n_rows, order, lib.bsb_byteslice_lookup_rows_auto,
+                                  lib.bsb_byteslice_lookup_pairs, lib.bsb_byteslice_lookup_rows)
     if rank_values is None:
         if out_dtype == torch.int32:  # codes as int32 (identity dictionaries)
             out = torch.empty(n, dtype=torch.int32, device=rows.device)

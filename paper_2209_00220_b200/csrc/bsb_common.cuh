@@ -95,6 +95,22 @@ __device__ __forceinline__ void ldg256_free(const void* p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
+// bsb_gather.cu: the sampled order check (*unsorted_dev = 1 when a sampled
+// adjacent pair descends, else 0) and the bucket partition into row |
+// position << 32 pairs, every kernel gated on *gate != 0 (gate NULL: always).
+int rows_order_check(const int64_t* rows, int64_t n_ids, uint32_t* unsorted_dev, cudaStream_t s);
+void rows_order_check_launch(const int64_t* rows, int64_t n_ids, uint32_t* unsorted_dev,
+                             cudaStream_t s);  // the kernel alone (word already zero)
+int rows_bucket_gated(const int64_t* rows, int64_t n_ids, int64_t n_rows, uint64_t* pairs,
+                      const uint32_t* gate, cudaStream_t s);
+
+// Device-side gate of a kernel that is one of two alternatives chosen by a
+// device word (no host synchronisation, graph-capturable): the kernel runs
+// when gate is NULL or (*gate != 0) == want.
+__device__ __forceinline__ bool gate_closed(const uint32_t* gate, bool want) {
+  return gate && (__ldg(gate) != 0) != want;
+}
+
 // 1-D TMA bulk copies global -> shared memory, completion on an mbarrier.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

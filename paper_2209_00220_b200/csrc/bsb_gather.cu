@@ -127,8 +127,9 @@ __device__ __forceinline__ uint32_t pair_row(int64_t r, int64_t n_rows) {
 
 __global__ void __launch_bounds__(1024)
 pair_hist_kernel(const int64_t* __restrict__ rows, int64_t n, int64_t n_rows, PairPlan pl,
-                 uint32_t* __restrict__ hist) {
+                 uint32_t* __restrict__ hist, const uint32_t* __restrict__ gate) {
   __shared__ uint32_t h[1 << kPairBucketBits];
+  if (gate_closed(gate, true)) return;
   for (int b = threadIdx.x; b < pl.n_buckets; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -144,8 +145,10 @@ pair_hist_kernel(const int64_t* __restrict__ rows, int64_t n, int64_t n_rows, Pa
 __global__ void __launch_bounds__(1024)
 pair_offsets_kernel(const uint32_t* __restrict__ hist, PairPlan pl, uint32_t n,
                     uint32_t* __restrict__ cur1, uint32_t* __restrict__ cur2,
-                    uint32_t* __restrict__ seg, uint32_t* __restrict__ seg1) {
+                    uint32_t* __restrict__ seg, uint32_t* __restrict__ seg1,
+                    const uint32_t* __restrict__ gate) {
   __shared__ uint32_t wsum[32];
+  if (gate_closed(gate, true)) return;
   constexpr int kPer = (1 << kPairBucketBits) / 1024;
   uint32_t c[kPer], tot = 0;
   const int b0 = threadIdx.x * kPer;
@@ -206,8 +209,9 @@ template <bool FIRST>
 __global__ void __launch_bounds__(kPairThreads, 3)
 pair_pass_kernel(const void* __restrict__ src, uint64_t* __restrict__ dst, int64_t n_rows,
                  PairPlan pl, const uint32_t* __restrict__ seg, int n_seg,
-                 uint32_t* __restrict__ cursor) {
+                 uint32_t* __restrict__ cursor, const uint32_t* __restrict__ gate) {
   extern __shared__ __align__(16) uint64_t pair_smem[];
+  if (gate_closed(gate, true)) return;
   uint64_t* stage = pair_smem;                      // kPairChunk + 2: the TMA destination
   uint64_t* pair_buf = pair_smem + kPairChunk + 2;  // kPairChunk pairs ordered by bin
   __shared__ uint64_t bar;
@@ -373,28 +377,24 @@ extern "C" int bsb_rows_sort(const int64_t* rows, int64_t n_ids, int64_t n_rows,
   return sort_pairs<unsigned long long>(rows, n_ids, bits - shift, shift, sorted_rows, perm, s);
 }
 
-extern "C" int bsb_rows_bucket(const int64_t* rows, int64_t n_ids, int64_t n_rows,
-                               uint64_t* pairs, int32_t* was_sorted, void* stream) {
-  if (!rows || !pairs || n_ids < 0 || n_rows <= 0) return BSB_EINVAL;
-  if (n_ids >= (int64_t)UINT32_MAX || n_rows >= (int64_t)UINT32_MAX) return BSB_EINVAL;
-  cudaStream_t s = as_stream(stream);
-  if (was_sorted) *was_sorted = 0;
-  if (n_ids == 0) return BSB_OK;
-  if (was_sorted && n_ids >= 2) {
-    unsigned int* bad = nullptr;
-    BSB_CUDA(cudaMallocAsync(&bad, 4, s));
-    BSB_CUDA(cudaMemsetAsync(bad, 0, 4, s));
-    rows_sample_check_kernel<<<4, 1024, 0, s>>>(rows, n_ids, bad);
+namespace bsb {
+
+void rows_order_check_launch(const int64_t* rows, int64_t n_ids, uint32_t* unsorted_dev,
+                             cudaStream_t s) {
+  rows_sample_check_kernel<<<4, 1024, 0, s>>>(rows, n_ids, unsorted_dev);
+}
+
+int rows_order_check(const int64_t* rows, int64_t n_ids, uint32_t* unsorted_dev, cudaStream_t s) {
+  BSB_CUDA(cudaMemsetAsync(unsorted_dev, 0, 4, s));
+  if (n_ids >= 2) {
+    rows_sample_check_kernel<<<4, 1024, 0, s>>>(rows, n_ids, unsorted_dev);
     BSB_LAUNCH_CHECK();
-    unsigned int h = 0;
-    BSB_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, s));
-    BSB_CUDA(cudaFreeAsync(bad, s));
-    BSB_CUDA(cudaStreamSynchronize(s));
-    if (!h) {
-      *was_sorted = 1;
-      return BSB_OK;
-    }
   }
+  return BSB_OK;
+}
+
+int rows_bucket_gated(const int64_t* rows, int64_t n_ids, int64_t n_rows, uint64_t* pairs,
+                      const uint32_t* gate, cudaStream_t s) {
   int bits = 1;
   while (bits < 32 && ((uint64_t)(n_rows - 1) >> bits) != 0) ++bits;
   PairPlan pl;
@@ -429,24 +429,42 @@ extern "C" int bsb_rows_bucket(const int64_t* rows, int64_t n_ids, int64_t n_row
   int gh = (int)((n_ids + 1024 * 8 - 1) / (1024 * 8));
   if (gh > sm_count() * 2) gh = sm_count() * 2;
   if (gh < 1) gh = 1;
-  pair_hist_kernel<<<gh, 1024, 0, s>>>(rows, n_ids, n_rows, pl, hist);
+  pair_hist_kernel<<<gh, 1024, 0, s>>>(rows, n_ids, n_rows, pl, hist, gate);
   BSB_LAUNCH_CHECK();
   uint32_t* seg1 = seg + kPairMaxBins + 2;  // the first pass's one segment {0, n}
-  pair_offsets_kernel<<<1, 1024, 0, s>>>(hist, pl, (uint32_t)n_ids, cur1, cur2, seg, seg1);
+  pair_offsets_kernel<<<1, 1024, 0, s>>>(hist, pl, (uint32_t)n_ids, cur1, cur2, seg, seg1,
+                                         gate);
   BSB_LAUNCH_CHECK();
   int gp = (int)(chunks < (int64_t)sm_count() * 3 ? chunks : (int64_t)sm_count() * 3);
   pair_pass_kernel<true><<<gp, kPairThreads, kPairSmemBytes, s>>>(
-      rows, pl.sub_bits ? mid : pairs, n_rows, pl, seg1, 1, cur1);
+      rows, pl.sub_bits ? mid : pairs, n_rows, pl, seg1, 1, cur1, gate);
   BSB_LAUNCH_CHECK();
   if (pl.sub_bits) {
     int gp2 = (int)(chunks + n_groups < (int64_t)sm_count() * 3 ? chunks + n_groups
                                                                  : (int64_t)sm_count() * 3);
-    pair_pass_kernel<false><<<gp2, kPairThreads, kPairSmemBytes, s>>>(mid, pairs, n_rows, pl,
-                                                                      seg, n_groups, cur2);
+    pair_pass_kernel<false><<<gp2, kPairThreads, kPairSmemBytes, s>>>(
+        mid, pairs, n_rows, pl, seg, n_groups, cur2, gate);
     BSB_LAUNCH_CHECK();
   }
   BSB_CUDA(cudaFreeAsync(scratch, s));
   return BSB_OK;
+}
+
+}  // namespace bsb
+
+extern "C" int bsb_rows_bucket(const int64_t* rows, int64_t n_ids, int64_t n_rows,
+                               uint64_t* pairs, uint32_t* unsorted_dev, void* stream) {
+  if (!rows || !pairs || n_ids < 0 || n_rows <= 0) return BSB_EINVAL;
+  if (n_ids >= (int64_t)UINT32_MAX || n_rows >= (int64_t)UINT32_MAX) return BSB_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  if (unsorted_dev) {
+    // the sampled order check of bsb_rows_sort, its verdict left on the
+    // device: every kernel below exits at once when the list looks ascending
+    const int rc = rows_order_check(rows, n_ids, unsorted_dev, s);
+    if (rc) return rc;
+  }
+  if (n_ids == 0) return BSB_OK;
+  return rows_bucket_gated(rows, n_ids, n_rows, pairs, unsorted_dev, s);
 }
 
 extern "C" int bsb_scatter(const void* in, const int64_t* perm, int64_t n, int32_t elem_bytes,

@@ -48,12 +48,14 @@ __device__ __forceinline__ void emit(uint64_t* oc, int64_t* ov, int32_t* ov32, i
 // back to the caller's order.  A kernel of its own: the same stores issued
 // from inside the gather measured 2.5x slower (B200: 2^24 int32 results, 409
 // MB written and 330 MB more read than the 64 MB the output has -- the column
-// sectors streaming through L2 evict the partially written output sectors,
-// an L2 evict_last policy on the stores changed nothing), while alone the
-// scatter keeps its 64 MB window in L2.
+// sectors streaming through L2 evict the partially written output sectors),
+// L2 evict_last / evict_first policies on the stores and the streamed loads
+// changed nothing in either form.
 template <typename T>
 __global__ void pair_scatter_kernel(const unsigned long long* __restrict__ pairs,
-                                    const T* __restrict__ in, int64_t n, T* __restrict__ out) {
+                                    const T* __restrict__ in, int64_t n, T* __restrict__ out,
+                                    const uint32_t* __restrict__ gate) {
+  if (gate_closed(gate, true)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[__ldg(pairs + i) >> 32] = in[i];
@@ -72,12 +74,12 @@ static int pair_out_alloc(PairOut& t, int64_t n, bool oc, bool ov, bool ov32, cu
   return BSB_OK;
 }
 static int pair_out_scatter(PairOut& t, const uint64_t* pairs, int64_t n, uint64_t* oc,
-                            int64_t* ov, int32_t* ov32, cudaStream_t s) {
+                            int64_t* ov, int32_t* ov32, const uint32_t* gate, cudaStream_t s) {
   const int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
   const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(pairs);
-  if (t.oc) pair_scatter_kernel<uint64_t><<<g, 256, 0, s>>>(pp, t.oc, n, oc);
-  if (t.ov) pair_scatter_kernel<int64_t><<<g, 256, 0, s>>>(pp, t.ov, n, ov);
-  if (t.ov32) pair_scatter_kernel<int32_t><<<g, 256, 0, s>>>(pp, t.ov32, n, ov32);
+  if (t.oc) pair_scatter_kernel<uint64_t><<<g, 256, 0, s>>>(pp, t.oc, n, oc, gate);
+  if (t.ov) pair_scatter_kernel<int64_t><<<g, 256, 0, s>>>(pp, t.ov, n, ov, gate);
+  if (t.ov32) pair_scatter_kernel<int32_t><<<g, 256, 0, s>>>(pp, t.ov32, n, ov32, gate);
   BSB_LAUNCH_CHECK();
   if (t.oc) BSB_CUDA(cudaFreeAsync(t.oc, s));
   if (t.ov) BSB_CUDA(cudaFreeAsync(t.ov, s));
@@ -92,7 +94,9 @@ __global__ void bs_lookup_kernel(const uint8_t* __restrict__ slices, int64_t str
                                  const int64_t* __restrict__ rank_values,
                                  int64_t* __restrict__ out_values,
                                  int32_t* __restrict__ out_values32, int64_t n_rows,
-                                 unsigned int* __restrict__ err) {
+                                 unsigned int* __restrict__ err,
+                                 const uint32_t* __restrict__ gate, bool want) {
+  if (gate_closed(gate, want)) return;
   const int shift = 8 * K - width;
   bool oob = false;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -346,11 +350,7 @@ using namespace bsb;
 
 // Reads the device error word of a row-id lookup (synchronises) and maps it
 // to a status: an out-of-range id wins over an absent code.
-static int read_err(unsigned int* err, cudaStream_t s) {
-  unsigned int h = 0;
-  BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
-  BSB_CUDA(cudaFreeAsync(err, s));
-  BSB_CUDA(cudaStreamSynchronize(s));
+static int err_status(unsigned int h) {
   if (h & kErrIndex) {
     set_error_msg("row id out of range");
     return BSB_EINDEX;
@@ -362,41 +362,119 @@ static int read_err(unsigned int* err, cudaStream_t s) {
   return BSB_OK;
 }
 
+static int read_err(unsigned int* err, cudaStream_t s) {
+  unsigned int h = 0;
+  BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
+  BSB_CUDA(cudaFreeAsync(err, s));
+  BSB_CUDA(cudaStreamSynchronize(s));
+  return err_status(h);
+}
+
 static int alloc_err(unsigned int** err, cudaStream_t s) {
   BSB_CUDA(cudaMallocAsync(err, 4, s));
   BSB_CUDA(cudaMemsetAsync(*err, 0, 4, s));
   return BSB_OK;
 }
 
-template <bool PAIRS>
-static int bs_lookup_rows_impl(const bsb_byteslice* col, const void* rows, int64_t n_ids,
-                               uint64_t* out_codes, const int64_t* rank_values,
+// pairs NULL: the row-id list `rows` as given.  Else the bucket-ordered pairs;
+// with unsorted_dev (bsb_rows_bucket's verdict) both forms are launched and
+// the one the verdict rules out exits at once.
+// Scratch of the *_auto lookups: the pairs and the order verdict.
+struct AutoScratch {
+  uint64_t* pairs = nullptr;
+  uint32_t* unsorted = nullptr;
+};
+static bool auto_fits(int64_t n_ids, int64_t n_rows) {
+  return n_ids >= 2 && n_ids < (int64_t)UINT32_MAX && n_rows < (int64_t)UINT32_MAX;
+}
+// One allocation, one memset: pairs | verdict | error word.  (Forking the
+// pair path onto a side stream, so that an ascending list's exiting kernels
+// run beside its gather, measured no faster: the cost is host launch time.)
+static int auto_begin(AutoScratch& a, const int64_t* rows, int64_t n_ids, unsigned int** err,
+                      cudaStream_t s) {
+  BSB_CUDA(cudaMallocAsync(&a.pairs, (size_t)n_ids * 8 + 16, s));
+  a.unsorted = reinterpret_cast<uint32_t*>(a.pairs + n_ids);
+  if (!*err) {
+    *err = a.unsorted + 1;
+    BSB_CUDA(cudaMemsetAsync(a.unsorted, 0, 8, s));
+  } else {
+    BSB_CUDA(cudaMemsetAsync(a.unsorted, 0, 4, s));
+  }
+  if (n_ids >= 2) {
+    rows_order_check_launch(rows, n_ids, a.unsorted, s);
+    BSB_LAUNCH_CHECK();
+  }
+  return BSB_OK;
+}
+// err_dev NULL: the error word lives in the scratch; read it, then free
+static int auto_end(AutoScratch& a, unsigned int* err, bool own_err, cudaStream_t s) {
+  unsigned int h = 0;
+  if (own_err) BSB_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s));
+  BSB_CUDA(cudaFreeAsync(a.pairs, s));
+  if (!own_err) return BSB_OK;
+  BSB_CUDA(cudaStreamSynchronize(s));
+  return err_status(h);
+}
+
+static int bs_lookup_rows_impl(const bsb_byteslice* col, const int64_t* rows,
+                               const uint64_t* pairs, const uint32_t* unsorted_dev,
+                               int64_t n_ids, uint64_t* out_codes, const int64_t* rank_values,
                                int64_t* out_values, int32_t* out_values32, uint32_t* err_dev,
-                               void* stream) {
-  if (!col || n_ids < 0 || (n_ids > 0 && !rows)) return BSB_EINVAL;
+                               void* stream, bool automatic = false) {
+  if (!col || n_ids < 0 || (n_ids > 0 && !rows && !pairs)) return BSB_EINVAL;
+  if (pairs && unsorted_dev && !rows) return BSB_EINVAL;
   if (n_ids == 0) return BSB_OK;
   cudaStream_t s = as_stream(stream);
+  const cudaStream_t ps = s;
   unsigned int* err = err_dev;
-  if (!err) {
+  AutoScratch au;
+  automatic = automatic && auto_fits(n_ids, col->n_rows);
+  if (automatic) {
+    const int rc = auto_begin(au, rows, n_ids, &err, s);
+    if (rc) return rc;
+    pairs = au.pairs;
+    unsorted_dev = au.unsorted;
+  } else if (!err) {
     const int rc = alloc_err(&err, s);
     if (rc) return rc;
   }
-  PairOut t;
-  if (PAIRS) {
-    const int rc = pair_out_alloc(t, n_ids, out_codes, rank_values && out_values, out_values32, s);
+  const int g = grid_for_l((n_ids + kBsIds - 1) / kBsIds, 256);
+  if (!pairs || unsorted_dev) {
+    bs_lookup_kernel<false><<<g, 256, 0, s>>>(col->slices, col->stride, col->n_slices,
+                                              col->width_bits, rows, n_ids, out_codes,
+                                              rank_values, out_values, out_values32,
+                                              col->n_rows, err, pairs ? unsorted_dev : nullptr,
+                                              false);
+    BSB_LAUNCH_CHECK();
+  }
+  if (automatic) {
+    const int rc = rows_bucket_gated(rows, n_ids, col->n_rows, au.pairs, au.unsorted, ps);
     if (rc) return rc;
   }
-  bs_lookup_kernel<PAIRS><<<grid_for_l((n_ids + kBsIds - 1) / kBsIds, 256), 256, 0, s>>>(
-      col->slices, col->stride, col->n_slices, col->width_bits, rows, n_ids,
-      PAIRS ? t.oc : out_codes, rank_values, PAIRS ? t.ov : out_values,
-      PAIRS ? t.ov32 : out_values32, col->n_rows, err);
-  BSB_LAUNCH_CHECK();
-  if (PAIRS) {
-    const int rc = pair_out_scatter(t, static_cast<const uint64_t*>(rows), n_ids, out_codes,
-                                    out_values, out_values32, s);
+  if (pairs) {
+    PairOut t;
+    int rc = pair_out_alloc(t, n_ids, out_codes, rank_values && out_values, out_values32, ps);
+    if (rc) return rc;
+    bs_lookup_kernel<true><<<g, 256, 0, ps>>>(col->slices, col->stride, col->n_slices,
+                                              col->width_bits, pairs, n_ids, t.oc, rank_values,
+                                              t.ov, t.ov32, col->n_rows, err, unsorted_dev, true);
+    BSB_LAUNCH_CHECK();
+    rc = pair_out_scatter(t, pairs, n_ids, out_codes, out_values, out_values32, unsorted_dev,
+                          ps);
     if (rc) return rc;
   }
+  if (automatic) return auto_end(au, err, !err_dev, s);
   return err_dev ? BSB_OK : read_err(err, s);
+}
+
+extern "C" int bsb_byteslice_lookup_rows_auto(const bsb_byteslice* col, const int64_t* rows,
+                                              int64_t n_ids, uint64_t* out_codes,
+                                              const int64_t* rank_values, int64_t* out_values,
+                                              int32_t* out_values32, uint32_t* err_dev,
+                                              void* stream) {
+  if (!rows && n_ids > 0) return BSB_EINVAL;
+  return bs_lookup_rows_impl(col, rows, nullptr, nullptr, n_ids, out_codes, rank_values,
+                             out_values, out_values32, err_dev, stream, true);
 }
 
 extern "C" int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t* rows,
@@ -404,17 +482,19 @@ extern "C" int bsb_byteslice_lookup_rows(const bsb_byteslice* col, const int64_t
                                          const int64_t* rank_values, int64_t* out_values,
                                          int32_t* out_values32, uint32_t* err_dev,
                                          void* stream) {
-  return bs_lookup_rows_impl<false>(col, rows, n_ids, out_codes, rank_values, out_values,
-                                    out_values32, err_dev, stream);
+  return bs_lookup_rows_impl(col, rows, nullptr, nullptr, n_ids, out_codes, rank_values,
+                             out_values, out_values32, err_dev, stream);
 }
 
 extern "C" int bsb_byteslice_lookup_pairs(const bsb_byteslice* col, const uint64_t* pairs,
+                                          const int64_t* rows, const uint32_t* unsorted_dev,
                                           int64_t n_ids, uint64_t* out_codes,
                                           const int64_t* rank_values, int64_t* out_values,
                                           int32_t* out_values32, uint32_t* err_dev,
                                           void* stream) {
-  return bs_lookup_rows_impl<true>(col, pairs, n_ids, out_codes, rank_values, out_values,
-                                   out_values32, err_dev, stream);
+  if (!pairs) return BSB_EINVAL;
+  return bs_lookup_rows_impl(col, rows, pairs, unsorted_dev, n_ids, out_codes, rank_values,
+                             out_values, out_values32, err_dev, stream);
 }
 
 extern "C" int bsb_vbs_lookup_rows(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
@@ -806,8 +886,10 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
                                            const __grid_constant__ Decoder D,
                                            uint64_t* __restrict__ oc, int64_t* __restrict__ ov,
                                            int32_t* __restrict__ ov32,
-                                           unsigned int* __restrict__ err) {
+                                           unsigned int* __restrict__ err,
+                                           const uint32_t* __restrict__ gate, bool want) {
   __shared__ int64_t e1sm[256];
+  if (gate_closed(gate, want)) return;
   const int64_t* e1s = D.e1;
   if (D.kind == 3) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) e1sm[i] = __ldg(D.e1 + i);
@@ -980,64 +1062,95 @@ extern "C" int bsb_vbs_lookup_bits(const bsb_vbs* col, const uint32_t* words,
                                 n_out_dev, as_stream(stream));
 }
 
-template <bool PAIRS>
-static int vbs_lookup_rows_dec_impl(const bsb_vbs* col, const void* rows, int64_t n_ids,
-                                    const bsb_decode* dec, uint64_t* out_padded,
+// pairs / unsorted_dev: see bs_lookup_rows_impl
+static int vbs_lookup_rows_dec_impl(const bsb_vbs* col, const int64_t* rows,
+                                    const uint64_t* pairs, const uint32_t* unsorted_dev,
+                                    int64_t n_ids, const bsb_decode* dec, uint64_t* out_padded,
                                     int64_t* out_values, int32_t* out_values32,
-                                    uint32_t* err_dev, void* stream) {
-  if (!col || n_ids < 0 || (n_ids > 0 && !rows)) return BSB_EINVAL;
+                                    uint32_t* err_dev, void* stream, bool automatic = false) {
+  if (!col || n_ids < 0 || (n_ids > 0 && !rows && !pairs)) return BSB_EINVAL;
+  if (pairs && unsorted_dev && !rows) return BSB_EINVAL;
   if (dec && (dec->kind == 1 || dec->kind > 3)) return BSB_EINVAL;
+  if (col->deep_mode != BSB_DEEP_PACKED && col->deep_mode != BSB_DEEP_SLICED) return BSB_EINVAL;
   if (n_ids == 0) return BSB_OK;
   cudaStream_t s = as_stream(stream);
   Decoder D;
   fill_decoder(D, dec);
   VbsLookupDesc vd;
   fill_lookup_desc(vd, col);
+  const cudaStream_t ps = s;
   unsigned int* err = err_dev;
-  if (!err) {
+  AutoScratch au;
+  automatic = automatic && auto_fits(n_ids, col->n_rows);
+  if (automatic) {
+    const int rc = auto_begin(au, rows, n_ids, &err, s);
+    if (rc) return rc;
+    pairs = au.pairs;
+    unsorted_dev = au.unsorted;
+  } else if (!err) {
     BSB_CUDA(cudaMallocAsync(&err, 4, s));
     BSB_CUDA(cudaMemsetAsync(err, 0, 4, s));
   }
   const int g = grid_for_l((n_ids + kVbsIds - 1) / kVbsIds, 256);
-  PairOut t;
-  if (PAIRS) {
-    const int rc = pair_out_alloc(t, n_ids, out_padded, out_values, out_values32, s);
+  const bool sliced = col->deep_mode == BSB_DEEP_SLICED;
+  if (!pairs || unsorted_dev) {
+    const uint32_t* gate = pairs ? unsorted_dev : nullptr;
+    if (sliced)
+      vbs_lookup_rows_dec_kernel<BSB_DEEP_SLICED, false><<<g, 256, 0, s>>>(
+          vd, rows, n_ids, D, out_padded, out_values, out_values32, err, gate, false);
+    else
+      vbs_lookup_rows_dec_kernel<BSB_DEEP_PACKED, false><<<g, 256, 0, s>>>(
+          vd, rows, n_ids, D, out_padded, out_values, out_values32, err, gate, false);
+    BSB_LAUNCH_CHECK();
+  }
+  if (automatic) {
+    const int rc = rows_bucket_gated(rows, n_ids, col->n_rows, au.pairs, au.unsorted, ps);
     if (rc) return rc;
   }
-  switch (col->deep_mode) {
-#define BSB_ROWS_DEC(M)                                                                    \
-  case M:                                                                                  \
-    vbs_lookup_rows_dec_kernel<M, PAIRS><<<g, 256, 0, s>>>(                                \
-        vd, rows, n_ids, D, PAIRS ? t.oc : out_padded, PAIRS ? t.ov : out_values,          \
-        PAIRS ? t.ov32 : out_values32, err);                                               \
-    break;
-    BSB_ROWS_DEC(BSB_DEEP_PACKED)
-    BSB_ROWS_DEC(BSB_DEEP_SLICED)
-#undef BSB_ROWS_DEC
-    default: return BSB_EINVAL;
-  }
-  BSB_LAUNCH_CHECK();
-  if (PAIRS) {
-    const int rc = pair_out_scatter(t, static_cast<const uint64_t*>(rows), n_ids, out_padded,
-                                    out_values, out_values32, s);
+  if (pairs) {
+    PairOut t;
+    int rc = pair_out_alloc(t, n_ids, out_padded, out_values, out_values32, ps);
+    if (rc) return rc;
+    if (sliced)
+      vbs_lookup_rows_dec_kernel<BSB_DEEP_SLICED, true><<<g, 256, 0, ps>>>(
+          vd, pairs, n_ids, D, t.oc, t.ov, t.ov32, err, unsorted_dev, true);
+    else
+      vbs_lookup_rows_dec_kernel<BSB_DEEP_PACKED, true><<<g, 256, 0, ps>>>(
+          vd, pairs, n_ids, D, t.oc, t.ov, t.ov32, err, unsorted_dev, true);
+    BSB_LAUNCH_CHECK();
+    rc = pair_out_scatter(t, pairs, n_ids, out_padded, out_values, out_values32, unsorted_dev,
+                          ps);
     if (rc) return rc;
   }
+  if (automatic) return auto_end(au, err, !err_dev, s);
   if (err_dev) return BSB_OK;
   return read_err(err, s);
+}
+
+extern "C" int bsb_vbs_lookup_rows_dec_auto(const bsb_vbs* col, const int64_t* rows,
+                                            int64_t n_ids, const bsb_decode* dec,
+                                            uint64_t* out_padded, int64_t* out_values,
+                                            int32_t* out_values32, uint32_t* err_dev,
+                                            void* stream) {
+  if (!rows && n_ids > 0) return BSB_EINVAL;
+  return vbs_lookup_rows_dec_impl(col, rows, nullptr, nullptr, n_ids, dec, out_padded,
+                                  out_values, out_values32, err_dev, stream, true);
 }
 
 extern "C" int bsb_vbs_lookup_rows_dec(const bsb_vbs* col, const int64_t* rows, int64_t n_ids,
                                        const bsb_decode* dec, uint64_t* out_padded,
                                        int64_t* out_values, int32_t* out_values32,
                                        uint32_t* err_dev, void* stream) {
-  return vbs_lookup_rows_dec_impl<false>(col, rows, n_ids, dec, out_padded, out_values,
-                                         out_values32, err_dev, stream);
+  return vbs_lookup_rows_dec_impl(col, rows, nullptr, nullptr, n_ids, dec, out_padded,
+                                  out_values, out_values32, err_dev, stream);
 }
 
-extern "C" int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs, int64_t n_ids,
-                                        const bsb_decode* dec, uint64_t* out_padded,
-                                        int64_t* out_values, int32_t* out_values32,
-                                        uint32_t* err_dev, void* stream) {
-  return vbs_lookup_rows_dec_impl<true>(col, pairs, n_ids, dec, out_padded, out_values,
-                                        out_values32, err_dev, stream);
+extern "C" int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs,
+                                        const int64_t* rows, const uint32_t* unsorted_dev,
+                                        int64_t n_ids, const bsb_decode* dec,
+                                        uint64_t* out_padded, int64_t* out_values,
+                                        int32_t* out_values32, uint32_t* err_dev, void* stream) {
+  if (!pairs) return BSB_EINVAL;
+  return vbs_lookup_rows_dec_impl(col, rows, pairs, unsorted_dev, n_ids, dec, out_padded,
+                                  out_values, out_values32, err_dev, stream);
 }

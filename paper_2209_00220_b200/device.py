@@ -123,30 +123,50 @@ BUCKET_ROWS_MIN = 1 << 24
 _PAIR_LIMIT = (1 << 32) - 1
 
 
-def gather_pairs(rows: torch.Tensor, n_rows: int, order: str = "auto"):
-    """Bucket-ordered row | position << 32 pairs for the *_lookup_pairs entry
-    points, or None when the list should be gathered as given (order="keep",
-    a short list, a small column, an ascending list, or sizes the 32-bit
-    pairs cannot hold).  order="bucket" forces the pairs (no order check, no
-    synchronisation)."""
-    import ctypes
+def auto_gather(n_ids: int, n_rows: int) -> bool:
+    """Whether order="auto" takes the *_lookup_rows_auto entry points (order
+    check and bucket partition chosen on the device): long lists over big
+    columns whose sizes fit the 32-bit pairs."""
+    return (BUCKET_GATHER_MIN <= n_ids < _PAIR_LIMIT and BUCKET_ROWS_MIN <= n_rows < _PAIR_LIMIT)
 
+
+def gather_pairs(rows: torch.Tensor, n_rows: int, check: bool = False):
+    """(pairs, unsorted) for the *_lookup_pairs entry points: pairs =
+    bucket-ordered row | position << 32 words (bsb_rows_bucket); unsorted =
+    None, or with check=True the device word holding the sampled order
+    check's verdict (0: the list looks ascending and pairs[] was not written;
+    the pair lookups then gather the list as given).  One list can serve
+    several columns of the same table.  Never synchronises."""
+    n = rows.numel()
+    if n >= _PAIR_LIMIT or n_rows >= _PAIR_LIMIT:
+        raise ValueError("bucket-ordered pairs hold 32-bit rows and positions")
+    lib = _lib.load()
+    pairs = torch.empty(n, dtype=torch.int64, device=rows.device)
+    uns = torch.empty(1, dtype=torch.int32, device=rows.device) if check else None
+    _lib.check(lib.bsb_rows_bucket(rows.data_ptr(), n, int(n_rows), pairs.data_ptr(),
+                                   _lib.ptr(uns), stream()), "gather_pairs")
+    return pairs, uns
+
+
+def row_gather_plan(rows: torch.Tensor, n_rows: int, order: str, auto_fn, pairs_fn, rows_fn):
+    """(fn, ids, perm) for a row-id lookup under `order`: fn(desc, ids, n, ...)
+    is the C entry point to call with the remaining arguments.  "auto": the
+    *_auto entry for long lists over big columns, else as given; "bucket":
+    bucket-ordered pairs (no order check); "sort": the sort + scatter-back
+    path (gather_order); "keep": as given."""
     if order not in ("auto", "sort", "bucket", "keep"):
         raise ValueError(f"unknown order {order!r}")
     n = rows.numel()
-    if order == "keep" or n == 0 or n >= _PAIR_LIMIT or n_rows >= _PAIR_LIMIT:
-        return None
-    if order != "bucket" and n < BUCKET_GATHER_MIN:
-        return None
-    if order == "auto" and n_rows < BUCKET_ROWS_MIN:
-        return None
-    lib = _lib.load()
-    pairs = torch.empty(n, dtype=torch.int64, device=rows.device)
-    was = ctypes.c_int32(0)
-    _lib.check(lib.bsb_rows_bucket(rows.data_ptr(), n, int(n_rows), pairs.data_ptr(),
-                                   None if order == "bucket" else ctypes.byref(was), stream()),
-               "gather_pairs")
-    return None if was.value else pairs
+    if order == "auto" and auto_gather(n, n_rows):
+        return auto_fn, rows, None
+    if order == "bucket" and 0 < n < _PAIR_LIMIT and n_rows < _PAIR_LIMIT:
+        pairs, _ = gather_pairs(rows, n_rows)
+
+        def fn(desc, ids, *rest):
+            return pairs_fn(desc, ids, None, None, *rest)
+        return fn, pairs, None
+    g, perm = gather_order(rows, n_rows, "sort" if order == "sort" else "keep")
+    return rows_fn, g, perm
 
 
 def scatter_back(out: torch.Tensor, perm) -> torch.Tensor:

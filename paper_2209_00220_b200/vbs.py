@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .bitvector import DeviceBitVector, as_device_bits
-from .device import (device, gather_order, gather_pairs, host_u32, host_u64, scatter_back, stream, to_dev_i64,
+from .device import (auto_gather, device, gather_order, host_u32, row_gather_plan, host_u64, scatter_back, stream, to_dev_i64,
                      to_dev_u8, to_dev_u64)
 from .predicate import DEFAULT_LANES, LaneConfig, Op, ResolvedPredicate
 from .stats import LazyScanStats, LookupStats, ScanStats
@@ -286,13 +286,12 @@ def lookup_vbs_rows(col: VbsColumn, rows, sorted_padded=None, dict_values=None,
     lc = None if level_counts is None else level_counts.data_ptr()
     if sorted_padded is None:
         out = torch.empty(n, dtype=torch.int64, device=rows.device)
-        pairs = None
-        if lc is None and order != "sort":
-            pairs = gather_pairs(rows, col.n_rows, order)
-        if pairs is not None:
-            _lib.check(lib.bsb_vbs_lookup_pairs_dec(col.desc_ref, pairs.data_ptr(), n, None,
-                                                    out.data_ptr(), None, None, _lib.ptr(err),
-                                                    stream()), "lookup_vbs")
+        if lc is None and order != "sort" and (order == "bucket" or (
+                order == "auto" and auto_gather(n, col.n_rows))):
+            fn, g, _ = row_gather_plan(rows, col.n_rows, order, lib.bsb_vbs_lookup_rows_dec_auto,
+                                       lib.bsb_vbs_lookup_pairs_dec, lib.bsb_vbs_lookup_rows_dec)
+            _lib.check(fn(col.desc_ref, g.data_ptr(), n, None, out.data_ptr(), None, None,
+                          _lib.ptr(err), stream()), "lookup_vbs")
             return out
         g, perm = gather_order(rows, col.n_rows, _vbs_order(col, order) if order in
                                ("auto", "sort") else "keep")
@@ -319,12 +318,8 @@ def lookup_vbs_rows_dec(col: VbsColumn, rows, decoder, out_dtype=torch.int64,
     lib = _lib.load()
     rows = to_dev_i64(rows)
     n = rows.numel()
-    pairs = None if order == "sort" else gather_pairs(rows, col.n_rows, order)
-    if pairs is not None:
-        fn, g, perm = lib.bsb_vbs_lookup_pairs_dec, pairs, None
-    else:
-        fn = lib.bsb_vbs_lookup_rows_dec
-        g, perm = gather_order(rows, col.n_rows, order if order == "sort" else "keep")
+    fn, g, perm = row_gather_plan(rows, col.n_rows, order, lib.bsb_vbs_lookup_rows_dec_auto,
+                                  lib.bsb_vbs_lookup_pairs_dec, lib.bsb_vbs_lookup_rows_dec)
     out = torch.empty(n, dtype=out_dtype, device=rows.device)
     p64 = out.data_ptr() if out_dtype == torch.int64 else None
     p32 = out.data_ptr() if out_dtype == torch.int32 else None

@@ -270,7 +270,8 @@ def test_row_lookups_bucket_pairs(n):
     import ctypes
 
     from paper_2209_00220_b200 import _lib
-    from paper_2209_00220_b200.device import stream
+    from paper_2209_00220_b200.device import (BUCKET_GATHER_MIN, BUCKET_ROWS_MIN, auto_gather,
+                                              gather_pairs, stream)
     rng = np.random.default_rng(n)
     m = 200_003 if n < (1 << 25) else 1_000_003
     ids = rng.integers(0, n, size=m)
@@ -311,6 +312,21 @@ def test_row_lookups_bucket_pairs(n):
     srt = np.sort(ids)
     got = B.lookup_byteslice_rows(col, torch.from_numpy(srt), order="auto").cpu().numpy()
     assert np.array_equal(got.view(np.uint64), codes[srt])
+    got = B.lookup_vbs_rows_dec(vcol, torch.from_numpy(srt), d.dev_decoder, out_dtype=torch.int32,
+                                order="auto").cpu().numpy()
+    assert np.array_equal(got, vals[srt].astype(np.int32))
+    for lst, want in ((ids, 1), (srt, 0)):  # the device-side verdict gates the pair lookups
+        tl = torch.from_numpy(lst).cuda()
+        pp, uns = gather_pairs(tl, n, check=True)
+        assert int(uns.item()) == want
+        o32 = torch.empty(m, dtype=torch.int32, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(_lib.load().bsb_byteslice_lookup_pairs(
+            col.desc_ref, pp.data_ptr(), tl.data_ptr(), uns.data_ptr(), m, None, None, None,
+            o32.data_ptr(), err.data_ptr(), stream()), "lookup_pairs")
+        assert np.array_equal(o32.cpu().numpy(), codes[lst].astype(np.int32))
+        assert int(err.item()) == 0
+    assert auto_gather(m, n) == (m >= BUCKET_GATHER_MIN and n >= BUCKET_ROWS_MIN)
     # bad ids: IndexError / the async error word, through the pairs as well
     for bad in (n, -1, 1 << 40):
         ids2 = ids.copy()

@@ -64,11 +64,11 @@ def main():
         lib.bsb_rows_bucket(ids.data_ptr(), m, n, pairs.data_ptr(), None, s)
 
     def bs_pairs():
-        lib.bsb_byteslice_lookup_pairs(col_b.desc_ref, pairs.data_ptr(), m, None, None, None,
+        lib.bsb_byteslice_lookup_pairs(col_b.desc_ref, pairs.data_ptr(), None, None, m, None, None, None,
                                        o32.data_ptr(), err.data_ptr(), s)
 
     def vbs_pairs():
-        lib.bsb_vbs_lookup_pairs_dec(col_v.desc_ref, pairs.data_ptr(), m, ctypes.byref(dec), None,
+        lib.bsb_vbs_lookup_pairs_dec(col_v.desc_ref, pairs.data_ptr(), None, None, m, ctypes.byref(dec), None,
                                      None, o32.data_ptr(), err.data_ptr(), s)
 
     def bs_rows(t):
@@ -81,8 +81,9 @@ def main():
                                                    err.data_ptr(), s)
 
     print(f"rows 2^{log2n}, ids 2^{log2n - 4}; times in us")
-    print("direct  bs unsorted %.1f  sorted %.1f | vbs unsorted %.1f sorted %.1f" % (
-        timed(bs_rows(ids)), timed(bs_rows(srt)), timed(vbs_rows(ids)), timed(vbs_rows(srt))))
+    if "--nodirect" not in sys.argv:
+      print("direct  bs unsorted %.1f  sorted %.1f | vbs unsorted %.1f sorted %.1f" % (
+          timed(bs_rows(ids)), timed(bs_rows(srt)), timed(vbs_rows(ids)), timed(vbs_rows(srt))))
     for bits in bits_list:
         lib.bsb_tune(b"pair_bits", bits)
         tb = timed(bucket)
