@@ -712,17 +712,22 @@ __device__ __forceinline__ uint64_t vbs_row_code(const VbsLookupDesc& d, int64_t
 // (ByteSlice: the K plane sectors; PP-VBS: the BS_1 sector) into the warp's
 // shared-memory stage, all in flight together, plus (PP-VBS) its existence
 // words and level-2 directory entry.  The lane then lists its block's set
-// rows as records (row in tile | code length - 1 | deep-row offset), the
+// rows as 16-bit records (row in tile | code length - 1), the
 // length coming from bit-sliced counts of the nested existence words.  Lane
 // k then assembles listed rows k, k+32, ... (kRowsPerLane at a time, their
 // deep-byte loads in flight together), decodes them (PPE first-level table
 // in shared memory) and writes them contiguously.  A bad code sets *err
 // (UINT64_MAX when err is the output count).
 constexpr int kBitsThreads = 128;
+__device__ uint32_t g_dense_rows = 96;  // selected rows per tile from which deep loads allocate in L1
+void set_dense_rows(int64_t v) {
+  const uint32_t h = v < 0 ? 96u : (uint32_t)v;
+  cudaMemcpyToSymbol(g_dense_rows, &h, 4);
+}
 
-// per-warp shared memory: row records (u32 PP-VBS, u16 ByteSlice) + stage
+// per-warp shared memory: row records (u16) + stage (+ PP-VBS existence words, directory)
 __host__ __device__ constexpr int bits_stage_bytes(bool vbs, int K) {
-  return vbs ? 4096 + 1024 + 128 * (K > 1 ? K - 1 : 0) + 256 : 2048 + 1024 * K;
+  return vbs ? 2048 + 1024 + 128 * (K > 1 ? K - 1 : 0) + 256 : 2048 + 1024 * K;
 }
 
 __device__ __forceinline__ void sts256(uint8_t* dst, const uint32_t (&v)[8]) {
@@ -748,7 +753,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   const int KL = KT > 0 ? KT : (VBS ? vd.K : K);
   const int KD = KL > 1 ? KL - 1 : 0;
   uint8_t* wbase = dsm + (DK == 3 ? 2048 : 0) + (threadIdx.x >> 5) * bits_stage_bytes(VBS, KL);
-  using Rec = typename std::conditional<VBS, uint32_t, uint16_t>::type;
+  using Rec = uint16_t;
   constexpr int kRowsPerLane = 1;  // rows assembled per lane at a time (bit-plane sectors: 8 registers per level in flight)
   Rec* idx = reinterpret_cast<Rec*>(wbase);
   uint8_t* stage = wbase + 1024 * sizeof(Rec);
@@ -786,9 +791,10 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           uint32_t v[8];
           ldg256_free(vd.bs1 + blk * 32, v);
           sts256(stage + lane * 32, v);
+          if (KL >= 2) smeta[lane] = m[2];  // the rows' deep-row offsets: popc(M_2 & below)
           if (MODE == BSB_DEEP_PACKED) {
 #pragma unroll
-            for (int j = 2; j <= kMaxLevels; ++j)
+            for (int j = 3; j <= kMaxLevels; ++j)
               if (j <= KL) smeta[(j - 2) * 32 + lane] = m[j];
           }
         }
@@ -817,12 +823,13 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           if (VBS) {
             const uint32_t lm1 = ((c0 >> bit) & 1u) | (((c1 >> bit) & 1u) << 1) |
                                  (((c2 >> bit) & 1u) << 2);
-            rec |= (lm1 << 10) | ((uint32_t)__popc(m[2] & ((1u << bit) - 1u)) << 13);
+            rec |= lm1 << 10;
           }
           idx[o++] = (Rec)rec;
         }
       }
       __syncwarp();
+      const bool dense = total >= g_dense_rows;
       for (uint32_t k0 = lane; k0 < total; k0 += 32 * kRowsPerLane) {
         uint64_t code[kRowsPerLane], pad[kRowsPerLane];
         int len[kRowsPerLane];
@@ -837,15 +844,19 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           if (VBS) {
             len[u] = on[u] ? 1 + (int)((r >> 10) & 7u) : 1;
             uint64_t cd = bp_row_byte_smem(stage + bl * 32, lr);
-            const int64_t q = MODE == BSB_DEEP_PACKED ? 0 : sdir[bl] + (r >> 13);
-            const int64_t blkr = t * 32 + bl;
             const uint32_t below = (1u << lr) - 1u;
+            const int64_t q = MODE == BSB_DEEP_PACKED || len[u] < 2
+                                  ? 0 : sdir[bl] + __popc(smeta[bl] & below);
+            const int64_t blkr = t * 32 + bl;
 #pragma unroll
             for (int j = 2; j <= kMaxLevels; ++j) {
               if (j <= KL && j <= len[u]) {
                 uint32_t byte;
                 if (MODE == BSB_DEEP_SLICED) {
-                  byte = bp_row_byte(vd.deep[j - 1] + (q >> 5) * 32, (int)(q & 31));
+                  // a dense tile's rows share deep sectors: let L1 keep them
+                  const uint8_t* sp = vd.deep[j - 1] + (q >> 5) * 32;
+                  byte = dense ? bp_row_byte_l1(sp, (int)(q & 31))
+                               : bp_row_byte(sp, (int)(q & 31));
                 } else {
                   byte = __ldg(vd.deep[j - 1] + (__ldg(vd.dir[j - 1] + blkr) +
                                                  __popc(smeta[(j - 2) * 32 + bl] & below)));

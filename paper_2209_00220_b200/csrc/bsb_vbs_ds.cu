@@ -831,6 +831,7 @@ void set_scan_nomemset(int64_t v); // bsb_scan.cu
 void set_bs_small(int64_t v);      // bsb_scan.cu
 void set_pdl(int64_t v);           // bsb_scan.cu
 void set_pair_bits(int64_t v);     // bsb_gather.cu
+void set_dense_rows(int64_t v);    // bsb_lookup.cu
 }
 
 extern "C" int bsb_tune(const char* key, int64_t value) {
@@ -857,6 +858,10 @@ extern "C" int bsb_tune(const char* key, int64_t value) {
   }
   if (std::strcmp(key, "ctas_per_sm") == 0) {  // persistent-grid cap (0 = none)
     bsb::set_ctas_per_sm_cap((int)value);
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "dense_rows") == 0) {  // fused PP-VBS lookup: L1-allocating deep loads from
+    bsb::set_dense_rows(value);               // this many selected rows per tile
     return BSB_OK;
   }
   if (std::strcmp(key, "pair_bits") == 0) {  // row buckets of bsb_rows_bucket (2^bits)
