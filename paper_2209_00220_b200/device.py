@@ -118,7 +118,10 @@ def gather_order(rows: torch.Tensor, n_rows: int, order: str = "auto"):
 
 # Row-id gathers over big columns: lists at least this long are partitioned
 # into bucket-ordered (row, position) pairs (bsb_rows_bucket) unless ascending.
-BUCKET_GATHER_MIN = 1 << 18
+# Measured crossover on a 2^28-row, 3-slice column (tools/auto_probe.py):
+# 2^20 ids 72 us as given vs 118 us bucketed, 2^22 ids 256 vs 232, 2^24 ids
+# 1000 vs 620.
+BUCKET_GATHER_MIN = 1 << 22
 BUCKET_ROWS_MIN = 1 << 24
 _PAIR_LIMIT = (1 << 32) - 1
 

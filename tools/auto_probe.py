@@ -8,7 +8,8 @@ from paper_2209_00220_b200.byteslice import build_byteslice
 from paper_2209_00220_b200.device import stream
 
 lib = _lib.load()
-n, m = 1 << 28, 1 << 24
+n = 1 << 28
+m = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 24)
 codes = torch.from_numpy(np.random.default_rng(3).integers(0, 1 << 24, n, dtype=np.int64)).cuda()
 col = build_byteslice(codes, 24)
 del codes
@@ -23,8 +24,6 @@ for name, t in (("sorted", srt), ("unsorted", ids)):
         ("auto       ", lambda: lib.bsb_byteslice_lookup_rows_auto(col.desc_ref, t.data_ptr(), m, None, None, None, o32.data_ptr(), err.data_ptr(), s)),
         ("auto + sync", lambda: lib.bsb_byteslice_lookup_rows_auto(col.desc_ref, t.data_ptr(), m, None, None, None, o32.data_ptr(), None, s)),
     ):
-        if name == "unsorted" and label.startswith("rows"):
-            continue
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
