@@ -397,19 +397,23 @@ __device__ __forceinline__ void conj_level(const uint32_t (&w)[8], const BsConjA
   else
     bs_level<false>(w, a.A[p], a.B[p], j, s);
 }
+template <bool BANY>
 __device__ __forceinline__ bool conj_tied(const BsConjArgs& a, int p, const BsState& s) {
-  return a.between[p] ? ((s.zeqA | s.zeqB) != 0) : (s.zeqA != 0);
+  return BANY && a.between[p] ? ((s.zeqA | s.zeqB) != 0) : (s.zeqA != 0);
 }
+template <bool BANY>
 __device__ __forceinline__ uint32_t conj_result(const BsConjArgs& a, int p, const BsState& s) {
-  return a.between[p] ? s.valid & (s.zgtA | s.zeqA) & ~s.zgtB
-                      : finalize_op(a.A[p].op, s.zgtA, s.zeqA, s.valid);
+  return BANY && a.between[p] ? s.valid & (s.zgtA | s.zeqA) & ~s.zgtB
+                              : finalize_op(a.A[p].op, s.zgtA, s.zeqA, s.valid);
 }
 
 // Two-stage pipeline per warp as in bs_scan_kernel: tile X's level-1
 // sectors come from the TMA-filled stage and its level-2 loads are issued;
 // tile Y (the previous one) consumes its level-2 sectors, runs any deeper
 // level, ANDs the NP results and writes the word.
-template <int NP, bool MASKED>
+// BANY false: no predicate of the group is a BETWEEN (the second leg's state
+// and compares drop out at compile time).
+template <int NP, bool MASKED, bool BANY>
 __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_constant__ BsConjArgs a) {
   constexpr int kW = kScanThreads / 32;
   __shared__ __align__(128) uint8_t sbuf[kW][2][NP][1024];
@@ -460,8 +464,8 @@ __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_c
         sX[p].zgtA = 0;
         sX[p].zeqA = valid;
         sX[p].zgtB = 0;
-        sX[p].zeqB = valid;
-        conj_level<true>(w, a, p, 0, sX[p]);
+        sX[p].zeqB = BANY ? valid : 0u;
+        conj_level<BANY>(w, a, p, 0, sX[p]);
       }
       __syncwarp();  // every lane has read this stage: refill it two tiles ahead
       if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -469,21 +473,21 @@ __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_c
       st ^= 1;
 #pragma unroll
       for (int p = 0; p < NP; ++p)
-        if (a.c[p].K >= 2 && conj_tied(a, p, sX[p]))
+        if (a.c[p].K >= 2 && conj_tied<BANY>(a, p, sX[p]))
           ldg256_sparse(a.c[p].slices + a.c[p].stride + b * 32, w2X[p]);
     }
     if (tY >= 0) {
       const int64_t b = tY * 32 + lane;
 #pragma unroll
       for (int p = 0; p < NP; ++p)
-        if (a.c[p].K >= 2 && conj_tied(a, p, sY[p])) conj_level<true>(w2Y[p], a, p, 1, sY[p]);
+        if (a.c[p].K >= 2 && conj_tied<BANY>(a, p, sY[p])) conj_level<BANY>(w2Y[p], a, p, 1, sY[p]);
 #pragma unroll
       for (int j = 2; j < kMaxLevels; ++j) {
         bool act[NP];
         bool any = false;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          act[p] = j < a.c[p].K && conj_tied(a, p, sY[p]);
+          act[p] = j < a.c[p].K && conj_tied<BANY>(a, p, sY[p]);
           any |= act[p];
         }
         if (!__any_sync(kFull, any)) break;
@@ -492,12 +496,12 @@ __global__ void __launch_bounds__(kScanThreads, 3) bs_conj_kernel(const __grid_c
           if (!act[p]) continue;
           uint32_t w[8];
           ldg256_sparse(a.c[p].slices + (int64_t)j * a.c[p].stride + b * 32, w);
-          conj_level<true>(w, a, p, j, sY[p]);
+          conj_level<BANY>(w, a, p, j, sY[p]);
         }
       }
       uint32_t res = sY[0].valid;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) res &= conj_result(a, p, sY[p]);
+      for (int p = 0; p < NP; ++p) res &= conj_result<BANY>(a, p, sY[p]);
       if (b < a.nb) a.out[b] = res;
       cnt += __popc(res);
     }
@@ -868,18 +872,21 @@ static int bs_conj2(const bsb_byteslice* c0, const bsb_pred* p0, const bsb_bytes
   a.out = out;
   a.count = reinterpret_cast<unsigned long long*>(count);
   BSB_CUDA(cudaMemsetAsync(count, 0, sizeof(uint64_t), s));
+  const bool bany = a.between[0] || a.between[1];
   auto go = [&](auto kern) -> int {
-    static bool carved[2] = {false, false};
-    if (!carved[mask != nullptr]) {
+    static bool carved[4] = {false, false, false, false};
+    const int ki = (mask != nullptr) + 2 * bany;
+    if (!carved[ki]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      carved[mask != nullptr] = true;
+      carved[ki] = true;
     }
     const int grid = persistent_grid(kern, kScanThreads, kScanThreads / 32, a.ntiles);
     kern<<<grid, kScanThreads, 0, s>>>(a);
     BSB_LAUNCH_CHECK();
     return BSB_OK;
   };
-  return mask ? go(bs_conj_kernel<2, true>) : go(bs_conj_kernel<2, false>);
+  if (bany) return mask ? go(bs_conj_kernel<2, true, true>) : go(bs_conj_kernel<2, false, true>);
+  return mask ? go(bs_conj_kernel<2, true, false>) : go(bs_conj_kernel<2, false, false>);
 }
 
 static int g_stats_rows = 0;  // bsb_tune("stats_rows"): PP-VBS stats via the row kernel
