@@ -339,6 +339,34 @@ def test_row_lookups_bucket_pairs(n):
         assert int(err.item()) & _lib.ERR_INDEX
 
 
+def test_row_lookup_auto_is_graph_capturable():
+    """The _auto row-id lookup (order verdict on the device, both gathers
+    gated on it, no host synchronisation with an error word) captured once as
+    a CUDA graph: replays over new random lists and over an ascending one
+    return codes[ids] each time."""
+    n, m = (1 << 25) + 777, (1 << 22) + 5
+    rng = np.random.default_rng(1)
+    codes = rng.integers(0, 1 << 20, size=n, dtype=np.uint64)
+    col = B.build_byteslice(codes, 20)
+    t = torch.from_numpy(rng.integers(0, n, size=m)).cuda()
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        B.lookup_byteslice_rows(col, t, out_dtype=torch.int32, err=err)  # attributes, pools
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            out = B.lookup_byteslice_rows(col, t, out_dtype=torch.int32, err=err)
+        for rep in range(3):
+            t.copy_(torch.from_numpy(rng.integers(0, n, size=m)) if rep < 2
+                    else torch.sort(t).values)
+            g.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(),
+                                  codes[t.cpu().numpy()].astype(np.int32)), rep
+    assert int(err.item()) == 0
+
+
 def test_byteslice_errors():
     with pytest.raises(ValueError):
         B.build_byteslice([], 8)
