@@ -151,7 +151,10 @@ const char* bsb_version(void);
  * bsb_conj_scan), "stats_rows" (1: PP-VBS ScanStats through the
  * row-parallel kernel instead of the deep-row-space one), "ctas_per_sm"
  * (cap on the CTAs per SM of the persistent scan kernels, 0 = none: room for
- * a kernel of another stream; measured slower).  Unknown key: BSB_EINVAL. */
+ * a kernel of another stream; measured slower), "pair_bits" (row-bucket bits
+ * of bsb_rows_bucket, 1..13), "dense_rows" (fused PP-VBS bitvector lookup:
+ * selected rows per 1024-row tile from which deep-sector loads allocate in
+ * L1; default 96).  Unknown key: BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */
