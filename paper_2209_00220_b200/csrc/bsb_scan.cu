@@ -3,6 +3,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <atomic>
+
 #include "bsb_scan_impl.cuh"
 
 namespace bsb {
@@ -23,7 +25,27 @@ struct ScanArgs {
   int8_t* depth;
   int32_t skipped_slot;
   int32_t depth_max;  // STATS: 1 = depth[b] = max(depth[b], d) (second BETWEEN leg)
+  // bs_scan_small_kernel: count accumulator | arrivals << 48 of this call (count_slot());
+  // the last CTA stores the total into *count, so no memset node precedes
+  // the kernel
+  unsigned long long* slot;
 };
+
+// Per-call count slots of the small-column scan: zero at load time, and the
+// kernel that used a slot leaves it zero again, so a call needs no memset.
+// A slot is reused only after kCountSlots later calls (a graph node keeps
+// its slot: replays of one graph are serialised by CUDA).
+constexpr int kCountSlots = 1 << 16;
+__device__ unsigned long long g_count_slots[kCountSlots];
+static unsigned long long* count_slot() {
+  static unsigned long long* base = [] {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_count_slots);
+    return static_cast<unsigned long long*>(p);
+  }();
+  static std::atomic<uint32_t> next{0};
+  return base ? base + (size_t)(next.fetch_add(1) % kCountSlots) : nullptr;
+}
 
 template <bool STATS>
 __device__ __forceinline__ void flush_stats(const ScanArgs& a, StatAcc& st) {
@@ -363,7 +385,27 @@ __global__ void __launch_bounds__(kScanThreads, 4) bs_scan_small_kernel(const __
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
-  if (lane == 0 && cnt && a.count) atomicAdd(a.count, cnt);
+  if (!a.count) return;
+  if (!a.slot) {  // count zeroed by the caller's memset
+    if (lane == 0 && cnt) atomicAdd(a.count, cnt);
+    return;
+  }
+  // count without a memset node: one atomicAdd per CTA carries its count (low
+  // 48 bits) and its arrival (bit 48 up); the CTA that sees every other
+  // arrival stores the total and leaves the slot zero
+  __shared__ unsigned long long wcnt[kScanThreads / 32];
+  if (lane == 0) wcnt[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+#pragma unroll
+    for (int q = 0; q < kScanThreads / 32; ++q) c += wcnt[q];
+    const unsigned long long old = atomicAdd(a.slot, c + (1ull << 48));
+    if ((old >> 48) == gridDim.x - 1) {
+      *a.count = (old & ((1ull << 48) - 1)) + c;
+      atomicExch(a.slot, 0ull);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -649,10 +691,13 @@ template <int LAYOUT>
 static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_t s) {
   const bool between = p->op == BSB_BETWEEN;
   const bool stats = a.stats != nullptr;
-  if (a.count && !g_scan_nomemset) BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
+  const bool small = !stats && LAYOUT == BSB_LAYOUT_BYTESLICE && !a.mask && small_bs_ok(a.ntiles);
+  if (small && a.count) a.slot = count_slot();
+  if (a.count && !a.slot && !g_scan_nomemset)
+    BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
     if (LAYOUT == BSB_LAYOUT_BYTESLICE) {
-      if (!a.mask && small_bs_ok(a.ntiles)) {
+      if (small) {
         constexpr int T = 4;
         const int64_t warps = (a.ntiles + T - 1) / T;
         const int grid = (int)((warps + kScanThreads / 32 - 1) / (kScanThreads / 32));
