@@ -154,7 +154,11 @@ const char* bsb_version(void);
  * a kernel of another stream; measured slower), "pair_bits" (row-bucket bits
  * of bsb_rows_bucket, 1..13), "dense_rows" (fused PP-VBS bitvector lookup:
  * selected rows per 1024-row tile from which deep-sector loads allocate in
- * L1; default 96).  Unknown key: BSB_EINVAL. */
+ * L1; default 96), "coop_tiles" (fused bitvector lookups of columns of at
+ * most this many 1024-row tiles run as ONE cooperative kernel -- per-warp
+ * tile runs, totals exchanged across a grid barrier -- instead of tile
+ * popcount + scan + lookup; default 2^14, 0 = never).  Unknown key:
+ * BSB_EINVAL. */
 int bsb_tune(const char* key, int64_t value);
 const char* bsb_last_error(void);
 /* Padded plane size for n rows (multiple of BSB_TILE_ROWS). */

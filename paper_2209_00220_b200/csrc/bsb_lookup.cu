@@ -1,5 +1,6 @@
 // bsb_lookup.cu -- row lookups (ByteSlice / PP-VBS), decode, bitvector
 // compaction and word-level bitvector algebra.
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 
 #include <cstdlib>
@@ -743,8 +744,9 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
     const int64_t* __restrict__ tile_incl, const __grid_constant__ Decoder D,
     uint64_t* __restrict__ oc, int64_t* __restrict__ ov, int32_t* __restrict__ ov32,
-    unsigned long long* __restrict__ err) {
+    unsigned long long* __restrict__ err, long long* __restrict__ cta_tot) {
   extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ long long s_wtot[kBitsThreads / 32 + 1];
   int64_t* e1s = reinterpret_cast<int64_t*>(dsm);  // DK == 3: first-level PPE table
   if (DK == 3) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) e1s[i] = __ldg(D.e1 + i);
@@ -764,12 +766,58 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int shift = VBS ? 0 : 8 * K - width;
   bool bad = false;
-  int64_t t = warp;
+  // Tile order.  cta_tot NULL: tiles round-robin over the warps, the selected
+  // rows before a tile come from tile_incl (tile popcount + scan kernels).
+  // cta_tot given (small columns, cooperative launch): every warp owns a
+  // contiguous run of tiles; the warps count their runs, the CTAs exchange
+  // totals across one grid barrier, and the running position is carried
+  // through the run -- the whole fused lookup is one kernel.
+  int64_t t = warp, t_end = ntiles, step = nwarps, running = 0;
+  if (cta_tot) {
+    const int wq = threadIdx.x >> 5;
+    const int64_t per_warp = (ntiles + nwarps - 1) / nwarps;
+    t = warp * per_warp;
+    t_end = t + per_warp < ntiles ? t + per_warp : ntiles;
+    step = 1;
+    uint32_t c1 = 0;
+    for (int64_t q = t; q < t_end; ++q)
+      if (q * 32 + lane < nb) c1 += __popc(__ldg(words + q * 32 + lane));
+    c1 = __reduce_add_sync(kFull, c1);
+    if (lane == 0) s_wtot[wq] = c1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long sum = 0;
+      for (int q = 0; q < kBitsThreads / 32; ++q) sum += s_wtot[q];
+      cta_tot[blockIdx.x] = sum;
+      if (blockIdx.x == 0) *err = 0ull;  // the count (atomicMax below; ~0 after a bad code)
+    }
+    cooperative_groups::this_grid().sync();
+    if (wq == 0) {
+      long long before = 0, grand = 0;
+      for (unsigned i = lane; i < gridDim.x; i += 32) {
+        const long long v = __ldcg(cta_tot + i);
+        grand += v;
+        if (i < blockIdx.x) before += v;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        before += __shfl_xor_sync(kFull, before, d);
+        grand += __shfl_xor_sync(kFull, grand, d);
+      }
+      if (lane == 0) {
+        s_wtot[kBitsThreads / 32] = before;
+        if (blockIdx.x == 0) atomicMax(err, (unsigned long long)grand);
+      }
+    }
+    __syncthreads();
+    running = s_wtot[kBitsThreads / 32];
+    for (int q = 0; q < wq; ++q) running += s_wtot[q];
+  }
   uint32_t w = 0;
-  if (t < ntiles) w = (t * 32 + lane) < nb ? __ldg(words + t * 32 + lane) : 0u;
-  for (; t < ntiles; t += nwarps) {
-    const int64_t tn = t + nwarps;
-    const uint32_t wn = (tn < ntiles && tn * 32 + lane < nb) ? __ldg(words + tn * 32 + lane) : 0u;
+  if (t < t_end) w = (t * 32 + lane) < nb ? __ldg(words + t * 32 + lane) : 0u;
+  for (; t < t_end; t += step) {
+    const int64_t tn = t + step;
+    const uint32_t wn = (tn < t_end && tn * 32 + lane < nb) ? __ldg(words + tn * 32 + lane) : 0u;
     const uint32_t c = __popc(w);
     const uint32_t incl = warp_incl_scan(c);
     const uint32_t total = __shfl_sync(kFull, incl, 31);
@@ -806,7 +854,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
         }
       }
       const uint32_t excl = incl - c;
-      const int64_t tbase = t ? __ldg(tile_incl + t - 1) : 0;
+      const int64_t tbase = cta_tot ? running : (t ? __ldg(tile_incl + t - 1) : 0);
       // each lane lists its block's set rows (ascending) as records
       {
         // bit-sliced (code length - 1) of the block's rows; lengths nest, so
@@ -885,9 +933,12 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
       }
       __syncwarp();
     }
+    running += total;
     w = wn;
   }
-  if (bad) *err = ~0ull;
+  if (bad) {
+    if (cta_tot) atomicMax(err, ~0ull); else *err = ~0ull;
+  }
 }
 
 // Row-id lookup + general decode; kVbsIds ids per thread in flight.
@@ -955,6 +1006,24 @@ __global__ void vbs_lookup_rows_dec_kernel(const __grid_constant__ VbsLookupDesc
 
 
 
+// Columns of at most this many 1024-row tiles take the one-kernel cooperative
+// fused lookup (bsb_tune "coop_tiles"; 0 = never).  Measured (B200, 1 % / 20 %
+// selections): 2^24 rows 34 -> 22 us / 49 -> 49 us (ByteSlice), 34 -> 27 / 80
+// -> 80 us (PP-VBS); 2^26 rows 59 -> 53 / 137 -> 133 and 86 -> 82 / 273 ->
+// 291 us: the launches it saves stop mattering and the contiguous tile runs
+// cost the dense PP-VBS case, hence 2^14 tiles.
+static int64_t g_coop_tiles = 1 << 14;
+void set_coop_tiles(int64_t v) { g_coop_tiles = v < 0 ? (1 << 14) : v; }
+static bool coop_lookup_ok(int64_t ntiles) {
+  static int supported = [] {
+    int dev = 0, ok = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    return ok;
+  }();
+  return supported && ntiles <= g_coop_tiles;
+}
+
 template <bool VBS>
 static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
                             const uint32_t* words, const bsb_decode* dec, uint64_t* oc,
@@ -962,23 +1031,30 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
   const int64_t n = VBS ? vcol->n_rows : bcol->n_rows;
   const int64_t nb = (n + 31) / 32;
   const int64_t ntiles = (nb + 31) / 32;
+  // Small selections' columns (<= kCoopTiles tiles): ONE cooperative kernel
+  // (the tile popcount / scan / copy launches cost more than the lookup).
+  const bool coop = coop_lookup_ok(ntiles);
+  const int64_t cta_cap = (int64_t)sm_count() * 32;
   int64_t* tc = nullptr;
-  BSB_CUDA(cudaMallocAsync(&tc, (ntiles * 2 + 4) * sizeof(int64_t), s));
-  int64_t* incl = tc + ntiles + 1;
-  unsigned long long* errw = reinterpret_cast<unsigned long long*>(incl + ntiles + 1);
-  const int grid = grid_for_l(ntiles * 32, 256);
-  tile_popc_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, tc);
-  BSB_LAUNCH_CHECK();
-  size_t tb = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tb, tc, incl, ntiles, s);
+  BSB_CUDA(cudaMallocAsync(&tc, (coop ? cta_cap + 4 : ntiles * 2 + 4) * sizeof(int64_t), s));
+  int64_t* incl = coop ? nullptr : tc + ntiles + 1;
+  unsigned long long* errw =
+      reinterpret_cast<unsigned long long*>(coop ? tc + cta_cap + 1 : incl + ntiles + 1);
   void* tmp = nullptr;
-  BSB_CUDA(cudaMallocAsync(&tmp, tb + 16, s));
-  cub::DeviceScan::InclusiveSum(tmp, tb, tc, incl, ntiles, s);
-  BSB_LAUNCH_CHECK();
-  if (n_out_dev)
-    BSB_CUDA(cudaMemcpyAsync(n_out_dev, incl + ntiles - 1, 8, cudaMemcpyDeviceToDevice, s));
-  else
-    BSB_CUDA(cudaMemsetAsync(errw, 0, 8, s));
+  if (!coop) {
+    const int grid = grid_for_l(ntiles * 32, 256);
+    tile_popc_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, tc);
+    BSB_LAUNCH_CHECK();
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, tc, incl, ntiles, s);
+    BSB_CUDA(cudaMallocAsync(&tmp, tb + 16, s));
+    cub::DeviceScan::InclusiveSum(tmp, tb, tc, incl, ntiles, s);
+    BSB_LAUNCH_CHECK();
+    if (n_out_dev)
+      BSB_CUDA(cudaMemcpyAsync(n_out_dev, incl + ntiles - 1, 8, cudaMemcpyDeviceToDevice, s));
+    else
+      BSB_CUDA(cudaMemsetAsync(errw, 0, 8, s));
+  }
   Decoder D;
   fill_decoder(D, dec);
   VbsLookupDesc vd;
@@ -994,10 +1070,24 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
     BSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBitsThreads, smem));
     const int bgrid = (int)std::min<int64_t>((ntiles + wpb - 1) / wpb,
                                              (int64_t)sm_count() * (per_sm < 1 ? 1 : per_sm));
+    unsigned long long* nout = n_out_dev ? reinterpret_cast<unsigned long long*>(n_out_dev) : errw;
+    if (coop) {
+      const uint8_t* a_sl = VBS ? nullptr : bcol->slices;
+      int64_t a_stride = VBS ? 0 : bcol->stride;
+      int a_k = VBS ? 0 : bcol->n_slices, a_w = VBS ? 0 : bcol->width_bits;
+      int64_t a_nb = nb, a_nt = ntiles;
+      const int64_t* a_incl = nullptr;
+      long long* a_cta = reinterpret_cast<long long*>(tc);
+      void* args[] = {&a_sl, &a_stride, &a_k, &a_w, &vd, &words, &a_nb, &a_nt, &a_incl,
+                      &D, &oc, &ov, &ov32, &nout, &a_cta};
+      BSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern),
+                                           dim3(bgrid < 1 ? 1 : bgrid), dim3(kBitsThreads), args,
+                                           (size_t)smem, s));
+      return BSB_OK;
+    }
     kern<<<bgrid < 1 ? 1 : bgrid, kBitsThreads, smem, s>>>(
         VBS ? nullptr : bcol->slices, VBS ? 0 : bcol->stride, VBS ? 0 : bcol->n_slices,
-        VBS ? 0 : bcol->width_bits, vd, words, nb, ntiles, incl, D, oc, ov, ov32,
-        n_out_dev ? reinterpret_cast<unsigned long long*>(n_out_dev) : errw);
+        VBS ? 0 : bcol->width_bits, vd, words, nb, ntiles, incl, D, oc, ov, ov32, nout, nullptr);
     BSB_LAUNCH_CHECK();
     return BSB_OK;
   };
@@ -1035,16 +1125,16 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
     }
   }
   if (rc != BSB_OK) return rc;
-  BSB_CUDA(cudaFreeAsync(tmp, s));
+  if (tmp) BSB_CUDA(cudaFreeAsync(tmp, s));
   if (n_out_dev || D.kind == 0) {
     BSB_CUDA(cudaFreeAsync(tc, s));
     return BSB_OK;
   }
-  unsigned long long h = 0;
+  unsigned long long h = 0;  // cooperative form: the count, or ~0 after a bad code
   BSB_CUDA(cudaMemcpyAsync(&h, errw, 8, cudaMemcpyDeviceToHost, s));
   BSB_CUDA(cudaFreeAsync(tc, s));
   BSB_CUDA(cudaStreamSynchronize(s));
-  if (h) {
+  if (coop ? h == ~0ull : h != 0) {
     set_error_msg("code not in dictionary");
     return BSB_ENOTFOUND;
   }

@@ -831,6 +831,7 @@ void set_scan_nomemset(int64_t v); // bsb_scan.cu
 void set_bs_small(int64_t v);      // bsb_scan.cu
 void set_pdl(int64_t v);           // bsb_scan.cu
 void set_pair_bits(int64_t v);     // bsb_gather.cu
+void set_coop_tiles(int64_t v);    // bsb_lookup.cu
 void set_dense_rows(int64_t v);    // bsb_lookup.cu
 }
 
@@ -862,6 +863,10 @@ extern "C" int bsb_tune(const char* key, int64_t value) {
   }
   if (std::strcmp(key, "dense_rows") == 0) {  // fused PP-VBS lookup: L1-allocating deep loads from
     bsb::set_dense_rows(value);               // this many selected rows per tile
+    return BSB_OK;
+  }
+  if (std::strcmp(key, "coop_tiles") == 0) {  // one-kernel fused lookup up to this many tiles
+    bsb::set_coop_tiles(value);
     return BSB_OK;
   }
   if (std::strcmp(key, "pair_bits") == 0) {  // row buckets of bsb_rows_bucket (2^bits)

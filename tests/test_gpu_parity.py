@@ -622,8 +622,19 @@ def _sel_cases(n, rng):
     yield f
 
 
+@pytest.fixture(params=["one_kernel", "popcount_scan"])
+def fused_lookup_form(request):
+    """Small columns take the one-kernel cooperative fused lookup; coop_tiles =
+    0 forces the tile popcount + scan + lookup sequence of big columns."""
+    from paper_2209_00220_b200 import _lib
+    lib = _lib.load()
+    lib.bsb_tune(b"coop_tiles", 0 if request.param == "popcount_scan" else -1)
+    yield request.param
+    lib.bsb_tune(b"coop_tiles", -1)
+
+
 @pytest.mark.parametrize("mode", ["packed", "sliced"])
-def test_vbs_fused_bits_lookup_and_tree_decode(mode):
+def test_vbs_fused_bits_lookup_and_tree_decode(mode, fused_lookup_form):
     """bsb_vbs_lookup_bits (bitvector -> codes / values in one kernel) and
     the PPE tree decoder equal the oracle's lookup + the row values."""
     n = 150_001
@@ -685,7 +696,7 @@ def test_tree_decoder_equals_binary_search_decoder():
         assert np.array_equal(v3, vals) and np.array_equal(v2, vals)
 
 
-def test_byteslice_fused_bits_lookup():
+def test_byteslice_fused_bits_lookup(fused_lookup_form):
     rng = np.random.default_rng(12)
     for n, w in ((70_001, 13), (4096, 24), (33, 40)):
         codes = rng.integers(0, 1 << min(w, 62), n, dtype=np.int64).astype(np.uint64)
@@ -707,7 +718,7 @@ def test_byteslice_fused_bits_lookup():
     assert np.array_equal(v, vals[flags])
 
 
-def test_vbs_errors():
+def test_vbs_errors(fused_lookup_form):
     col = B.build_vbs([1, 2], [1, 1])
     with pytest.raises(ValueError):
         B.scan_vbs(col, ResolvedPredicate.compare(Op.EQ, 0x0101, 2))
