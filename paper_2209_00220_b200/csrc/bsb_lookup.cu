@@ -737,7 +737,7 @@ __device__ __forceinline__ void sts256(uint8_t* dst, const uint32_t (&v)[8]) {
   d[1] = make_uint4(v[4], v[5], v[6], v[7]);
 }
 
-template <bool VBS, int DK, int MODE, int KT>
+template <bool VBS, int DK, int MODE, int KT, bool COOP = false>
 __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     const uint8_t* __restrict__ slices, int64_t stride, int K, int width,  // ByteSlice
     const __grid_constant__ VbsLookupDesc vd,                              // PP-VBS
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   // totals across one grid barrier, and the running position is carried
   // through the run -- the whole fused lookup is one kernel.
   int64_t t = warp, t_end = ntiles, step = nwarps, running = 0;
-  if (cta_tot) {
+  if (COOP) {
     const int wq = threadIdx.x >> 5;
     const int64_t per_warp = (ntiles + nwarps - 1) / nwarps;
     t = warp * per_warp;
@@ -812,6 +812,10 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
     __syncthreads();
     running = s_wtot[kBitsThreads / 32];
     for (int q = 0; q < wq; ++q) running += s_wtot[q];
+  }
+  if (!COOP) {  // the compiler keeps ntiles / nwarps, no extra registers
+    t_end = ntiles;
+    step = nwarps;
   }
   uint32_t w = 0;
   if (t < t_end) w = (t * 32 + lane) < nb ? __ldg(words + t * 32 + lane) : 0u;
@@ -854,7 +858,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
         }
       }
       const uint32_t excl = incl - c;
-      const int64_t tbase = cta_tot ? running : (t ? __ldg(tile_incl + t - 1) : 0);
+      const int64_t tbase = COOP ? running : (t ? __ldg(tile_incl + t - 1) : 0);
       // each lane lists its block's set rows (ascending) as records
       {
         // bit-sliced (code length - 1) of the block's rows; lengths nest, so
@@ -933,11 +937,11 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
       }
       __syncwarp();
     }
-    running += total;
+    if (COOP) running += total;
     w = wn;
   }
   if (bad) {
-    if (cta_tot) atomicMax(err, ~0ull); else *err = ~0ull;
+    if (COOP) atomicMax(err, ~0ull); else *err = ~0ull;
   }
 }
 
@@ -1063,7 +1067,7 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
   const int wpb = kBitsThreads / 32;
   const int smem = wpb * bits_stage_bytes(VBS, VBS ? vcol->max_len : bcol->n_slices) +
                    (D.kind == 3 ? 2048 : 0);
-  auto launch = [&](auto kern) -> int {
+  auto launch1 = [&](auto kern) -> int {
     if (smem > 48 * 1024)
       BSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
@@ -1091,30 +1095,31 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
     BSB_LAUNCH_CHECK();
     return BSB_OK;
   };
+#define BSB_LB(...) \
+  (coop ? launch1(lookup_bits_kernel<__VA_ARGS__, true>) : launch1(lookup_bits_kernel<__VA_ARGS__, false>))
   int rc;
   if (!VBS) {
-    rc = D.kind == 1 ? launch(lookup_bits_kernel<VBS, 1, 0, 0>)
-                     : launch(lookup_bits_kernel<VBS, 0, 0, 0>);
+    rc = D.kind == 1 ? BSB_LB(VBS, 1, 0, 0) : BSB_LB(VBS, 0, 0, 0);
   } else {
     // SLICED (the default deep layout) gets the code length as a template
     // argument; the other layouts take it at run time.
     auto sliced_k = [&](auto dk) -> int {
       constexpr int DKC = decltype(dk)::value;
       switch (vcol->max_len) {
-        case 2: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 2>);
-        case 3: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 3>);
-        case 4: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 4>);
-        case 5: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 5>);
-        case 6: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 6>);
-        case 7: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 7>);
-        case 8: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 8>);
-        default: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_SLICED, 0>);
+        case 2: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 2);
+        case 3: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 3);
+        case 4: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 4);
+        case 5: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 5);
+        case 6: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 6);
+        case 7: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 7);
+        case 8: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 8);
+        default: return BSB_LB(VBS, DKC, BSB_DEEP_SLICED, 0);
       }
     };
     auto by_mode = [&](auto dk) -> int {
       constexpr int DKC = decltype(dk)::value;
       switch (vcol->deep_mode) {
-        case BSB_DEEP_PACKED: return launch(lookup_bits_kernel<VBS, DKC, BSB_DEEP_PACKED, 0>);
+        case BSB_DEEP_PACKED: return BSB_LB(VBS, DKC, BSB_DEEP_PACKED, 0);
         default: return sliced_k(dk);
       }
     };
@@ -1124,6 +1129,7 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
       default: rc = by_mode(std::integral_constant<int, 3>()); break;
     }
   }
+#undef BSB_LB
   if (rc != BSB_OK) return rc;
   if (tmp) BSB_CUDA(cudaFreeAsync(tmp, s));
   if (n_out_dev || D.kind == 0) {
