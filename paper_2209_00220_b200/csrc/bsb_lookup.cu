@@ -249,8 +249,88 @@ __global__ void vbs_lookup_kernel(const __grid_constant__ VbsLookupDesc d,
 }
 
 // --- bitvector -> ascending row ids (bitvector.py:71-72) ---------------------
+// Both kernels take a SUPER-TILE of 4 tiles (128 words, 4096 rows) per warp
+// iteration, lane l holding the 4 consecutive words 4l .. 4l+3 from one
+// 16-byte load, two super-tiles' loads in flight per iteration: with one
+// 4-byte load per lane and iteration (the first form) the 64 MB of a 2^29-row
+// selection took 27 + 69 us -- ~0.8 TB/s, all load latency -- inside every
+// cfg5 step.
+__device__ __forceinline__ uint4 sel_words4(const uint32_t* __restrict__ words, int64_t w0,
+                                            int64_t nb) {
+  if (w0 + 4 <= nb) return __ldg(reinterpret_cast<const uint4*>(words + w0));
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);  // the column's last words
+  if (w0 < nb) v.x = __ldg(words + w0);
+  if (w0 + 1 < nb) v.y = __ldg(words + w0 + 1);
+  if (w0 + 2 < nb) v.z = __ldg(words + w0 + 2);
+  return v;
+}
+
+// tile_counts[t] = set bits of tile t.  words must be 16-byte aligned.
 __global__ void tile_popc_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
                                  int64_t* __restrict__ tile_counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nsuper = (ntiles + 3) >> 2;
+  for (int64_t s0 = warp * 2; s0 < nsuper; s0 += nwarps * 2) {
+    uint4 v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) v[u] = sel_words4(words, (s0 + u) * 128 + lane * 4, nb);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      // a tile = 8 consecutive lanes (32 words): sum inside each group of 8
+      unsigned c = __popc(v[u].x) + __popc(v[u].y) + __popc(v[u].z) + __popc(v[u].w);
+      c += __shfl_xor_sync(kFull, c, 1);
+      c += __shfl_xor_sync(kFull, c, 2);
+      c += __shfl_xor_sync(kFull, c, 4);
+      const int64_t t = (s0 + u) * 4 + (lane >> 3);
+      if ((lane & 7) == 0 && t < ntiles) tile_counts[t] = c;
+    }
+  }
+}
+
+__global__ void tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
+                                 const int64_t* __restrict__ tile_incl, int64_t row_offset,
+                                 const int64_t* __restrict__ base_dev,
+                                 int64_t* __restrict__ rows_out) {
+  if (base_dev) rows_out += __ldg(base_dev);  // compaction into a shared id array
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nsuper = (ntiles + 3) >> 2;
+  for (int64_t s0 = warp * 2; s0 < nsuper; s0 += nwarps * 2) {
+    uint4 v[2];
+    int64_t before[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      v[u] = sel_words4(words, (s0 + u) * 128 + lane * 4, nb);
+      const int64_t t0 = (s0 + u) * 4;  // selected rows before the super-tile
+      before[u] = (t0 > 0 && t0 <= ntiles) ? __ldg(tile_incl + t0 - 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t wq[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      const uint32_t c = __popc(wq[0]) + __popc(wq[1]) + __popc(wq[2]) + __popc(wq[3]);
+      if (!__any_sync(kFull, c != 0)) continue;
+      const uint32_t incl = warp_incl_scan(c);
+      int64_t pos = before[u] + (incl - c);
+      const int64_t b0 = (s0 + u) * 128 + lane * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t w = wq[q];
+        while (w) {
+          const int bit = __ffs(w) - 1;
+          w &= w - 1;
+          rows_out[pos++] = row_offset + (b0 + q) * 32 + bit;
+        }
+      }
+    }
+  }
+}
+
+// the first forms (any alignment of words): one word per lane and iteration
+__global__ void tile_popc1_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
+                                  int64_t* __restrict__ tile_counts) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -262,11 +342,11 @@ __global__ void tile_popc_kernel(const uint32_t* __restrict__ words, int64_t nb,
   }
 }
 
-__global__ void tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
-                                 const int64_t* __restrict__ tile_incl, int64_t row_offset,
-                                 const int64_t* __restrict__ base_dev,
-                                 int64_t* __restrict__ rows_out) {
-  if (base_dev) rows_out += __ldg(base_dev);  // compaction into a shared id array
+__global__ void tile_emit1_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
+                                  const int64_t* __restrict__ tile_incl, int64_t row_offset,
+                                  const int64_t* __restrict__ base_dev,
+                                  int64_t* __restrict__ rows_out) {
+  if (base_dev) rows_out += __ldg(base_dev);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -282,6 +362,17 @@ __global__ void tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb,
       w &= w - 1;
       rows_out[pos++] = row_offset + b * 32 + bit;
     }
+  }
+}
+
+// tile counts of a selection (either form, by the alignment of words)
+static void launch_tile_popc(const uint32_t* words, int64_t nb, int64_t ntiles, int64_t* tc,
+                             cudaStream_t s) {
+  if ((reinterpret_cast<uintptr_t>(words) & 15u) == 0) {
+    const int64_t nsuper = (ntiles + 3) / 4;
+    tile_popc_kernel<<<grid_for_l((nsuper + 1) / 2 * 32, 256), 256, 0, s>>>(words, nb, ntiles, tc);
+  } else {
+    tile_popc1_kernel<<<grid_for_l(ntiles * 32, 256), 256, 0, s>>>(words, nb, ntiles, tc);
   }
 }
 
@@ -321,8 +412,7 @@ static int bits_to_rows_impl(const uint32_t* words, int64_t n_rows, int64_t row_
   int64_t* tc = nullptr;
   BSB_CUDA(cudaMallocAsync(&tc, (ntiles * 2 + 2) * sizeof(int64_t), s));
   int64_t* incl = tc + ntiles + 1;
-  const int grid = grid_for_l(ntiles * 32, 256);
-  tile_popc_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, tc);
+  launch_tile_popc(words, nb, ntiles, tc, s);
   BSB_LAUNCH_CHECK();
   size_t tmp_bytes = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, tc, incl, ntiles, s);
@@ -331,8 +421,14 @@ static int bits_to_rows_impl(const uint32_t* words, int64_t n_rows, int64_t row_
   cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, tc, incl, ntiles, s);
   BSB_LAUNCH_CHECK();
   if (rows_out) {
-    tile_emit_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, incl, row_offset, base_dev,
-                                          rows_out);
+    if ((reinterpret_cast<uintptr_t>(words) & 15u) == 0) {
+      const int64_t nsuper = (ntiles + 3) / 4;
+      tile_emit_kernel<<<grid_for_l((nsuper + 1) / 2 * 32, 256), 256, 0, s>>>(
+          words, nb, ntiles, incl, row_offset, base_dev, rows_out);
+    } else {
+      tile_emit1_kernel<<<grid_for_l(ntiles * 32, 256), 256, 0, s>>>(
+          words, nb, ntiles, incl, row_offset, base_dev, rows_out);
+    }
     BSB_LAUNCH_CHECK();
   }
   if (n_out_dev)
@@ -1046,8 +1142,7 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
       reinterpret_cast<unsigned long long*>(coop ? tc + cta_cap + 1 : incl + ntiles + 1);
   void* tmp = nullptr;
   if (!coop) {
-    const int grid = grid_for_l(ntiles * 32, 256);
-    tile_popc_kernel<<<grid, 256, 0, s>>>(words, nb, ntiles, tc);
+    launch_tile_popc(words, nb, ntiles, tc, s);
     BSB_LAUNCH_CHECK();
     size_t tb = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tb, tc, incl, ntiles, s);
