@@ -339,6 +339,35 @@ def test_row_lookups_bucket_pairs(n):
         assert int(err.item()) & _lib.ERR_INDEX
 
 
+def test_rows_bucket_edge_sizes():
+    """bsb_rows_bucket at the edges: one id, chunk-size boundaries, a one-row
+    column, bucket counts of 2 .. 2^13, an id list that is only 8-byte aligned
+    (the first pass then loads its chunks without the bulk copy), all ids in
+    one bucket, and ascending lists forced through the pairs."""
+    rng = np.random.default_rng(77)
+    cases = [(1, 1), (1, 5), (33, 1), (33, 4095), (1024, 4096), (1025, 4097), (5000, 8193),
+             (1 << 17, 12_289), (1 << 21, 40_001), ((1 << 23) + 3, 70_001)]
+    for n, m in cases:
+        codes = rng.integers(0, 1 << 16, size=n, dtype=np.uint64)
+        col = B.build_byteslice(codes, 16)
+        for kind in ("random", "one_bucket", "ascending", "unaligned"):
+            if kind == "one_bucket":
+                ids = rng.integers(0, min(n, 700), size=m)
+            elif kind == "ascending":
+                ids = np.sort(rng.integers(0, n, size=m))
+            else:
+                ids = rng.integers(0, n, size=m)
+            if kind == "unaligned":
+                buf = torch.empty(m + 1, dtype=torch.int64, device="cuda")
+                t = buf[1:]
+                t.copy_(torch.from_numpy(ids))
+                assert t.data_ptr() % 16 == 8
+            else:
+                t = torch.from_numpy(ids).cuda()
+            got = B.lookup_byteslice_rows(col, t, order="bucket").cpu().numpy()
+            assert np.array_equal(got.view(np.uint64), codes[ids]), (n, m, kind)
+
+
 def test_row_lookup_auto_is_graph_capturable():
     """The _auto row-id lookup (order verdict on the device, both gathers
     gated on it, no host synchronisation with an error word) captured once as
