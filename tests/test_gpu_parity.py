@@ -339,6 +339,37 @@ def test_row_lookups_bucket_pairs(n):
         assert int(err.item()) & _lib.ERR_INDEX
 
 
+def test_bits_to_rows_any_alignment_and_size():
+    """Bitvector -> ascending row ids over 16-byte aligned words (super-tiles
+    of 4 tiles, 16-byte loads) and over words at a 4-byte offset (the
+    one-word-per-lane form), ragged sizes around the 4096-row super-tile, with
+    a row offset; and the fused lookup over the same selections."""
+    from paper_2209_00220_b200 import _lib
+    from paper_2209_00220_b200.device import stream
+    lib = _lib.load()
+    rng = np.random.default_rng(5)
+    for n in (1, 31, 1024, 4095, 4096, 4097, 8192 + 33, 1_000_003):
+        for p in (0.0, 0.02, 0.5, 1.0):
+            flags = rng.random(n) < p
+            want = np.flatnonzero(flags) + 1000
+            words = np.zeros((n + 31) // 32 + 1, np.uint32)
+            words[1:] = O.bools_to_words(flags)
+            buf = torch.from_numpy(words.view(np.int32)).cuda()
+            for off in (0, 1):  # off = 1: the data as given, at a 4-byte offset
+                if off == 0:
+                    w = buf[1:].clone()
+                    assert w.data_ptr() % 16 == 0
+                else:
+                    w = buf[1:]
+                    assert w.data_ptr() % 16 == 4
+                out = torch.empty(max(len(want), 1), dtype=torch.int64, device="cuda")
+                cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+                _lib.check(lib.bsb_bits_to_rows_async(w.data_ptr(), n, 1000, out.data_ptr(),
+                                                      cnt.data_ptr(), stream()), "bits_to_rows")
+                assert int(cnt.item()) == len(want), (n, p, off)
+                assert np.array_equal(out[:len(want)].cpu().numpy(), want), (n, p, off)
+
+
 def test_rows_bucket_edge_sizes():
     """bsb_rows_bucket at the edges: one id, chunk-size boundaries, a one-row
     column, bucket counts of 2 .. 2^13, an id list that is only 8-byte aligned
