@@ -170,8 +170,12 @@ __device__ __forceinline__ bool ds_level(const DsArgs& a, int j, int64_t dbk, co
 // and the mask is AND-ed into the result words in phase 3 -- the same words
 // (AND is idempotent).  With a gate, EPI runs when the mask's row count is
 // above gate_max and the compacted vbs_dsm_kernel otherwise.
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool EPI = false>
+// LM: the shallow (1-byte-code) rows' result -- 0: none matches, 1: compared
+// against the first-slice bytes (the "L1" code paths), 2: every one matches;
+// 0 and 2 read no first-slice byte (constants of the literals).
+template <bool BETWEEN, int LM, int ST, bool UNR, bool EPI = false>
 __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_constant__ DsArgs a) {
+  constexpr bool L1 = LM == 1;
   if (EPI && a.gate && *a.gate <= a.gate_max) return;
   constexpr int kRd = ST * 32 + 8;  // deep blocks touched by a super-tile (+ guard)
   __shared__ uint32_t rd_all[kDsWarps][kRd];
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kDsThreads, 4) vbs_ds_kernel(const __grid_cons
       const uint32_t m2 = m2P[u];
       uint32_t valid =
           tile < a.full_tiles ? kFull : (tile < a.ntiles ? tail_valid(b, a.n_rows) : 0u);
-      uint32_t res = 0;
+      uint32_t res = LM == 2 ? (valid & ~m2) : 0u;
       if (L1) {
         uint32_t w[8];
 #pragma unroll
@@ -394,8 +398,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //   * each lane writes its R result words (zeros where the mask empties a
 //     block; the same words as scanning whole and AND-ing the mask).
 // Instructions and sectors scale with the masked-in blocks, not the column.
-template <bool BETWEEN, bool L1, int R, int WARPS, int MINB, int STAGE>
+template <bool BETWEEN, int LM, int R, int WARPS, int MINB, int STAGE>
 __global__ void __launch_bounds__(WARPS * 32, MINB) vbs_dsm_kernel(const __grid_constant__ DsArgs a) {
+  constexpr bool L1 = LM == 1;
   if (a.gate && *a.gate > a.gate_max) return;
   static_assert(R == 4 || R == 8, "R row blocks per lane: 4 or 8");
   constexpr int NB = R * 32;    // row blocks per super-tile
@@ -497,7 +502,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) vbs_dsm_kernel(const __grid_
       for (int q = 0; q < R; q += 4) {
         *reinterpret_cast<uint4*>(&S.m2[lane * R + q]) = make_uint4(m[q], m[q + 1], m[q + 2], m[q + 3]);
         *reinterpret_cast<uint4*>(&S.vw[lane * R + q]) = make_uint4(v[q], v[q + 1], v[q + 2], v[q + 3]);
-        *reinterpret_cast<uint4*>(&S.res[lane * R + q]) = make_uint4(0u, 0u, 0u, 0u);
+        // shallow rows: compared in phase 1 (LM 1), else a constant of the literals
+        *reinterpret_cast<uint4*>(&S.res[lane * R + q]) =
+            LM == 2 ? make_uint4(v[q] & ~m[q], v[q + 1] & ~m[q + 1], v[q + 2] & ~m[q + 2],
+                                 v[q + 3] & ~m[q + 3])
+                    : make_uint4(0u, 0u, 0u, 0u);
         *reinterpret_cast<uint2*>(&S.offs[lane * R + q]) =
             make_uint2((uint32_t)o16[q] | ((uint32_t)o16[q + 1] << 16),
                        (uint32_t)o16[q + 2] | ((uint32_t)o16[q + 3] << 16));
@@ -630,9 +639,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) vbs_dsm_kernel(const __grid_
   if (lane == 0 && cnt) atomicAdd(a.count, cnt);
 }
 
-template <bool BETWEEN, bool L1, int R, int WARPS, int MINB, int STAGE>
+template <bool BETWEEN, int LM, int R, int WARPS, int MINB, int STAGE>
 static int launch_dsm_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_dsm_kernel<BETWEEN, L1, R, WARPS, MINB, STAGE>;
+  auto kern = vbs_dsm_kernel<BETWEEN, LM, R, WARPS, MINB, STAGE>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, 0);
   if (per_sm < 1) per_sm = 1;
@@ -646,19 +655,19 @@ static int launch_dsm_k(const DsArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 static int tune(int i);
-template <bool BETWEEN, bool L1>
+template <bool BETWEEN, int LM>
 static int launch_dsm(const DsArgs& a, cudaStream_t s) {
   switch (tune(6)) {
-    case 1: return launch_dsm_k<BETWEEN, L1, 4, 8, 6, 16>(a, s);
-    case 2: return launch_dsm_k<BETWEEN, L1, 8, 4, 6, 32>(a, s);
-    case 3: return launch_dsm_k<BETWEEN, L1, 8, 4, 4, 64>(a, s);
-    default: return launch_dsm_k<BETWEEN, L1, 4, 8, 4, 32>(a, s);
+    case 1: return launch_dsm_k<BETWEEN, LM, 4, 8, 6, 16>(a, s);
+    case 2: return launch_dsm_k<BETWEEN, LM, 8, 4, 6, 32>(a, s);
+    case 3: return launch_dsm_k<BETWEEN, LM, 8, 4, 4, 64>(a, s);
+    default: return launch_dsm_k<BETWEEN, LM, 4, 8, 4, 32>(a, s);
   }
 }
 
-template <bool BETWEEN, bool L1, int ST, bool UNR, bool EPI = false>
+template <bool BETWEEN, int LM, int ST, bool UNR, bool EPI = false>
 static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
-  auto kern = vbs_ds_kernel<BETWEEN, L1, ST, UNR, EPI>;
+  auto kern = vbs_ds_kernel<BETWEEN, LM, ST, UNR, EPI>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDsThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -672,28 +681,28 @@ static int launch_ds_k(const DsArgs& a, cudaStream_t s) {
   return BSB_OK;
 }
 
-template <bool BETWEEN, bool L1, bool UNR>
+template <bool BETWEEN, int LM, bool UNR>
 static int launch_ds_u(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
-    case 1: return launch_ds_k<BETWEEN, L1, 1, UNR>(a, s);
-    case 2: return launch_ds_k<BETWEEN, L1, 2, UNR>(a, s);
-    case 3: return launch_ds_k<BETWEEN, L1, 3, UNR>(a, s);
-    default: return launch_ds_k<BETWEEN, L1, 4, UNR>(a, s);
+    case 1: return launch_ds_k<BETWEEN, LM, 1, UNR>(a, s);
+    case 2: return launch_ds_k<BETWEEN, LM, 2, UNR>(a, s);
+    case 3: return launch_ds_k<BETWEEN, LM, 3, UNR>(a, s);
+    default: return launch_ds_k<BETWEEN, LM, 4, UNR>(a, s);
   }
 }
-template <bool BETWEEN, bool L1>
+template <bool BETWEEN, int LM>
 static int launch_ds_epi(const DsArgs& a, int st, cudaStream_t s) {
   switch (st) {
-    case 1: return launch_ds_k<BETWEEN, L1, 1, true, true>(a, s);
-    case 2: return launch_ds_k<BETWEEN, L1, 2, true, true>(a, s);
-    case 3: return launch_ds_k<BETWEEN, L1, 3, true, true>(a, s);
-    default: return launch_ds_k<BETWEEN, L1, 4, true, true>(a, s);
+    case 1: return launch_ds_k<BETWEEN, LM, 1, true, true>(a, s);
+    case 2: return launch_ds_k<BETWEEN, LM, 2, true, true>(a, s);
+    case 3: return launch_ds_k<BETWEEN, LM, 3, true, true>(a, s);
+    default: return launch_ds_k<BETWEEN, LM, 4, true, true>(a, s);
   }
 }
-template <bool BETWEEN, bool L1>
+template <bool BETWEEN, int LM>
 static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
   if (!a.mask)
-    return unr ? launch_ds_u<BETWEEN, L1, true>(a, st, s) : launch_ds_u<BETWEEN, L1, false>(a, st, s);
+    return unr ? launch_ds_u<BETWEEN, LM, true>(a, st, s) : launch_ds_u<BETWEEN, LM, false>(a, st, s);
   // Masked: the compacted kernel and EPI behind the gate (the mask's row
   // count vs gate_max; each exits at once when the other applies), or EPI
   // alone when there is no gate, the gate is off (gate_max 0), bsb_tune
@@ -703,10 +712,10 @@ static int launch_ds(const DsArgs& a, int st, bool unr, cudaStream_t s) {
   if (!a.gate || a.gate_max == 0 || tune(5) != 0 || !al16) {
     DsArgs e = a;
     e.gate = nullptr;
-    return launch_ds_epi<BETWEEN, L1>(e, st, s);
+    return launch_ds_epi<BETWEEN, LM>(e, st, s);
   }
-  const int rc = launch_dsm<BETWEEN, L1>(a, s);
-  return rc ? rc : launch_ds_epi<BETWEEN, L1>(a, st, s);
+  const int rc = launch_dsm<BETWEEN, LM>(a, s);
+  return rc ? rc : launch_ds_epi<BETWEEN, LM>(a, st, s);
 }
 
 // Run-time tunables (bsb_tune): 0 enable (0 off, 1 all scans, 2 unmasked
@@ -813,11 +822,33 @@ int vbs_ds_scan(const VbsDesc& d, int64_t n_rows, int64_t stride, int64_t deep_r
   a.tQ = make_plane_thr(tQ);
   a.twoQ = tQ < 256;
   a.inv = inv;
-  const bool l1 = inv != 0 || (tP < 256 && tP < tQ);  // else no shallow row can match
+  // The shallow result ([byte >= tP] & ~[byte >= tQ]) ^ inv is a constant of
+  // the literals when neither threshold can split a byte (tP, tQ outside
+  // 1..255) or the window is empty: then no first-slice byte is read.  E.g.
+  // LE / LT with a literal whose first byte is 255 (a value right of every
+  // first-level slot: all of a Zipf column's long codes) matches every
+  // 1-byte-code row; GE / GT / BETWEEN from such a value match none.
+  const bool p_var = tP >= 1 && tP <= 255, q_var = tQ >= 1 && tQ <= 255;
+  int lm = 1;
+  if (!p_var && !q_var) {
+    const bool pq = tP <= 0 && tQ >= 256;  // P always, Q never
+    lm = (((pq ? kFull : 0u) ^ inv) != 0u) ? 2 : 0;
+  } else if (!inv && tP >= tQ) {  // empty window
+    lm = 0;
+  }
   if (!gate) BSB_CUDA(cudaMemsetAsync(count, 0, 8, s));  // gated: zeroed by the caller
-  if (between)
-    return l1 ? launch_ds<true, true>(a, st, unr, s) : launch_ds<true, false>(a, st, unr, s);
-  return l1 ? launch_ds<false, true>(a, st, unr, s) : launch_ds<false, false>(a, st, unr, s);
+  if (between) {
+    switch (lm) {
+      case 0: return launch_ds<true, 0>(a, st, unr, s);
+      case 2: return launch_ds<true, 2>(a, st, unr, s);
+      default: return launch_ds<true, 1>(a, st, unr, s);
+    }
+  }
+  switch (lm) {
+    case 0: return launch_ds<false, 0>(a, st, unr, s);
+    case 2: return launch_ds<false, 2>(a, st, unr, s);
+    default: return launch_ds<false, 1>(a, st, unr, s);
+  }
 }
 
 }  // namespace bsb

@@ -504,6 +504,57 @@ def test_vbs_zipf_between_windows_vs_oracle(mode):
                               O.naive_filter(vals, "BETWEEN", q(1 - p - mm), q(1 - mm)))
 
 
+def test_vbs_shallow_rows_settled_by_the_literal():
+    """SLICED deep-space scans read no first-slice byte when the literals
+    alone settle every 1-byte-code row: a first byte of 255 (a value right of
+    every first-level slot: all long codes of a Zipf column) under LE / LT /
+    NE matches them all, under GE / GT / EQ / BETWEEN none, and a 1-byte 0 /
+    255 literal does the same from the other side.  Every operator, masked
+    (sparse and dense) and unmasked, against the oracle and the raw values."""
+    n = (1 << 18) + 777
+    vals, od, codes, lens = _ppe_column(1.1, 16, n, 3)
+    col = B.build_vbs(codes, lens, deep_mode="sliced")
+    ocol = O.vbs_build(codes, lens)
+    K = ocol.K
+    rng = np.random.default_rng(9)
+    first = (codes >> (np.uint64(8) * (lens.astype(np.uint64) - np.uint64(1)))) & np.uint64(0xFF)
+    right = np.unique(vals[(lens > 1) & (first == 255)])  # long codes right of every slot
+    other = np.unique(vals[(lens > 1) & (first != 255)])  # long codes in a gap between slots
+    assert len(right) > 100
+    lits = [int(right[0]), int(right[len(right) // 2]), int(right[-1]),
+            int(vals.min()), int(np.unique(vals[lens == 1]).max())]
+    lits += [int(other[len(other) // 2])] if len(other) else []
+    masks = [None, O.bools_to_words(rng.random(n) < 0.5), O.bools_to_words(rng.random(n) < 0.01)]
+    for v in lits:
+        for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+            opred = od.encode_literal(op, v)
+            for m_o in masks:
+                want, _ = O.vbs_scan(ocol, opred, m_o)
+                bv, _ = B.scan_vbs(col, rp(list(opred)),
+                                   None if m_o is None else B.ResultBitVector(n, m_o))
+                assert np.array_equal(bv.words, want), (v, op)
+            assert np.array_equal(O.words_to_bools(O.vbs_scan(ocol, opred)[0], n),
+                                  O.naive_filter(vals, op, v)), (v, op)
+    for lo, hi in ((lits[0], lits[1]), (lits[3], lits[2]), (lits[4], lits[1]), (lits[3], lits[4])):
+        opred = od.encode_literal("BETWEEN", lo, hi)
+        for m_o in masks:
+            want, _ = O.vbs_scan(ocol, opred, m_o)
+            bv, _ = B.scan_vbs(col, rp(list(opred)),
+                               None if m_o is None else B.ResultBitVector(n, m_o))
+            assert np.array_equal(bv.words, want), (lo, hi)
+    # raw code-space literals: 1-byte 0x00 / 0xFF and a 2-byte 0xFF.. literal
+    for lit, ll in ((0, 1), (255, 1), (0xFF00, 2), (0xFFFF, 2)):
+        if ll > K:
+            continue
+        for op in ("EQ", "NE", "LT", "LE", "GT", "GE"):
+            p = O.pred_compare(op, lit, ll)
+            for m_o in masks[:2]:
+                want, _ = O.vbs_scan(ocol, p, m_o)
+                bv, _ = B.scan_vbs(col, rp(list(p)),
+                                   None if m_o is None else B.ResultBitVector(n, m_o))
+                assert np.array_equal(bv.words, want), (lit, ll, op)
+
+
 @pytest.mark.parametrize("mode", ["packed", "sliced"])
 def test_vbs_random_codes_all_ops_masks_vs_oracle(mode):
     rng = np.random.default_rng(77)
