@@ -3,7 +3,9 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "bsb_scan_impl.cuh"
 
@@ -25,26 +27,42 @@ struct ScanArgs {
   int8_t* depth;
   int32_t skipped_slot;
   int32_t depth_max;  // STATS: 1 = depth[b] = max(depth[b], d) (second BETWEEN leg)
-  // bs_scan_small_kernel: count accumulator | arrivals << 48 of this call (count_slot());
+  // bs_scan_small_kernel: count accumulator | arrivals << 48 of the call's stream (count_slot());
   // the last CTA stores the total into *count, so no memset node precedes
   // the kernel
   unsigned long long* slot;
 };
 
-// Per-call count slots of the small-column scan: zero at load time, and the
-// kernel that used a slot leaves it zero again, so a call needs no memset.
-// A slot is reused only after kCountSlots later calls (a graph node keeps
-// its slot: replays of one graph are serialised by CUDA).
+// Count slots of the small-column scan: zero at load time, and the kernel
+// that used a slot leaves it zero again, so a call needs no memset.  A slot
+// belongs to one (stream, capture) pair for the life of the process: kernels
+// of one stream -- or of one branch of one captured graph -- never overlap
+// (the scan's epilogue comes after its griddepcontrol.wait), so no two
+// kernels ever hold a slot at once.  NULL when the arena is used up (the
+// caller then zeroes count with a memset as before).
 constexpr int kCountSlots = 1 << 16;
 __device__ unsigned long long g_count_slots[kCountSlots];
-static unsigned long long* count_slot() {
+static unsigned long long* count_slot(cudaStream_t s) {
   static unsigned long long* base = [] {
     void* p = nullptr;
     cudaGetSymbolAddress(&p, g_count_slots);
     return static_cast<unsigned long long*>(p);
   }();
-  static std::atomic<uint32_t> next{0};
-  return base ? base + (size_t)(next.fetch_add(1) % kCountSlots) : nullptr;
+  if (!base) return nullptr;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long cap = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &cap) != cudaSuccess) return nullptr;
+  if (st != cudaStreamCaptureStatusActive) cap = 0;
+  static std::mutex mu;
+  static std::map<std::pair<unsigned long long, cudaStream_t>, int> slots;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(cap, s);
+  auto it = slots.find(key);
+  if (it == slots.end()) {
+    if ((int)slots.size() >= kCountSlots) return nullptr;
+    it = slots.emplace(key, (int)slots.size()).first;
+  }
+  return base + it->second;
 }
 
 template <bool STATS>
@@ -692,7 +710,7 @@ static int scan_dispatch(ScanArgs& a, const bsb_pred* p, int levels, cudaStream_
   const bool between = p->op == BSB_BETWEEN;
   const bool stats = a.stats != nullptr;
   const bool small = !stats && LAYOUT == BSB_LAYOUT_BYTESLICE && !a.mask && small_bs_ok(a.ntiles);
-  if (small && a.count) a.slot = count_slot();
+  if (small && a.count) a.slot = count_slot(s);
   if (a.count && !a.slot && !g_scan_nomemset)
     BSB_CUDA(cudaMemsetAsync(a.count, 0, sizeof(uint64_t), s));
   if (!stats) {
