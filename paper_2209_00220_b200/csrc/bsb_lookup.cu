@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int shift = VBS ? 0 : 8 * K - width;
+  const int shift = VBS ? 0 : 8 * KL - width;
   bool bad = false;
   // Tile order.  cta_tot NULL: tiles round-robin over the warps, the selected
   // rows before a tile come from tile_incl (tile popcount + scan kernels).
@@ -947,7 +947,9 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
           }
         }
       } else if (w) {
-        for (int j = 0; j < K; ++j) {
+#pragma unroll
+        for (int j = 0; j < kMaxLevels; ++j) {
+          if (j >= KL) break;
           uint32_t v[8];
           ldg256_free(slices + j * stride + blk * 32, v);
           sts256(stage + j * 1024 + lane * 32, v);
@@ -1018,7 +1020,7 @@ __global__ void __launch_bounds__(kBitsThreads) lookup_bits_kernel(
             uint64_t cd = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLevels; ++j)
-              if (j < K) cd = (cd << 8) | bp_row_byte_smem(stage + j * 1024 + bl * 32, lr);
+              if (j < KL) cd = (cd << 8) | bp_row_byte_smem(stage + j * 1024 + bl * 32, lr);
             code[u] = pad[u] = cd >> shift;
             len[u] = 0;
           }
@@ -1194,7 +1196,18 @@ static int lookup_bits_impl(const bsb_byteslice* bcol, const bsb_vbs* vcol,
   (coop ? launch1(lookup_bits_kernel<__VA_ARGS__, true>) : launch1(lookup_bits_kernel<__VA_ARGS__, false>))
   int rc;
   if (!VBS) {
-    rc = D.kind == 1 ? BSB_LB(VBS, 1, 0, 0) : BSB_LB(VBS, 0, 0, 0);
+    // ByteSlice: the common slice counts as a template argument (no dead
+    // level iterations in the per-row assembly)
+    auto bs_k = [&](auto dk) -> int {
+      constexpr int DKC = decltype(dk)::value;
+      switch (bcol->n_slices) {
+        case 2: return BSB_LB(VBS, DKC, 0, 2);
+        case 3: return BSB_LB(VBS, DKC, 0, 3);
+        case 4: return BSB_LB(VBS, DKC, 0, 4);
+        default: return BSB_LB(VBS, DKC, 0, 0);
+      }
+    };
+    rc = D.kind == 1 ? bs_k(std::integral_constant<int, 1>()) : bs_k(std::integral_constant<int, 0>());
   } else {
     // SLICED (the default deep layout) gets the code length as a template
     // argument; the other layouts take it at run time.
