@@ -409,10 +409,13 @@ METRIC5 = ("scan Gcodes/s (cfg5: 4 columns x 2^32 rows row-range sharded; u0<q10
 KERNEL5 = {"u0": "bs_scan_kernel<LT> (ByteSlice w=32, bit-plane sectors)",
            "u1": "bs_scan_kernel<GE> (ByteSlice w=32, bit-plane sectors)",
            "z0": "vbs_ds_kernel<BETWEEN> (PP-VBS SLICED, deep-row space)",
-           "z1": "vbs_ds_kernel<LE> (PP-VBS SLICED, deep-row space)",
+           "z1": "vbs_ds_kernel<LE, LM=2> (PP-VBS SLICED, deep-row space; the 1-byte-code rows "
+                 "settled by the literal, no first-slice bytes read)",
            "and4": "bsb_conj_scan: bs_conj_kernel (u0 AND u1, TMA-staged, AND in registers) "
-                   "+ vbs_ds_kernel<EPI> z0 + vbs_ds_kernel<EPI> z1 (running mask AND-ed in "
-                   "the epilogue)"}
+                   "+ z0 leg + z1 leg, each vbs_dsm_kernel (work compacted to the masked-in "
+                   "blocks) when the running count is at most 6 % of the rows, else "
+                   "vbs_ds_kernel<EPI> (running mask AND-ed in the epilogue); both are "
+                   "launched, gated on the device-resident count"}
 
 
 def run_cfg5(args, world, rank, local):
