@@ -302,6 +302,10 @@ def test_row_lookups_bucket_pairs(n):
     padded = vcodes << (np.uint64(8) * (np.uint64(K) - lens.astype(np.uint64)))
     got = B.lookup_vbs_rows(vcol, t, order="bucket").cpu().numpy()
     assert np.array_equal(got.view(np.uint64), padded[ids])
+    if n < 100_000:  # the reference-packed deep layout through the pairs as well
+        pcol = B.build_vbs(vcodes, lens, deep_mode="packed")
+        got = B.lookup_vbs_rows(pcol, t, order="bucket").cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), padded[ids])
     d = B.Dictionary.build(B.build_frequency_table(vals, B.ColumnKind.NUMERIC),
                            "prefix_preserving")
     for order in ("bucket", "auto"):
