@@ -339,11 +339,15 @@ int bsb_vbs_lookup_pairs_dec(const bsb_vbs* col, const uint64_t* pairs, const in
                              uint64_t* out_padded, int64_t* out_values, int32_t* out_values32,
                              uint32_t* err_dev, void* stream);
 /* bsb_byteslice_lookup_rows / bsb_vbs_lookup_rows_dec with the locality
- * chosen on the device: the sampled order check, then the gather of rows[] as
- * given and the bucket partition + pair gather, each gated on the verdict
- * (the one that does not apply exits at once).  Same arguments, same output,
- * no host synchronisation beyond err_dev == NULL's.  Lists of fewer than 2
- * ids or sizes the 32-bit pairs cannot hold are gathered as given. */
+ * chosen from a sampled order check (4096 adjacent pairs): an ascending list
+ * is gathered as given, any other through the bucket partition + pair gather.
+ * Same arguments, same output.  On an idle, non-capturing stream the host
+ * reads the verdict from a mapped word (a poll of ~10 us, no stream
+ * synchronisation) and launches only the form that applies; otherwise both
+ * forms are launched, each gated on the device-resident verdict (the one that
+ * does not apply exits at once), so the call is graph-capturable and never
+ * waits for work queued earlier.  Lists of fewer than 2 ids or sizes the
+ * 32-bit pairs cannot hold are gathered as given. */
 int bsb_byteslice_lookup_rows_auto(const bsb_byteslice* col, const int64_t* rows, int64_t n_ids,
                                    uint64_t* out_codes, const int64_t* rank_values,
                                    int64_t* out_values, int32_t* out_values32,

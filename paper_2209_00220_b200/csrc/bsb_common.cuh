@@ -103,6 +103,11 @@ void rows_order_check_launch(const int64_t* rows, int64_t n_ids, uint32_t* unsor
                              cudaStream_t s);  // the kernel alone (word already zero)
 int rows_bucket_gated(const int64_t* rows, int64_t n_ids, int64_t n_rows, uint64_t* pairs,
                       const uint32_t* gate, cudaStream_t s);
+// The same check with the verdict read by the HOST from a mapped word (a poll
+// of a few microseconds, no stream synchronisation): 0 = looks ascending, 1 =
+// not, -1 = not taken (the stream is capturing or has work queued, or the
+// poll timed out) -- the caller then leaves the choice to the device.
+int rows_order_poll(const int64_t* rows, int64_t n_ids, cudaStream_t s);
 
 // Device-side gate of a kernel that is one of two alternatives chosen by a
 // device word (no host synchronisation, graph-capturable): the kernel runs

@@ -6,6 +6,8 @@
 // its sectors, and DRAM pages are visited in order); the looked-up values are
 // then scattered back to input order.  The host wrappers
 // (lookup_*_rows(order="auto")) use this for large unsorted lists.
+#include <atomic>
+#include <chrono>
 #include <cstring>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -378,6 +380,59 @@ extern "C" int bsb_rows_sort(const int64_t* rows, int64_t n_ids, int64_t n_rows,
 }
 
 namespace bsb {
+
+// One CTA: 4096 sampled adjacent pairs, verdict + 1 into a host-mapped word.
+__global__ void __launch_bounds__(1024)
+rows_sample_poll_kernel(const int64_t* __restrict__ rows, int64_t n,
+                        volatile uint32_t* __restrict__ flag) {
+  bool b = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t i = (n - 1) * (int64_t)(threadIdx.x + 1024 * q) / 4096;
+    b |= i + 1 < n && __ldg(rows + i + 1) < __ldg(rows + i);
+  }
+  const int any = __syncthreads_or(b);
+  if (threadIdx.x == 0) {
+    *flag = any ? 2u : 1u;
+    __threadfence_system();
+  }
+}
+
+int rows_order_poll(const int64_t* rows, int64_t n_ids, cudaStream_t s) {
+  constexpr int kSlots = 1024;
+  struct Ring {
+    volatile uint32_t* host = nullptr;
+    uint32_t* dev = nullptr;
+    Ring() {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, kSlots * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) return;
+      void* d = nullptr;
+      if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return;
+      host = static_cast<volatile uint32_t*>(h);
+      dev = static_cast<uint32_t*>(d);
+    }
+  };
+  static Ring ring;
+  static std::atomic<uint32_t> next{0};
+  if (!ring.dev || n_ids < 2) return -1;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+  // only on an idle stream: behind queued work the poll would wait for all of it
+  if (cudaStreamQuery(s) != cudaSuccess) {
+    cudaGetLastError();  // cudaErrorNotReady is not an error
+    return -1;
+  }
+  const uint32_t slot = next.fetch_add(1) % kSlots;
+  ring.host[slot] = 0u;
+  rows_sample_poll_kernel<<<1, 1024, 0, s>>>(rows, n_ids, ring.dev + slot);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const uint32_t v = ring.host[slot];
+    if (v) return (int)v - 1;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(500)) return -1;
+  }
+}
 
 void rows_order_check_launch(const int64_t* rows, int64_t n_ids, uint32_t* unsorted_dev,
                              cudaStream_t s) {
