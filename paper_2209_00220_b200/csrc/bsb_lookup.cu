@@ -292,7 +292,7 @@ __global__ void tile_popc_kernel(const uint32_t* __restrict__ words, int64_t nb,
   }
 }
 
-__global__ void tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
+__global__ void __launch_bounds__(256, 8) tile_emit_kernel(const uint32_t* __restrict__ words, int64_t nb, int64_t ntiles,
                                  const int64_t* __restrict__ tile_incl, int64_t row_offset,
                                  const int64_t* __restrict__ base_dev,
                                  int64_t* __restrict__ rows_out) {
