@@ -601,9 +601,12 @@ def run_cfg5(args, world, rank, local):
                     "dictionaries": round(tab.t_dict, 2), "layouts": round(tab.t_build, 2),
                     "parity": round(t_parity, 2), "alg_bytes": round(t_alg, 2)},
     }
-    # kernels of the rank's step: one per single scan, 4 per AND chain, 3 for
-    # each segment's compaction (tile popcount, CUB scan, emit)
-    out["gpu_launches"] = int(args.steps * S * (4 + 4 + 3))
+    # this library's kernels in the rank's step, per segment: one per single
+    # scan (4); the AND chain's fused ByteSlice pair + a compacted and an
+    # epilogue-masked kernel per PP-VBS leg, one of which exits at its gate (5);
+    # the compaction's tile popcount and emit (2; CUB's scan between them is
+    # not counted)
+    out["gpu_launches"] = int(args.steps * S * (4 + 5 + 2))
     if world == 1 and not args.profile and not args.no_extra:
         del graph, step, tab
         torch.cuda.synchronize()
